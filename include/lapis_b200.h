@@ -1,0 +1,151 @@
+/*
+ * lapis_b200.h — C ABI of the B200 (sm_100a) execution backend for the LAPIS
+ * hot path: CSR SpMV, CSR x dense SpMM, dense matmul / matvec /
+ * batch_matmul, and the parallel_reduce family.
+ *
+ * The reference (arXiv 2509.25605, /root/reference) executes these kernels as
+ * emitted Kokkos C++ on a serial stub; its "FFI" is the emitted C++ signature
+ * plus the runtime-header library seam.  Each entry below replaces one of
+ * those, cited as reference file:line.  Conventions:
+ *
+ *   - all buffer pointers are DEVICE pointers (the "unmanaged View" analogue)
+ *     in row-major LayoutRight (runtime_header.py:39-41); the caller owns them
+ *     and the library keeps none of them after return (plans excepted);
+ *   - outputs (y, Y, C) are overwritten, never accumulated (interp.py:812);
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
+ *     stream-ordered and asynchronous, nothing synchronises the device;
+ *   - return 0 on success, a LAPIS_B200_ERR_* code otherwise, with a
+ *     thread-local message in lapis_b200_last_error(); the host process is
+ *     never aborted (the reference stub calls exit(1),
+ *     lapis_serial_stub.hpp:29-32).
+ */
+#ifndef LAPIS_B200_H
+#define LAPIS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define LAPIS_B200_OK 0
+#define LAPIS_B200_ERR_ARG 1         /* bad argument (shape, pointer, dtype) */
+#define LAPIS_B200_ERR_CUDA 2        /* CUDA runtime / launch error */
+#define LAPIS_B200_ERR_UNSUPPORTED 3 /* dtype / mode combination not provided */
+#define LAPIS_B200_ERR_NOMEM 4       /* device allocation failed */
+
+/* element types: the reference's scalar kinds f32, f64, i32, i64/index
+ * (ir.py:23-92; index is 64-bit, emitter.py:39-42) */
+#define LAPIS_B200_F32 0
+#define LAPIS_B200_F64 1
+#define LAPIS_B200_I32 2
+#define LAPIS_B200_I64 3
+
+/* reduction combiners (dialect.py:128-154 classify_combiner; identities
+ * interp.py:186-195) */
+#define LAPIS_B200_ADD 0
+#define LAPIS_B200_MUL 1
+#define LAPIS_B200_MIN 2
+#define LAPIS_B200_MAX 3
+
+/* dense matmul precision modes (lapis_b200_gemm `mode`) */
+#define LAPIS_B200_GEMM_AUTO 0    /* f32 -> TF32X3, f64 -> DMMA, ints -> EXACT */
+#define LAPIS_B200_GEMM_TF32X3 1  /* f32: 3xTF32 split on tcgen05 (kind::tf32), TMEM accum */
+#define LAPIS_B200_GEMM_DMMA 2    /* f64: DMMA tensor cores */
+#define LAPIS_B200_GEMM_EXACT 3   /* reference order: sequential k, no FMA -> bit-exact */
+
+/* ----------------------------------------------------------------- library */
+const char* lapis_b200_last_error(void);
+int lapis_b200_version(void);
+/* Select and warm up `device` for the calling thread (lapis_initialize,
+ * golden/cpp/spmv.hpp:8-10). */
+int lapis_b200_init(int device);
+/* Release cached per-device workspaces (lapis_finalize, spmv.hpp:12-14). */
+int lapis_b200_finalize(void);
+
+/* The CSR vector-length hint the reference computes before every SpMV:
+ * min(nextPow2(ceil(nnz / max(nrows, 1))), max_vector_length)
+ * (loop_mapping.py:224-246; emitted as golden/cpp/spmv.hpp:17-33).  Host-only. */
+int64_t lapis_b200_csr_vector_length(int64_t nrows, int64_t nnz, int64_t max_vector_length);
+
+/* ------------------------------------------------------------- sparse.spmv_csr
+ * y[i] = sum_{j in [rowptr[i], rowptr[i+1])} values[j] * x[colind[j]]
+ * Replaces the emitted `spmv(rowptr, colind, values, x, y)`
+ * (tests/golden/cpp/spmv.hpp:16-70, op contract dialect.py:222,797-812,
+ * semantics interp.py:798-812).
+ *   rowptr_bytes, colind_bytes in {4, 8} (i32 or i64/index);
+ *   dtype in {F32, F64, I32, I64} for values / x / y;
+ *   vector_length = 0: tiled row-stream kernel (rows up to 512 entries are
+ *     summed sequentially in ascending order, bit-identical to the reference);
+ *   vector_length = 1..32 (power of two): the emitted TeamPolicy mapping with
+ *     that vector length (one row per `vector_length` lanes, shuffle tree). */
+int lapis_b200_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz,
+                        const void* rowptr, int rowptr_bytes,
+                        const void* colind, int colind_bytes,
+                        const void* values, const void* x, void* y,
+                        int dtype, int vector_length, void* stream);
+
+/* A CSR "plan": structure-only analysis (tile -> first-row table of the tiled
+ * kernel) cached across calls on the same rowptr, the analogue of hoisting
+ * the rowptr-derived vector length out of the call.  The plan
+ * keeps a device allocation until lapis_b200_csr_plan_destroy. */
+typedef struct lapis_b200_csr_plan_s* lapis_b200_csr_plan;
+int lapis_b200_csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rowptr_bytes,
+                               void* stream, lapis_b200_csr_plan* out_plan);
+int lapis_b200_csr_plan_destroy(lapis_b200_csr_plan plan);
+int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int rowptr_bytes,
+                             const void* colind, int colind_bytes, const void* values,
+                             const void* x, void* y, int dtype, void* stream);
+
+/* ------------------------------------------------------------- CSR x dense SpMM
+ * Y[i, c] = sum_j values[j] * X[colind[j], c],  c in [0, k)
+ * No reference op: replaces the emitted loop-nest kernel of
+ * oracle/ir/spmm.mlir (thread_parallel over N*K, same per-(i, c) order as
+ * interp.py:798-812).  Rows with <= 4096 entries are summed sequentially per
+ * column (bit-identical); longer rows are split and combined in fixed order. */
+int lapis_b200_spmm_csr(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k,
+                        const void* rowptr, int rowptr_bytes,
+                        const void* colind, int colind_bytes,
+                        const void* values, const void* X, int64_t ldx,
+                        void* Y, int64_t ldy, int dtype, void* stream);
+
+/* ------------------------------------------------------------------ dense
+ * C = A * B — LAPIS::gemm (runtime_header.py:249-266, emitted by
+ * emitter.py:550-552 after linalg_lowering.py:32-45), same math as the loop
+ * route linalg.matmul (interp.py:711-722). */
+int lapis_b200_gemm(int64_t m, int64_t n, int64_t k,
+                    const void* A, int64_t lda, const void* B, int64_t ldb,
+                    void* C, int64_t ldc, int dtype, int mode, void* stream);
+/* y = A * x — LAPIS::gemv (runtime_header.py:268-282; interp.py:729-739). */
+int lapis_b200_gemv(int64_t m, int64_t n, const void* A, int64_t lda,
+                    const void* x, void* y, int dtype, void* stream);
+/* C[b] = A[b] * B[b], contiguous batches — linalg.batch_matmul
+ * (linalg_lowering.py:158-173, interp.py:746-763). */
+int lapis_b200_batch_gemm(int64_t batch, int64_t m, int64_t n, int64_t k,
+                          const void* A, const void* B, void* C, int dtype, int mode,
+                          void* stream);
+/* out = fold over one axis of a row-major rows x cols array — linalg.reduce /
+ * parallel_reduce (linalg_lowering.py:214-252, interp.py:779-795).
+ * axis = 1: out[rows]; axis = 0: out[cols]. */
+int lapis_b200_reduce_2d(int64_t rows, int64_t cols, const void* src, void* out,
+                         int axis, int combiner, int dtype, void* stream);
+/* y = (x > 0) ? x : 0 — linalg.elementwise{cmpf ogt; select} (the GCN ReLU,
+ * interp.py:520-545, 766-776). */
+int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream);
+
+/* ------------------------------------------------------- synthetic inputs
+ * Not reference interfaces: on-device generators for the benchmark matrices
+ * (SURVEY 8(d)), rows [row_begin, row_end) of an n^d-point grid, natural
+ * ordering, sorted columns.  points = 5 (2-D, diag 4, off -1) or 27 (3-D,
+ * diag 26, off -1).  rowptr (int64, row_end-row_begin+1 entries) is rebased to
+ * 0; colind (int32) holds global columns.  Pass colind = values = NULL to
+ * fill rowptr only. */
+int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,
+                             int64_t* rowptr, int32_t* colind, double* values, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAPIS_B200_H */

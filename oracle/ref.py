@@ -2,9 +2,10 @@
 Kokkos C++ for the hot kernels, running on the reference's OWN serial Kokkos
 stub (built by oracle/build.py).  TEST / BASELINE INFRASTRUCTURE ONLY.
 
-Each call returns (output, best_seconds, mean_seconds) where the timings cover
-`reps` calls of the emitted function after one warm-up call (the warm-up
-performs the lazy host->"device" DualView copies, as in the reference).
+Each call returns (output, seconds) where ``seconds`` is a numpy array with the
+wall time of each of `reps` calls of the emitted function, taken after one
+warm-up call (the warm-up performs the lazy host->"device" DualView copies, as
+in the reference).
 """
 from __future__ import annotations
 
@@ -29,16 +30,16 @@ def lib() -> C.CDLL:
         if not _build.REF_SO.exists():
             raise RuntimeError("reference CPU path not built (needs /root/reference once)")
         _lib = C.CDLL(str(_build.REF_SO))
-        i64, vp, ci, dp = C.c_int64, C.c_void_p, C.c_int, C.POINTER(C.c_double)
+        i64, vp, ci = C.c_int64, C.c_void_p, C.c_int
         for name in ("ref_spmv_f64_i64", "ref_spmv_f64_i32", "ref_spmm_f64_i32", "ref_gcn_f32_i32"):
             f = getattr(_lib, name)
-            f.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, ci, ci, dp, dp]
+            f.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, ci, ci, vp]
             f.restype = ci
         for name in ("ref_matmul_f32", "ref_matmul_f64"):
             f = getattr(_lib, name)
-            f.argtypes = [i64, i64, i64, vp, vp, vp, ci, ci, dp, dp]
+            f.argtypes = [i64, i64, i64, vp, vp, vp, ci, ci, vp]
             f.restype = ci
-        _lib.ref_matvec_f64.argtypes = [i64, i64, vp, vp, vp, ci, dp, dp]
+        _lib.ref_matvec_f64.argtypes = [i64, i64, vp, vp, vp, ci, vp]
         _lib.ref_spmv_transfer_probe.argtypes = [vp]
     return _lib
 
@@ -48,12 +49,12 @@ def _p(a):
 
 
 def _csr_call(entry, nrows, ncols, k, kout, rowptr, colind, values, x, w, out, reps, threads):
-    best, mean = C.c_double(0), C.c_double(0)
+    times = np.zeros(max(reps, 1))
     rc = getattr(lib(), entry)(nrows, ncols, k, kout, _p(rowptr), _p(colind), _p(values), _p(x),
-                               _p(w), _p(out), reps, threads, C.byref(best), C.byref(mean))
+                               _p(w), _p(out), reps, threads, _p(times))
     if rc != 0:
         raise RuntimeError(f"{entry} failed ({rc})")
-    return out, best.value, mean.value
+    return out, times[:reps]
 
 
 def spmv_csr(rowptr, colind, values, x, reps=1, threads=1):
@@ -99,22 +100,20 @@ def matmul(A, B, reps=1, threads=1):
     n = B.shape[1]
     out = np.zeros((m, n), dtype=A.dtype)
     entry = {np.dtype(np.float32): "ref_matmul_f32", np.dtype(np.float64): "ref_matmul_f64"}[A.dtype]
-    best, mean = C.c_double(0), C.c_double(0)
-    rc = getattr(lib(), entry)(m, n, k, _p(A), _p(B), _p(out), reps, threads,
-                               C.byref(best), C.byref(mean))
+    times = np.zeros(max(reps, 1))
+    rc = getattr(lib(), entry)(m, n, k, _p(A), _p(B), _p(out), reps, threads, _p(times))
     if rc != 0:
         raise RuntimeError(f"{entry} failed ({rc})")
-    return out, best.value, mean.value
+    return out, times[:reps]
 
 
 def matvec(A, x, reps=1):
     A = np.ascontiguousarray(A, dtype=np.float64)
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.zeros(A.shape[0])
-    best, mean = C.c_double(0), C.c_double(0)
-    lib().ref_matvec_f64(A.shape[0], A.shape[1], _p(A), _p(x), _p(y), reps,
-                         C.byref(best), C.byref(mean))
-    return y, best.value, mean.value
+    times = np.zeros(max(reps, 1))
+    lib().ref_matvec_f64(A.shape[0], A.shape[1], _p(A), _p(x), _p(y), reps, _p(times))
+    return y, times[:reps]
 
 
 def spmv_transfer_probe():

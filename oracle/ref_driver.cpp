@@ -102,16 +102,31 @@ static std::vector<Block> make_blocks(int64_t nrows, int64_t ncols, int64_t k, i
       B.rp.modifyHost();
     }
     B.ci = LAPIS::DualView<REF_CT*>("colind", nnz);
-    fill1(B.ci, colind + base, nnz);
     B.v = LAPIS::DualView<REF_VT*>("values", nnz);
     fill1(B.v, values + base, nnz);
 #if REF_KIND == 1
     (void)k; (void)kout;
-    B.x = LAPIS::DualView<REF_VT*>("x", ncols);
-    fill1(B.x, x, ncols);
+    // x restricted to the block's column window [cmin, cmax], colind rebased by
+    // cmin: the same products in the same order, without replicating all of x
+    // per thread (the config-5 x is 1.6 GB).
+    int64_t cmin = ncols, cmax = -1;
+    for (int64_t j = 0; j < nnz; ++j) {
+      const int64_t cj = (int64_t)colind[base + j];
+      cmin = cj < cmin ? cj : cmin;
+      cmax = cj > cmax ? cj : cmax;
+    }
+    if (cmax < cmin) { cmin = 0; cmax = -1; }
+    {
+      auto h = B.ci.host_view();
+      for (int64_t j = 0; j < nnz; ++j) h(j) = (REF_CT)((int64_t)colind[base + j] - cmin);
+      B.ci.modifyHost();
+    }
+    B.x = LAPIS::DualView<REF_VT*>("x", cmax - cmin + 1);
+    fill1(B.x, x + cmin, cmax - cmin + 1);
     B.y = LAPIS::DualView<REF_VT*>("y", n);
     B.y.modifyHost();
 #else
+    fill1(B.ci, colind + base, nnz);
     B.x = LAPIS::DualView<REF_VT**>("x", ncols, k);
     fill2(B.x, x, ncols, k, k);
 #if REF_KIND == 5
@@ -139,26 +154,21 @@ static void call_block(Block& B) {
 }
 }  // namespace
 
-// Returns the best wall time of `reps` timed calls (seconds) through *best_s,
-// and the mean through *mean_s; writes the result rows to y (row-major).
+// Writes the wall time of each of `reps` timed calls (seconds) to times[] and
+// the result rows to y (row-major).
 extern "C" int REF_ENTRY(int64_t nrows, int64_t ncols, int64_t k, int64_t kout,
                          const int64_t* rowptr, const REF_CT* colind, const REF_VT* values,
                          const REF_VT* x, const REF_VT* w, REF_VT* y, int reps, int threads,
-                         double* best_s, double* mean_s) {
+                         double* times) {
   lapis_initialize();
   int nblk = std::max(1, (int)std::min<int64_t>(threads, std::max<int64_t>(nrows, 1)));
   auto bl = make_blocks(nrows, ncols, k, kout, rowptr, colind, values, x, w, nblk);
   for (auto& B : bl) call_block(B);  // warm-up: lazy H2D copies happen here, serially
-  double best = 1e300, sum = 0.0;
   for (int r = 0; r < reps; ++r) {
     double t0 = now_s();
     run_blocks(nblk, [&](int b) { call_block(bl[b]); });
-    double dt = now_s() - t0;
-    best = std::min(best, dt);
-    sum += dt;
+    if (times) times[r] = now_s() - t0;
   }
-  if (best_s) *best_s = reps > 0 ? best : 0.0;
-  if (mean_s) *mean_s = reps > 0 ? sum / reps : 0.0;
   for (auto& B : bl) {
     B.y.syncHost();
     auto h = B.y.host_view();
@@ -178,7 +188,7 @@ extern "C" int REF_ENTRY(int64_t nrows, int64_t ncols, int64_t k, int64_t kout,
 #elif REF_KIND == 3
 // ------------------------------------------------------------ dense matmul
 extern "C" int REF_ENTRY(int64_t m, int64_t n, int64_t k, const REF_VT* a, const REF_VT* b,
-                         REF_VT* c, int reps, int threads, double* best_s, double* mean_s) {
+                         REF_VT* c, int reps, int threads, double* times) {
   lapis_initialize();
   int nblk = std::max(1, (int)std::min<int64_t>(threads, std::max<int64_t>(m, 1)));
   struct MB { int64_t r0, r1; LAPIS::DualView<REF_VT**> a, b, c; };
@@ -194,15 +204,11 @@ extern "C" int REF_ENTRY(int64_t m, int64_t n, int64_t k, const REF_VT* a, const
     B.c.modifyHost();
   }
   for (auto& B : bl) B.c = matmul(B.a, B.b, B.c);
-  double best = 1e300, sum = 0.0;
   for (int r = 0; r < reps; ++r) {
     double t0 = now_s();
     run_blocks(nblk, [&](int t) { bl[t].c = matmul(bl[t].a, bl[t].b, bl[t].c); });
-    double dt = now_s() - t0;
-    best = std::min(best, dt); sum += dt;
+    if (times) times[r] = now_s() - t0;
   }
-  if (best_s) *best_s = reps > 0 ? best : 0.0;
-  if (mean_s) *mean_s = reps > 0 ? sum / reps : 0.0;
   for (auto& B : bl) {
     B.c.syncHost();
     auto h = B.c.host_view();
@@ -216,7 +222,7 @@ extern "C" int REF_ENTRY(int64_t m, int64_t n, int64_t k, const REF_VT* a, const
 #elif REF_KIND == 4
 // ------------------------------------------------------------ dense matvec
 extern "C" int REF_ENTRY(int64_t m, int64_t n, const REF_VT* a, const REF_VT* x, REF_VT* y,
-                         int reps, double* best_s, double* mean_s) {
+                         int reps, double* times) {
   lapis_initialize();
   LAPIS::DualView<REF_VT**> A("a", m, n);
   fill2(A, a, m, n, n);
@@ -225,15 +231,11 @@ extern "C" int REF_ENTRY(int64_t m, int64_t n, const REF_VT* a, const REF_VT* x,
   LAPIS::DualView<REF_VT*> Y("y", m);
   Y.modifyHost();
   Y = matvec(A, X, Y);
-  double best = 1e300, sum = 0.0;
   for (int r = 0; r < reps; ++r) {
     double t0 = now_s();
     Y = matvec(A, X, Y);
-    double dt = now_s() - t0;
-    best = std::min(best, dt); sum += dt;
+    if (times) times[r] = now_s() - t0;
   }
-  if (best_s) *best_s = reps > 0 ? best : 0.0;
-  if (mean_s) *mean_s = reps > 0 ? sum / reps : 0.0;
   Y.syncHost();
   auto h = Y.host_view();
   for (int64_t i = 0; i < m; ++i) y[i] = h(i);

@@ -1,0 +1,158 @@
+// capi.cu — the extern "C" boundary declared in include/lapis_b200.h.
+// Thin: argument checks, stream casts, error capture; the kernels live in the
+// other translation units.
+#include "common.cuh"
+
+#include <cstdio>
+#include <cstring>
+
+namespace lapis_b200 {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return LAPIS_B200_OK;
+  const int code = (e == cudaErrorMemoryAllocation) ? LAPIS_B200_ERR_NOMEM : LAPIS_B200_ERR_CUDA;
+  return fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
+
+// kernels (other translation units)
+int spmv_csr(int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
+             const void*, void*, int, int, cudaStream_t);
+int csr_plan_create(int64_t, int64_t, const void*, int, cudaStream_t, void**);
+int csr_plan_destroy(void*);
+int spmv_csr_plan(void*, const void*, int, const void*, int, const void*, const void*, void*, int,
+                  cudaStream_t);
+int spmm_csr(int64_t, int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
+             const void*, int64_t, void*, int64_t, int, cudaStream_t);
+int gemm_dispatch(int64_t, int64_t, int64_t, int64_t, const void*, int64_t, const void*, int64_t,
+                  void*, int64_t, int64_t, int64_t, int64_t, int, int, cudaStream_t);
+int gemv(int64_t, int64_t, const void*, int64_t, const void*, void*, int, cudaStream_t);
+int reduce_2d(int64_t, int64_t, const void*, void*, int, int, int, cudaStream_t);
+int relu(int64_t, const void*, void*, int, cudaStream_t);
+int synth_stencil(int, int64_t, int64_t, int64_t, int64_t*, int32_t*, double*, cudaStream_t);
+void release_workspaces();
+
+}  // namespace lapis_b200
+
+using namespace lapis_b200;
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* lapis_b200_last_error(void) { return g_last_error.c_str(); }
+
+int lapis_b200_version(void) { return 100; }
+
+int lapis_b200_init(int device) {
+  int n = 0;
+  LB_TRY(check_cuda(cudaGetDeviceCount(&n), "cudaGetDeviceCount"));
+  if (device < 0 || device >= n) return fail(LAPIS_B200_ERR_ARG, "init: no such device");
+  LB_TRY(check_cuda(cudaSetDevice(device), "cudaSetDevice"));
+  cudaDeviceProp prop;
+  LB_TRY(check_cuda(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties"));
+  if (prop.major != 10)
+    return fail(LAPIS_B200_ERR_UNSUPPORTED, "init: kernels are built for sm_100a (B200)");
+  LB_TRY(check_cuda(cudaFree(nullptr), "context init"));
+  return LAPIS_B200_OK;
+}
+
+int lapis_b200_finalize(void) {
+  release_workspaces();
+  return LAPIS_B200_OK;
+}
+
+int64_t lapis_b200_csr_vector_length(int64_t nrows, int64_t nnz, int64_t cap) {
+  // loop_mapping.py:224-246: k = ceildivsi(nnz, max(nrows, 1)); smallest power
+  // of two p <= cap/2 with k <= p, else cap
+  const int64_t rows = nrows > 1 ? nrows : 1;
+  int64_t k = nnz / rows;
+  if ((nnz % rows != 0) && ((nnz < 0) == (rows < 0))) k += 1;  // runtime_header.py:75-80
+  int64_t acc = cap;
+  for (int64_t p = cap / 2; p >= 1; p /= 2)
+    if (k <= p) acc = p;
+  return acc;
+}
+
+int lapis_b200_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr,
+                        int rowptr_bytes, const void* colind, int colind_bytes,
+                        const void* values, const void* x, void* y, int dtype,
+                        int vector_length, void* stream) {
+  return spmv_csr(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, x, y,
+                  dtype, vector_length, S(stream));
+}
+
+int lapis_b200_csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rowptr_bytes,
+                               void* stream, lapis_b200_csr_plan* out_plan) {
+  return csr_plan_create(nrows, nnz, rowptr, rowptr_bytes, S(stream),
+                         reinterpret_cast<void**>(out_plan));
+}
+
+int lapis_b200_csr_plan_destroy(lapis_b200_csr_plan plan) { return csr_plan_destroy(plan); }
+
+int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int rowptr_bytes,
+                             const void* colind, int colind_bytes, const void* values,
+                             const void* x, void* y, int dtype, void* stream) {
+  return spmv_csr_plan(plan, rowptr, rowptr_bytes, colind, colind_bytes, values, x, y, dtype,
+                       S(stream));
+}
+
+int lapis_b200_spmm_csr(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const void* rowptr,
+                        int rowptr_bytes, const void* colind, int colind_bytes,
+                        const void* values, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                        int dtype, void* stream) {
+  return spmm_csr(nrows, ncols, nnz, k, rowptr, rowptr_bytes, colind, colind_bytes, values, X,
+                  ldx, Y, ldy, dtype, S(stream));
+}
+
+int lapis_b200_gemm(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                    int64_t ldb, void* C, int64_t ldc, int dtype, int mode, void* stream) {
+  return gemm_dispatch(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, dtype, mode, S(stream));
+}
+
+int lapis_b200_gemv(int64_t m, int64_t n, const void* A, int64_t lda, const void* x, void* y,
+                    int dtype, void* stream) {
+  if (m < 0 || n < 0 || lda < n) return fail(LAPIS_B200_ERR_ARG, "gemv: bad extents");
+  if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "gemv: unsupported dtype");
+  if (m > 0 && (!y || (n > 0 && (!A || !x)))) return fail(LAPIS_B200_ERR_ARG, "gemv: null operand");
+  return gemv(m, n, A, lda, x, y, dtype, S(stream));
+}
+
+int lapis_b200_batch_gemm(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
+                          const void* B, void* C, int dtype, int mode, void* stream) {
+  if (batch < 0) return fail(LAPIS_B200_ERR_ARG, "batch_gemm: negative batch");
+  return gemm_dispatch(batch, m, n, k, A, k, B, n, C, n, m * k, k * n, m * n, dtype, mode,
+                       S(stream));
+}
+
+int lapis_b200_reduce_2d(int64_t rows, int64_t cols, const void* src, void* out, int axis,
+                         int combiner, int dtype, void* stream) {
+  if (rows < 0 || cols < 0) return fail(LAPIS_B200_ERR_ARG, "reduce: negative extent");
+  if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "reduce: unsupported dtype");
+  if ((rows > 0 && cols > 0 && !src) || ((axis == 1 ? rows : cols) > 0 && !out))
+    return fail(LAPIS_B200_ERR_ARG, "reduce: null operand");
+  return reduce_2d(rows, cols, src, out, axis, combiner, dtype, S(stream));
+}
+
+int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream) {
+  if (n < 0) return fail(LAPIS_B200_ERR_ARG, "relu: negative extent");
+  if (n > 0 && (!x || !y)) return fail(LAPIS_B200_ERR_ARG, "relu: null operand");
+  return relu(n, x, y, dtype, S(stream));
+}
+
+int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,
+                             int64_t* rowptr, int32_t* colind, double* values, void* stream) {
+  return synth_stencil(points, n, row_begin, row_end, rowptr, colind, values, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// common.cuh — shared helpers for the sm_100a kernels behind include/lapis_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "../../include/lapis_b200.h"
+
+namespace lapis_b200 {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_cuda(cudaError_t e, const char* what);
+int check_launch(const char* what);
+
+#define LB_TRY(expr)              \
+  do {                            \
+    int _rc = (expr);             \
+    if (_rc != LAPIS_B200_OK) return _rc; \
+  } while (0)
+
+// ------------------------------------------------------- element arithmetic
+// Reference semantics: every op is rounded to the element type before the next
+// one (interp.py:168-183), ints wrap (interp.py:145-152).  The explicit _rn
+// intrinsics keep nvcc from contracting mul+add into an FMA, so a sequential
+// sum reproduces the reference bit for bit.
+template <class T> struct Arith;
+template <> struct Arith<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double zero() { return 0.0; }
+};
+template <> struct Arith<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float zero() { return 0.0f; }
+};
+template <> struct Arith<long long> {
+  static __device__ __forceinline__ long long mul(long long a, long long b) {
+    return (long long)((unsigned long long)a * (unsigned long long)b);
+  }
+  static __device__ __forceinline__ long long add(long long a, long long b) {
+    return (long long)((unsigned long long)a + (unsigned long long)b);
+  }
+  static __device__ __forceinline__ long long zero() { return 0; }
+};
+template <> struct Arith<int> {
+  static __device__ __forceinline__ int mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
+  static __device__ __forceinline__ int add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
+  static __device__ __forceinline__ int zero() { return 0; }
+};
+
+// warp shuffle for 64-bit types
+template <class T>
+__device__ __forceinline__ T shfl_xor(T v, int mask, int width = 32) {
+  return __shfl_xor_sync(0xffffffffu, v, mask, width);
+}
+
+// streaming (read-once) loads: bypass L1 allocation, keep L2 policy default
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+               : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ longlong2 ld_stream(const longlong2* p) {
+  longlong2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s64 {%0,%1}, [%2];"
+               : "=l"(r.x), "=l"(r.y) : "l"(p));
+  return r;
+}
+
+inline int elem_bytes(int dtype) {
+  return (dtype == LAPIS_B200_F64 || dtype == LAPIS_B200_I64) ? 8 : 4;
+}
+inline bool valid_dtype(int dtype) { return dtype >= LAPIS_B200_F32 && dtype <= LAPIS_B200_I64; }
+
+inline int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+}  // namespace lapis_b200

@@ -1,0 +1,280 @@
+// dense.cu — reference-order dense kernels for sm_100a:
+//   * gemm_exact / batch_gemm_exact: C[i,j] = sum_k A[i,k]*B[k,j] with the
+//     k loop ascending and non-contracted mul/add per step — the order of
+//     interp.py:711-722 / 746-763 and of the emitted TeamPolicy nest
+//     (golden/cpp/matmul_f64.hpp:23-38), hence bit-identical for every dtype
+//     (ints wrap).  Shared-memory tiled so A and B are read once per tile.
+//   * gemv: one thread per row (RangePolicy(0, m) of runtime_header.py:268-282)
+//     summing sequentially, with A staged through shared memory in 32-column
+//     slabs so the HBM reads stay coalesced although each thread walks a row.
+//   * reduce_2d: the parallel_reduce family (interp.py:779-795) with the
+//     reference combiners and identities; same staging for the row fold.
+//   * relu: the GCN elementwise select (cmpf ogt + select).
+// The tensor-core fp32 (3xTF32, tcgen05) and fp64 (DMMA) GEMMs live in
+// gemm_tf32x3.cu and gemm_dmma.cu.
+#include "common.cuh"
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+namespace lapis_b200 {
+
+// --------------------------------------------------------------- combiners
+template <class T> __device__ __forceinline__ T ident_min();
+template <class T> __device__ __forceinline__ T ident_max();
+template <> __device__ __forceinline__ double ident_min<double>() { return INFINITY; }
+template <> __device__ __forceinline__ double ident_max<double>() { return -INFINITY; }
+template <> __device__ __forceinline__ float ident_min<float>() { return INFINITY; }
+template <> __device__ __forceinline__ float ident_max<float>() { return -INFINITY; }
+template <> __device__ __forceinline__ long long ident_min<long long>() { return LLONG_MAX; }
+template <> __device__ __forceinline__ long long ident_max<long long>() { return LLONG_MIN; }
+template <> __device__ __forceinline__ int ident_min<int>() { return INT_MAX; }
+template <> __device__ __forceinline__ int ident_max<int>() { return INT_MIN; }
+
+template <class T>
+__device__ __forceinline__ T identity(int comb) {
+  switch (comb) {
+    case LAPIS_B200_ADD: return Arith<T>::zero();
+    case LAPIS_B200_MUL: return T(1);
+    case LAPIS_B200_MIN: return ident_min<T>();
+    default: return ident_max<T>();
+  }
+}
+
+// interp.py:174-183: add/mul rounded; min/max keep acc unless the contribution wins
+template <class T>
+__device__ __forceinline__ T combine(T acc, T v, int comb) {
+  switch (comb) {
+    case LAPIS_B200_ADD: return Arith<T>::add(acc, v);
+    case LAPIS_B200_MUL: return Arith<T>::mul(acc, v);
+    case LAPIS_B200_MIN: return (acc <= v) ? acc : v;
+    default: return (acc >= v) ? acc : v;
+  }
+}
+
+// -------------------------------------------------------------- exact GEMM
+constexpr int EG_TILE = 32;   // C tile 32 x 32, K slab 32
+constexpr int EG_ROWS = 4;    // outputs per thread (rows)
+
+template <class T>
+__global__ void __launch_bounds__(256)
+gemm_exact_kernel(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int64_t lda,
+                  const T* __restrict__ B, int64_t ldb, T* __restrict__ C, int64_t ldc,
+                  int64_t strideA, int64_t strideB, int64_t strideC) {
+  __shared__ T As[EG_TILE][EG_TILE + 1];
+  __shared__ T Bs[EG_TILE][EG_TILE + 1];
+  A += blockIdx.z * strideA;
+  B += blockIdx.z * strideB;
+  C += blockIdx.z * strideC;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t row0 = (int64_t)blockIdx.y * EG_TILE, col0 = (int64_t)blockIdx.x * EG_TILE;
+  T acc[EG_ROWS];
+#pragma unroll
+  for (int q = 0; q < EG_ROWS; ++q) acc[q] = Arith<T>::zero();
+  for (int64_t k0 = 0; k0 < k; k0 += EG_TILE) {
+#pragma unroll
+    for (int q = 0; q < EG_ROWS; ++q) {
+      const int r = ty * EG_ROWS + q;
+      const int64_t ar = row0 + r, ak = k0 + tx;
+      As[r][tx] = (ar < m && ak < k) ? A[ar * lda + ak] : Arith<T>::zero();
+      const int64_t bk = k0 + r, bc = col0 + tx;
+      Bs[r][tx] = (bk < k && bc < n) ? B[bk * ldb + bc] : Arith<T>::zero();
+    }
+    __syncthreads();
+    const int kk_end = (int)((k - k0) < EG_TILE ? (k - k0) : EG_TILE);
+    for (int kk = 0; kk < kk_end; ++kk) {
+      const T b = Bs[kk][tx];
+#pragma unroll
+      for (int q = 0; q < EG_ROWS; ++q)
+        acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(As[ty * EG_ROWS + q][kk], b));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < EG_ROWS; ++q) {
+    const int64_t r = row0 + ty * EG_ROWS + q, c = col0 + tx;
+    if (r < m && c < n) C[r * ldc + c] = acc[q];
+  }
+}
+
+// ------------------------------------------------- row-sequential row folds
+// One thread per row; A staged through shared memory in 32-column slabs.
+constexpr int RF_ROWS = 128;
+
+template <class T, bool DOT>
+__global__ void __launch_bounds__(RF_ROWS)
+row_fold_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
+                const T* __restrict__ x, T* __restrict__ y, int comb) {
+  __shared__ T tile[RF_ROWS][33];
+  __shared__ T xs[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * RF_ROWS;
+  T acc = DOT ? Arith<T>::zero() : identity<T>(comb);
+  for (int64_t c0 = 0; c0 < n; c0 += 32) {
+    const int64_t c = c0 + lane;
+    // each warp loads 32 row segments of 32 columns (coalesced per segment)
+    for (int r = warp; r < RF_ROWS; r += RF_ROWS / 32) {
+      const int64_t gr = row0 + r;
+      tile[r][lane] = (gr < m && c < n) ? A[gr * lda + c] : Arith<T>::zero();
+    }
+    if (DOT && t < 32) xs[t] = (c < n) ? x[c] : Arith<T>::zero();
+    __syncthreads();
+    const int cend = (int)((n - c0) < 32 ? (n - c0) : 32);
+    for (int q = 0; q < cend; ++q) {
+      if (DOT) acc = Arith<T>::add(acc, Arith<T>::mul(tile[t][q], xs[q]));
+      else acc = combine(acc, tile[t][q], comb);
+    }
+    __syncthreads();
+  }
+  const int64_t row = row0 + t;
+  if (row < m) y[row] = acc;
+}
+
+// column fold (axis 0): one thread per column, rows in ascending order
+template <class T>
+__global__ void col_fold_kernel(int64_t rows, int64_t cols, const T* __restrict__ src,
+                                T* __restrict__ out, int comb) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  T acc = identity<T>(comb);
+  for (int64_t r = 0; r < rows; ++r) acc = combine(acc, src[r * cols + c], comb);
+  out[c] = acc;
+}
+
+template <class T>
+__global__ void relu_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = x[i];
+    y[i] = (v > T(0)) ? v : T(0);  // cmpf ogt + select: NaN and -0.0 map to +0
+  }
+}
+
+// =============================================================== host side
+template <class T>
+static int launch_gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
+                             int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                             int64_t sA, int64_t sB, int64_t sC, cudaStream_t st) {
+  dim3 grid((unsigned)((n + EG_TILE - 1) / EG_TILE), (unsigned)((m + EG_TILE - 1) / EG_TILE),
+            (unsigned)batch);
+  if (grid.y > 65535 || grid.z > 65535) return fail(LAPIS_B200_ERR_ARG, "gemm: grid too large");
+  gemm_exact_kernel<T><<<grid, 256, 0, st>>>(m, n, k, (const T*)A, lda, (const T*)B, ldb, (T*)C,
+                                             ldc, sA, sB, sC);
+  return check_launch("gemm_exact_kernel");
+}
+
+int gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+               const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+               int64_t sC, int dtype, cudaStream_t st) {
+  switch (dtype) {
+    case LAPIS_B200_F64: return launch_gemm_exact<double>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+    case LAPIS_B200_F32: return launch_gemm_exact<float>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+    case LAPIS_B200_I64: return launch_gemm_exact<long long>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+    case LAPIS_B200_I32: return launch_gemm_exact<int>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+  }
+  return fail(LAPIS_B200_ERR_ARG, "gemm: unsupported dtype");
+}
+
+template <class T, bool DOT>
+static int launch_row_fold(int64_t m, int64_t n, const void* A, int64_t lda, const void* x,
+                           void* y, int comb, cudaStream_t st) {
+  const int64_t blocks = (m + RF_ROWS - 1) / RF_ROWS;
+  row_fold_kernel<T, DOT><<<(unsigned)blocks, RF_ROWS, 0, st>>>(m, n, (const T*)A, lda,
+                                                                  (const T*)x, (T*)y, comb);
+  return check_launch("row_fold_kernel");
+}
+
+int gemv(int64_t m, int64_t n, const void* A, int64_t lda, const void* x, void* y, int dtype,
+         cudaStream_t st) {
+  if (m == 0) return LAPIS_B200_OK;
+  switch (dtype) {
+    case LAPIS_B200_F64: return launch_row_fold<double, true>(m, n, A, lda, x, y, 0, st);
+    case LAPIS_B200_F32: return launch_row_fold<float, true>(m, n, A, lda, x, y, 0, st);
+    case LAPIS_B200_I64: return launch_row_fold<long long, true>(m, n, A, lda, x, y, 0, st);
+    case LAPIS_B200_I32: return launch_row_fold<int, true>(m, n, A, lda, x, y, 0, st);
+  }
+  return fail(LAPIS_B200_ERR_ARG, "gemv: unsupported dtype");
+}
+
+template <class T>
+static int launch_reduce(int64_t rows, int64_t cols, const void* src, void* out, int axis,
+                         int comb, cudaStream_t st) {
+  if (axis == 1) return launch_row_fold<T, false>(rows, cols, src, cols, nullptr, out, comb, st);
+  if (cols == 0) return LAPIS_B200_OK;
+  col_fold_kernel<T><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(rows, cols, (const T*)src,
+                                                                      (T*)out, comb);
+  return check_launch("col_fold_kernel");
+}
+
+int reduce_2d(int64_t rows, int64_t cols, const void* src, void* out, int axis, int comb,
+              int dtype, cudaStream_t st) {
+  if (axis != 0 && axis != 1) return fail(LAPIS_B200_ERR_ARG, "reduce: axis must be 0 or 1");
+  if (comb < LAPIS_B200_ADD || comb > LAPIS_B200_MAX)
+    return fail(LAPIS_B200_ERR_ARG, "reduce: unknown combiner");
+  if ((axis == 1 ? rows : cols) == 0) return LAPIS_B200_OK;
+  switch (dtype) {
+    case LAPIS_B200_F64: return launch_reduce<double>(rows, cols, src, out, axis, comb, st);
+    case LAPIS_B200_F32: return launch_reduce<float>(rows, cols, src, out, axis, comb, st);
+    case LAPIS_B200_I64: return launch_reduce<long long>(rows, cols, src, out, axis, comb, st);
+    case LAPIS_B200_I32: return launch_reduce<int>(rows, cols, src, out, axis, comb, st);
+  }
+  return fail(LAPIS_B200_ERR_ARG, "reduce: unsupported dtype");
+}
+
+int relu(int64_t n, const void* x, void* y, int dtype, cudaStream_t st) {
+  if (n == 0) return LAPIS_B200_OK;
+  const int64_t blocks = (n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32;
+  if (dtype == LAPIS_B200_F64)
+    relu_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(n, (const double*)x, (double*)y);
+  else if (dtype == LAPIS_B200_F32)
+    relu_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(n, (const float*)x, (float*)y);
+  else
+    return fail(LAPIS_B200_ERR_UNSUPPORTED, "relu: floating-point dtypes only");
+  return check_launch("relu_kernel");
+}
+
+}  // namespace lapis_b200
+
+namespace lapis_b200 {
+
+// tensor-core paths (gemm_tf32x3.cu, gemm_dmma.cu); return UNSUPPORTED when a
+// shape/dtype falls outside what they implement
+int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+                int64_t sC, cudaStream_t st) __attribute__((weak));
+int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+              const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+              int64_t sC, cudaStream_t st) __attribute__((weak));
+
+int gemm_dispatch(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+                  int64_t sC, int dtype, int mode, cudaStream_t st) {
+  if (m < 0 || n < 0 || k < 0 || lda < k || ldb < n || ldc < n)
+    return fail(LAPIS_B200_ERR_ARG, "gemm: bad extents / leading dimensions");
+  if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "gemm: unsupported dtype");
+  if (batch == 0 || m == 0 || n == 0) return LAPIS_B200_OK;
+  if (!C || (k > 0 && (!A || !B))) return fail(LAPIS_B200_ERR_ARG, "gemm: null operand");
+  if (mode == LAPIS_B200_GEMM_AUTO) {
+    if (dtype == LAPIS_B200_F32 && gemm_tf32x3) mode = LAPIS_B200_GEMM_TF32X3;
+    else if (dtype == LAPIS_B200_F64 && gemm_dmma) mode = LAPIS_B200_GEMM_DMMA;
+    else mode = LAPIS_B200_GEMM_EXACT;
+  }
+  switch (mode) {
+    case LAPIS_B200_GEMM_EXACT:
+      return gemm_exact(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, dtype, st);
+    case LAPIS_B200_GEMM_TF32X3:
+      if (dtype != LAPIS_B200_F32 || !gemm_tf32x3)
+        return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm: TF32X3 is an f32 mode");
+      return gemm_tf32x3(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+    case LAPIS_B200_GEMM_DMMA:
+      if (dtype != LAPIS_B200_F64 || !gemm_dmma)
+        return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm: DMMA is an f64 mode");
+      return gemm_dmma(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+  }
+  return fail(LAPIS_B200_ERR_ARG, "gemm: unknown mode");
+}
+
+void release_workspaces() {}
+
+}  // namespace lapis_b200

@@ -1,0 +1,245 @@
+// spmm.cu — CSR x dense SpMM for sm_100a:  Y[i, c] = sum_j values[j] * X[colind[j], c].
+//
+// The reference has no SpMM op; the loop nest oracle/ir/spmm.mlir
+// is what its preset lowers (thread_parallel over N*K, CSR vector-length hint),
+// with the per-(i, c) order of interp.py:798-812: j ascending, mul and add
+// each rounded.
+//
+// Kernel 1 (spmm_row_kernel): one warp per row, lanes across the dense
+//   columns (2 per lane, 16-byte vector gathers of each X row), the j loop
+//   walked in ascending order with non-contracted mul/add -> bit-identical to
+//   the reference for every row of <= SPLIT entries.  Rows longer than SPLIT
+//   are left to kernels 2-3.
+// Kernel 2 (spmm_chunk_kernel): the nonzero stream is cut into fixed chunks of
+//   SPLIT entries; for each long row overlapping chunk q a CTA computes the
+//   partial row over the overlap (8 warps on contiguous sub-ranges, folded in
+//   warp order) into slot (q, 0 = row began earlier | 1 = row begins here).
+// Kernel 3 (spmm_combine_kernel): for each long row, sums its chunk partials
+//   in chunk order.  Deterministic (fixed association), parity by tolerance.
+// This splits power-law hub rows (config 3: max 117,686 entries) over many
+// SMs without atomics.
+#include "common.cuh"
+
+namespace lapis_b200 {
+
+constexpr int SPMM_WARPS = 8;
+constexpr int64_t SPLIT = 2048;
+
+// --------------------------------------------------------------- kernel 1
+template <class T, class RP, class CI, int EPL>
+__global__ void __launch_bounds__(SPMM_WARPS * 32)
+spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+                const CI* __restrict__ colind, const T* __restrict__ values,
+                const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * SPMM_WARPS + (threadIdx.x >> 5);
+  if (row >= nrows) return;
+  const int64_t b = (int64_t)rowptr[row];
+  int64_t e = (int64_t)rowptr[row + 1];
+  if (e < b) e = b;
+  if (e - b > SPLIT) return;  // long row: kernels 2-3
+  for (int64_t c0 = 0; c0 < k; c0 += 32 * EPL) {
+    const int64_t col = c0 + (int64_t)lane * EPL;
+    const bool full = col + EPL <= k;
+    T acc[EPL];
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) acc[q] = Arith<T>::zero();
+    int64_t j = b;
+    for (; j + 4 <= e; j += 4) {
+      T v[4];
+      int64_t ci[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { v[u] = values[j + u]; ci[u] = (int64_t)colind[j + u]; }
+      T xv[4][EPL];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const T* xr = X + ci[u] * ldx + col;
+        if (EPL == 2 && full) {
+          if constexpr (sizeof(T) == 8) {
+            const longlong2 w = __ldg(reinterpret_cast<const longlong2*>(xr));
+            memcpy(&xv[u][0], &w.x, 8);
+            memcpy(&xv[u][EPL - 1], &w.y, 8);
+          } else {
+            const int2 w = __ldg(reinterpret_cast<const int2*>(xr));
+            memcpy(&xv[u][0], &w.x, 4);
+            memcpy(&xv[u][EPL - 1], &w.y, 4);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < EPL; ++q) xv[u][q] = (col + q < k) ? __ldg(xr + q) : Arith<T>::zero();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v[u], xv[u][q]));
+    }
+    for (; j < e; ++j) {
+      const T v = values[j];
+      const T* xr = X + (int64_t)colind[j] * ldx + col;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q)
+        if (col + q < k) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v, __ldg(xr + q)));
+    }
+    T* yr = Y + row * ldy + col;
+#pragma unroll
+    for (int q = 0; q < EPL; ++q)
+      if (col + q < k) yr[q] = acc[q];
+  }
+}
+
+// --------------------------------------------------------------- kernel 2
+template <class RP>
+__device__ __forceinline__ int64_t first_row_ending_after(int64_t nrows, const RP* rowptr,
+                                                          int64_t value) {
+  // smallest r in [0, nrows) with rowptr[r+1] > value (nrows if none)
+  int64_t lo = 0, hi = nrows;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)rowptr[mid + 1] > value) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+template <class T, class RP, class CI>
+__global__ void __launch_bounds__(SPMM_WARPS * 32)
+spmm_chunk_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+                  const CI* __restrict__ colind, const T* __restrict__ values,
+                  const T* __restrict__ X, int64_t ldx, T* __restrict__ part,
+                  int64_t* __restrict__ slot_row) {
+  extern __shared__ unsigned char smem_raw[];
+  T* wpart = reinterpret_cast<T*>(smem_raw);  // [SPMM_WARPS][k]
+  const int64_t q = blockIdx.x;
+  const int64_t base = (int64_t)rowptr[0];
+  const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // a long row (> SPLIT entries) cannot lie strictly inside one chunk, so only
+  // the first and the last row overlapping [lo, hi) can be long
+  const int64_t r_first = first_row_ending_after(nrows, rowptr, lo);
+  const int64_t r_last = first_row_ending_after(nrows, rowptr, hi - 1);
+  for (int cand = 0; cand < 2; ++cand) {
+    const int64_t r = cand == 0 ? r_first : r_last;
+    if (r >= nrows || (cand == 1 && r_last == r_first)) continue;
+    const int64_t b = (int64_t)rowptr[r];
+    if (b >= hi) continue;
+    const int64_t e = (int64_t)rowptr[r + 1];
+    if (e - b <= SPLIT) continue;  // short rows belong to kernel 1
+    const int64_t s0 = b > lo ? b : lo, s1 = e < hi ? e : hi;
+    const int slot = (b < lo) ? 0 : 1;
+    // warp w folds the contiguous sub-range [s0 + w*len/W, s0 + (w+1)*len/W)
+    const int64_t len = s1 - s0;
+    const int64_t w0 = s0 + len * warp / SPMM_WARPS, w1 = s0 + len * (warp + 1) / SPMM_WARPS;
+    for (int64_t col = lane; col < k; col += 32) {
+      T acc = Arith<T>::zero();
+      for (int64_t j = w0; j < w1; ++j)
+        acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(X + (int64_t)colind[j] * ldx + col)));
+      wpart[warp * k + col] = acc;
+    }
+    __syncthreads();
+    T* dst = part + (q * 2 + slot) * k;
+    for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
+      T acc = Arith<T>::zero();
+      for (int w = 0; w < SPMM_WARPS; ++w) acc = Arith<T>::add(acc, wpart[w * k + col]);
+      dst[col] = acc;
+    }
+    if (threadIdx.x == 0) slot_row[q * 2 + slot] = r;
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------- kernel 3
+template <class T, class RP>
+__global__ void spmm_combine_kernel(int64_t k, const RP* __restrict__ rowptr,
+                                    const T* __restrict__ part, const int64_t* __restrict__ slot_row,
+                                    T* __restrict__ Y, int64_t ldy) {
+  const int64_t q = blockIdx.x;
+  const int64_t r = slot_row[q * 2 + 1];
+  if (r < 0) return;
+  const int64_t base = (int64_t)rowptr[0];
+  const int64_t qend = ((int64_t)rowptr[r + 1] - base - 1) / SPLIT;
+  for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
+    T acc = part[(q * 2 + 1) * k + col];
+    for (int64_t qq = q + 1; qq <= qend; ++qq) acc = Arith<T>::add(acc, part[(qq * 2 + 0) * k + col]);
+    Y[r * ldy + col] = acc;
+  }
+}
+
+// ================================================================ host side
+template <class T, class RP, class CI>
+struct SpmmOp {
+  static int run(int64_t nrows, int64_t nnz, int64_t k, const void* rowptr, const void* colind,
+                 const void* values, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                 cudaStream_t st) {
+    const int64_t blocks = (nrows + SPMM_WARPS - 1) / SPMM_WARPS;
+    if (blocks > 0x7fffffffLL) return fail(LAPIS_B200_ERR_ARG, "spmm: too many rows");
+    const bool vec = (ldx % 2 == 0) && ((uintptr_t)X % (2 * sizeof(T)) == 0);
+    if (vec)
+      spmm_row_kernel<T, RP, CI, 2><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+          (T*)Y, ldy);
+    else
+      spmm_row_kernel<T, RP, CI, 1><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+          (T*)Y, ldy);
+    LB_TRY(check_launch("spmm_row_kernel"));
+    if (nnz <= SPLIT) return LAPIS_B200_OK;  // no row can be long
+    const int64_t nchunks = (nnz + SPLIT - 1) / SPLIT;
+    T* part = nullptr;
+    int64_t* slot_row = nullptr;
+    LB_TRY(check_cuda(cudaMallocAsync((void**)&part, nchunks * 2 * k * sizeof(T), st), "alloc(part)"));
+    int rc = check_cuda(cudaMallocAsync((void**)&slot_row, nchunks * 2 * sizeof(int64_t), st),
+                        "alloc(slot_row)");
+    if (rc == LAPIS_B200_OK)
+      rc = check_cuda(cudaMemsetAsync(slot_row, 0xff, nchunks * 2 * sizeof(int64_t), st), "memset");
+    const size_t smem = (size_t)SPMM_WARPS * k * sizeof(T);
+    if (rc == LAPIS_B200_OK && smem > 48 * 1024) {
+      rc = check_cuda(cudaFuncSetAttribute(spmm_chunk_kernel<T, RP, CI>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                      "smem attr");
+      if (rc == LAPIS_B200_OK && smem > 200 * 1024)
+        rc = fail(LAPIS_B200_ERR_UNSUPPORTED, "spmm: k too large for long-row staging");
+    }
+    if (rc == LAPIS_B200_OK) {
+      spmm_chunk_kernel<T, RP, CI><<<(unsigned)nchunks, SPMM_WARPS * 32, smem, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+          part, slot_row);
+      rc = check_launch("spmm_chunk_kernel");
+    }
+    if (rc == LAPIS_B200_OK) {
+      spmm_combine_kernel<T, RP><<<(unsigned)nchunks, 64, 0, st>>>(k, (const RP*)rowptr, part,
+                                                                  slot_row, (T*)Y, ldy);
+      rc = check_launch("spmm_combine_kernel");
+    }
+    if (part) cudaFreeAsync(part, st);
+    if (slot_row) cudaFreeAsync(slot_row, st);
+    return rc;
+  }
+};
+
+int spmm_csr(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const void* rowptr,
+             int rp_bytes, const void* colind, int ci_bytes, const void* values, const void* X,
+             int64_t ldx, void* Y, int64_t ldy, int dtype, cudaStream_t st) {
+  if (nrows < 0 || ncols < 0 || nnz < 0 || k < 0) return fail(LAPIS_B200_ERR_ARG, "spmm: negative extent");
+  if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "spmm: unsupported dtype");
+  if ((rp_bytes != 4 && rp_bytes != 8) || (ci_bytes != 4 && ci_bytes != 8))
+    return fail(LAPIS_B200_ERR_ARG, "spmm: index widths must be 4 or 8 bytes");
+  if (ldx < k || ldy < k) return fail(LAPIS_B200_ERR_ARG, "spmm: leading dimension < k");
+  if (!rowptr || (nrows > 0 && k > 0 && !Y) || (nnz > 0 && (!colind || !values || !X)))
+    return fail(LAPIS_B200_ERR_ARG, "spmm: null operand");
+  if (nrows == 0 || k == 0) return LAPIS_B200_OK;
+#define LB_SPMM(T)                                                                             \
+  if (rp_bytes == 8 && ci_bytes == 4) return SpmmOp<T, int64_t, int32_t>::run(nrows, nnz, k, rowptr, colind, values, X, ldx, Y, ldy, st); \
+  if (rp_bytes == 8 && ci_bytes == 8) return SpmmOp<T, int64_t, int64_t>::run(nrows, nnz, k, rowptr, colind, values, X, ldx, Y, ldy, st); \
+  if (rp_bytes == 4 && ci_bytes == 4) return SpmmOp<T, int32_t, int32_t>::run(nrows, nnz, k, rowptr, colind, values, X, ldx, Y, ldy, st); \
+  return SpmmOp<T, int32_t, int64_t>::run(nrows, nnz, k, rowptr, colind, values, X, ldx, Y, ldy, st);
+  switch (dtype) {
+    case LAPIS_B200_F64: { LB_SPMM(double) }
+    case LAPIS_B200_F32: { LB_SPMM(float) }
+    case LAPIS_B200_I64: { LB_SPMM(long long) }
+    case LAPIS_B200_I32: { LB_SPMM(int) }
+  }
+#undef LB_SPMM
+  return fail(LAPIS_B200_ERR_ARG, "spmm: unsupported dtype");
+}
+
+}  // namespace lapis_b200

@@ -1,0 +1,359 @@
+// spmv.cu — CSR SpMV for sm_100a.
+//
+// Semantics: interp.py:798-812 (_h_spmv_csr) — y[i] = sum over
+// j in [rowptr[i], max(rowptr[i], rowptr[i+1])) of values[j] * x[colind[j]],
+// ascending j, each op rounded (interp.py:168-183).
+//
+// Two kernels:
+//
+// 1. spmv_tile_kernel (default, vector_length = 0): a "row-stream tile".
+//    Work units are rows + nonzeros (key(r) = rowptr[r] - rowptr[0] + r is
+//    strictly increasing); tile c owns the rows whose key falls in
+//    [c*TILE_KEYS, (c+1)*TILE_KEYS), so every tile holds a bounded number of
+//    rows AND nonzeros whatever the row-length distribution (empty rows and
+//    hub rows included).  The CTA streams its contiguous nonzero range with
+//    16-byte loads (colind, values), gathers x through the read-only path,
+//    stages the products in shared memory, and then ONE thread per row sums
+//    that row's products in ascending order with non-contracted mul/add: the
+//    result is bit-identical to the reference for every row of <= LONG_ROW
+//    entries.  A longer row can only be the last row of its tile; it is
+//    reduced by the whole CTA (strided partials + fixed tree).
+//    The tile -> first-row table is a structure-only plan (partition kernel),
+//    computed per call or cached in a lapis_b200_csr_plan.
+//
+// 2. spmv_vector_kernel<VL> (vector_length = VL): the emitted TeamPolicy
+//    mapping of golden/cpp/spmv.hpp:45-66 — one row per VL lanes
+//    (Kokkos thread -> sub-warp, vector -> lane), ThreadVectorRange reduce as
+//    a shuffle tree, single(PerThread) store by lane 0.
+#include "common.cuh"
+
+namespace lapis_b200 {
+
+constexpr int TILE_THREADS = 256;
+constexpr int TILE_KEYS = 1024;                   // rows + nonzeros owned per tile
+constexpr int LONG_ROW = 512;                     // last-row length handled in shared memory
+constexpr int TILE_CAP = TILE_KEYS + LONG_ROW;    // products staged per tile
+
+// ---------------------------------------------------------------- plan
+template <class RP>
+__global__ void tile_partition_kernel(int64_t nrows, const RP* __restrict__ rowptr,
+                                      int64_t ntiles, int64_t* __restrict__ tile_row) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r > nrows) return;
+  const int64_t base = (int64_t)rowptr[0];
+  const int64_t key = (int64_t)rowptr[r] - base + r;
+  const int64_t keyprev = (r == 0) ? -1 : (int64_t)rowptr[r - 1] - base + (r - 1);
+  // tile c starts at row r iff c*TILE_KEYS lies in (keyprev, key]
+  const int64_t c0 = (keyprev < 0) ? 0 : keyprev / TILE_KEYS + 1;
+  const int64_t c1 = (r == nrows) ? ntiles : key / TILE_KEYS;
+  for (int64_t c = c0; c <= c1 && c <= ntiles; ++c) tile_row[c] = r;
+}
+
+// ------------------------------------------------------------ vector loads
+template <class T>
+__device__ __forceinline__ void load4(const T* p, T out[4]) {
+  if constexpr (sizeof(T) == 4) {
+    int4 v = ld_stream(reinterpret_cast<const int4*>(p));
+    const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) memcpy(&out[q], &w[q], 4);
+  } else {
+    longlong2 a = ld_stream(reinterpret_cast<const longlong2*>(p));
+    longlong2 b = ld_stream(reinterpret_cast<const longlong2*>(p + 2));
+    const long long w[4] = {a.x, a.y, b.x, b.y};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) memcpy(&out[q], &w[q], 8);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T block_sum(T part, T* scratch) {
+  // fixed-order tree: xor butterfly inside each warp, then warp 0 folds the
+  // per-warp partials in ascending warp order
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) part = Arith<T>::add(part, shfl_xor(part, off));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = part;
+  __syncthreads();
+  T tot = Arith<T>::zero();
+  if (threadIdx.x == 0)
+    for (int w = 0; w < TILE_THREADS / 32; ++w) tot = Arith<T>::add(tot, scratch[w]);
+  return tot;
+}
+
+// ------------------------------------------------------------ tile kernel
+template <class T, class RP, class CI, bool VEC>
+__global__ void __launch_bounds__(TILE_THREADS)
+spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
+                 const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
+                 const int64_t* __restrict__ tile_row) {
+  __shared__ T prod[TILE_CAP];
+  __shared__ int64_t rps[TILE_KEYS + 1];
+  const int64_t c = blockIdx.x;
+  const int64_t r_begin = tile_row[c], r_end = tile_row[c + 1];
+  const int nr = (int)(r_end - r_begin);
+  if (nr <= 0) return;
+  for (int i = threadIdx.x; i <= nr; i += TILE_THREADS) rps[i] = (int64_t)rowptr[r_begin + i];
+  __syncthreads();
+  const int64_t s = rps[0];
+  const int64_t e = rps[nr];
+  const bool long_last = (e - rps[nr - 1]) > LONG_ROW;
+  const int64_t et = long_last ? rps[nr - 1] : e;
+
+  // ---- phase A: stream [s, et), products -> shared memory
+  if (VEC) {
+    const int64_t g0 = s >> 2, g1 = (et + 3) >> 2;
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += TILE_THREADS) {
+      const int64_t j0 = g << 2;
+      if (j0 >= s && j0 + 4 <= et) {
+        CI ci[4];
+        T v[4];
+        load4(colind + j0, ci);
+        load4(values + j0, v);
+        T xv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xv[q] = __ldg(x + (int64_t)ci[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) prod[j0 - s + q] = Arith<T>::mul(v[q], xv[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t j = j0 + q;
+          if (j >= s && j < et)
+            prod[j - s] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
+        }
+      }
+    }
+  } else {
+    for (int64_t j = s + threadIdx.x; j < et; j += TILE_THREADS)
+      prod[j - s] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
+  }
+  __syncthreads();
+
+  // ---- phase B: one thread per row, ascending sequential sum (reference order)
+  const int nshort = long_last ? nr - 1 : nr;
+  for (int i = threadIdx.x; i < nshort; i += TILE_THREADS) {
+    const int64_t b = rps[i] - s;
+    const int64_t len = rps[i + 1] - rps[i];
+    T acc = Arith<T>::zero();
+    for (int64_t q = 0; q < len; ++q) acc = Arith<T>::add(acc, prod[b + q]);
+    y[r_begin + i] = acc;
+  }
+
+  // ---- long last row: whole-CTA strided partials + fixed tree
+  if (long_last) {
+    const int64_t rs = rps[nr - 1];
+    T part = Arith<T>::zero();
+#pragma unroll 4
+    for (int64_t j = rs + threadIdx.x; j < e; j += TILE_THREADS)
+      part = Arith<T>::add(part, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
+    T tot = block_sum(part, prod);
+    if (threadIdx.x == 0) y[r_end - 1] = tot;
+  }
+}
+
+// ---------------------------------------------------------- vector kernel
+template <class T, class RP, class CI, int VL>
+__global__ void __launch_bounds__(256)
+spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
+                   const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
+  const int lane = threadIdx.x & (VL - 1);
+  const int64_t groups_per_grid = (int64_t)gridDim.x * (blockDim.x / VL);
+  const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VL;
+  const int64_t my_off = (threadIdx.x & 31) / VL;
+  // warp-uniform trip count so every lane reaches the shuffles
+  for (int64_t wrow = warp_first; wrow < nrows; wrow += groups_per_grid) {
+    const int64_t row = wrow + my_off;
+    T acc = Arith<T>::zero();
+    if (row < nrows) {
+      const int64_t b = (int64_t)rowptr[row];
+      int64_t e = (int64_t)rowptr[row + 1];
+      if (e < b) e = b;  // interp.py:808 range(begin, max(begin, end))
+      for (int64_t j = b + lane; j < e; j += VL)
+        acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
+    }
+#pragma unroll
+    for (int off = VL / 2; off >= 1; off >>= 1) acc = Arith<T>::add(acc, shfl_xor(acc, off, VL));
+    if (lane == 0 && row < nrows) y[row] = acc;
+  }
+}
+
+// ================================================================ host side
+struct CsrPlanImpl {
+  int64_t nrows = 0, nnz = 0, ntiles = 0;
+  int64_t* tile_row = nullptr;  // device, ntiles + 1 entries
+  int device = 0;
+};
+
+static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
+  const int64_t total = nrows + nnz;
+  return (total + TILE_KEYS - 1) / TILE_KEYS;
+}
+
+int launch_partition(int64_t nrows, const void* rowptr, int rp_bytes, int64_t ntiles,
+                     int64_t* tile_row, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t blocks = (nrows + 1 + threads - 1) / threads;
+  if (rp_bytes == 8)
+    tile_partition_kernel<int64_t><<<(unsigned)blocks, threads, 0, st>>>(
+        nrows, (const int64_t*)rowptr, ntiles, tile_row);
+  else
+    tile_partition_kernel<int32_t><<<(unsigned)blocks, threads, 0, st>>>(
+        nrows, (const int32_t*)rowptr, ntiles, tile_row);
+  return check_launch("tile_partition_kernel");
+}
+
+template <class T, class RP, class CI>
+static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
+                         const void* values, const void* x, void* y, const int64_t* tile_row,
+                         cudaStream_t st) {
+  const bool vec = ((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0);
+  if (ntiles > 0x7fffffffLL) return fail(LAPIS_B200_ERR_ARG, "spmv: too many tiles");
+  if (vec)
+    spmv_tile_kernel<T, RP, CI, true><<<(unsigned)ntiles, TILE_THREADS, 0, st>>>(
+        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row);
+  else
+    spmv_tile_kernel<T, RP, CI, false><<<(unsigned)ntiles, TILE_THREADS, 0, st>>>(
+        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row);
+  return check_launch("spmv_tile_kernel");
+}
+
+template <class T, class RP, class CI, int VL>
+static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind,
+                           const void* values, const void* x, void* y, cudaStream_t st) {
+  const int threads = 256;
+  int64_t blocks = (nrows * VL + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 64;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  spmv_vector_kernel<T, RP, CI, VL><<<(unsigned)blocks, threads, 0, st>>>(
+      nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y);
+  return check_launch("spmv_vector_kernel");
+}
+
+template <class T, class RP, class CI>
+static int dispatch_vl(int vl, int64_t nrows, const void* rowptr, const void* colind,
+                       const void* values, const void* x, void* y, cudaStream_t st) {
+  switch (vl) {
+    case 1: return launch_vector_t<T, RP, CI, 1>(nrows, rowptr, colind, values, x, y, st);
+    case 2: return launch_vector_t<T, RP, CI, 2>(nrows, rowptr, colind, values, x, y, st);
+    case 4: return launch_vector_t<T, RP, CI, 4>(nrows, rowptr, colind, values, x, y, st);
+    case 8: return launch_vector_t<T, RP, CI, 8>(nrows, rowptr, colind, values, x, y, st);
+    case 16: return launch_vector_t<T, RP, CI, 16>(nrows, rowptr, colind, values, x, y, st);
+    case 32: return launch_vector_t<T, RP, CI, 32>(nrows, rowptr, colind, values, x, y, st);
+  }
+  return fail(LAPIS_B200_ERR_ARG, "spmv: vector_length must be 0 or a power of two <= 32");
+}
+
+// type dispatch: F(T, RP, CI)
+template <template <class, class, class> class F, class... Args>
+static int dispatch_types(int dtype, int rp_bytes, int ci_bytes, Args&&... args) {
+#define LB_CI(T, RP)                                                        \
+  return ci_bytes == 8 ? F<T, RP, int64_t>::run(std::forward<Args>(args)...) \
+                       : F<T, RP, int32_t>::run(std::forward<Args>(args)...)
+#define LB_RP(T) \
+  if (rp_bytes == 8) { LB_CI(T, int64_t); } else { LB_CI(T, int32_t); }
+  switch (dtype) {
+    case LAPIS_B200_F64: LB_RP(double)
+    case LAPIS_B200_F32: LB_RP(float)
+    case LAPIS_B200_I64: LB_RP(long long)
+    case LAPIS_B200_I32: LB_RP(int)
+  }
+#undef LB_RP
+#undef LB_CI
+  return fail(LAPIS_B200_ERR_ARG, "unsupported dtype");
+}
+
+template <class T, class RP, class CI>
+struct TileOp {
+  static int run(int64_t ntiles, const void* rp, const void* ci, const void* v, const void* x,
+                 void* y, const int64_t* tr, cudaStream_t st) {
+    return launch_tile_t<T, RP, CI>(ntiles, rp, ci, v, x, y, tr, st);
+  }
+};
+template <class T, class RP, class CI>
+struct VecOp {
+  static int run(int vl, int64_t nrows, const void* rp, const void* ci, const void* v,
+                 const void* x, void* y, cudaStream_t st) {
+    return dispatch_vl<T, RP, CI>(vl, nrows, rp, ci, v, x, y, st);
+  }
+};
+
+static int validate(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int rp_bytes,
+                    const void* colind, int ci_bytes, const void* values, const void* x,
+                    const void* y, int dtype) {
+  if (nrows < 0 || ncols < 0 || nnz < 0) return fail(LAPIS_B200_ERR_ARG, "spmv: negative extent");
+  if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "spmv: unsupported dtype");
+  if ((rp_bytes != 4 && rp_bytes != 8) || (ci_bytes != 4 && ci_bytes != 8))
+    return fail(LAPIS_B200_ERR_ARG, "spmv: index widths must be 4 or 8 bytes");
+  if (!rowptr) return fail(LAPIS_B200_ERR_ARG, "spmv: null rowptr");
+  if (nrows > 0 && !y) return fail(LAPIS_B200_ERR_ARG, "spmv: null y");
+  if (nnz > 0 && (!colind || !values || !x)) return fail(LAPIS_B200_ERR_ARG, "spmv: null operand");
+  if (rp_bytes == 4 && nnz > 0x7fffffffLL)
+    return fail(LAPIS_B200_ERR_ARG, "spmv: nnz exceeds an i32 rowptr");
+  return LAPIS_B200_OK;
+}
+
+int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int rp_bytes,
+             const void* colind, int ci_bytes, const void* values, const void* x, void* y,
+             int dtype, int vl, cudaStream_t st) {
+  LB_TRY(validate(nrows, ncols, nnz, rowptr, rp_bytes, colind, ci_bytes, values, x, y, dtype));
+  if (nrows == 0) return LAPIS_B200_OK;
+  if (vl != 0) return dispatch_types<VecOp>(dtype, rp_bytes, ci_bytes, vl, nrows, rowptr, colind,
+                                            values, x, y, st);
+  const int64_t ntiles = ntiles_for(nrows, nnz);
+  int64_t* tile_row = nullptr;
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&tile_row, (ntiles + 1) * sizeof(int64_t), st),
+                    "cudaMallocAsync(tile_row)"));
+  int rc = launch_partition(nrows, rowptr, rp_bytes, ntiles, tile_row, st);
+  if (rc == LAPIS_B200_OK)
+    rc = dispatch_types<TileOp>(dtype, rp_bytes, ci_bytes, ntiles, rowptr, colind, values, x, y,
+                                (const int64_t*)tile_row, st);
+  cudaFreeAsync(tile_row, st);
+  return rc;
+}
+
+int csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes,
+                    cudaStream_t st, void** out) {
+  if (!out) return fail(LAPIS_B200_ERR_ARG, "plan: null out pointer");
+  *out = nullptr;
+  if (nrows < 0 || nnz < 0 || !rowptr || (rp_bytes != 4 && rp_bytes != 8))
+    return fail(LAPIS_B200_ERR_ARG, "plan: bad arguments");
+  auto* p = new CsrPlanImpl();
+  p->nrows = nrows;
+  p->nnz = nnz;
+  p->ntiles = ntiles_for(nrows, nnz);
+  cudaGetDevice(&p->device);
+  int rc = check_cuda(cudaMalloc((void**)&p->tile_row, (p->ntiles + 1) * sizeof(int64_t)),
+                      "cudaMalloc(plan)");
+  if (rc == LAPIS_B200_OK && nrows > 0)
+    rc = launch_partition(nrows, rowptr, rp_bytes, p->ntiles, p->tile_row, st);
+  if (rc != LAPIS_B200_OK) {
+    if (p->tile_row) cudaFree(p->tile_row);
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return LAPIS_B200_OK;
+}
+
+int csr_plan_destroy(void* plan) {
+  auto* p = static_cast<CsrPlanImpl*>(plan);
+  if (!p) return LAPIS_B200_OK;
+  int rc = check_cuda(cudaFree(p->tile_row), "cudaFree(plan)");
+  delete p;
+  return rc;
+}
+
+int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* colind, int ci_bytes,
+                  const void* values, const void* x, void* y, int dtype, cudaStream_t st) {
+  auto* p = static_cast<CsrPlanImpl*>(plan);
+  if (!p) return fail(LAPIS_B200_ERR_ARG, "spmv: null plan");
+  LB_TRY(validate(p->nrows, 0, p->nnz, rowptr, rp_bytes, colind, ci_bytes, values, x, y, dtype));
+  if (p->nrows == 0) return LAPIS_B200_OK;
+  return dispatch_types<TileOp>(dtype, rp_bytes, ci_bytes, p->ntiles, rowptr, colind, values, x,
+                                y, (const int64_t*)p->tile_row, st);
+}
+
+}  // namespace lapis_b200

@@ -1,0 +1,254 @@
+"""Tensor-level entry points: PyTorch CUDA tensors in, C ABI calls out.
+
+PyTorch is plumbing here (device memory, streams); every operation is one or
+more of our sm_100a kernels launched through include/lapis_b200.h on the
+tensor's current CUDA stream.  Tensors are passed zero-copy (data_ptr) the way
+the reference passes unmanaged Kokkos Views; they must be CUDA, row-major
+contiguous (LayoutRight, runtime_header.py:39-41) and of a supported dtype.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi
+from ._capi import BackendError, check
+
+_DTYPES = {torch.float32: _capi.F32, torch.float64: _capi.F64,
+           torch.int32: _capi.I32, torch.int64: _capi.I64}
+_COMBINERS = {"add": _capi.ADD, "mul": _capi.MUL, "min": _capi.MIN, "max": _capi.MAX}
+_MODES = {"auto": _capi.GEMM_AUTO, "tf32x3": _capi.GEMM_TF32X3, "dmma": _capi.GEMM_DMMA,
+          "exact": _capi.GEMM_EXACT}
+_initialised: set[int] = set()
+
+
+def _device_init(t: torch.Tensor) -> None:
+    idx = t.device.index if t.device.index is not None else torch.cuda.current_device()
+    if idx not in _initialised:
+        check(_capi.lib().lapis_b200_init(idx), "lapis_b200_init")
+        _initialised.add(idx)
+
+
+def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise BackendError(f"{name} must be a CUDA tensor (no CPU fallback)", _capi.ERR_ARG)
+    if not t.is_contiguous():
+        raise BackendError(f"{name} must be row-major contiguous", _capi.ERR_ARG)
+    _device_init(t)
+    return t
+
+
+def _dtype(t: torch.Tensor, name: str) -> int:
+    if t.dtype not in _DTYPES:
+        raise BackendError(f"{name}: unsupported dtype {t.dtype}", _capi.ERR_ARG)
+    return _DTYPES[t.dtype]
+
+
+def _idx_bytes(t: torch.Tensor, name: str) -> int:
+    if t.dtype not in (torch.int32, torch.int64):
+        raise BackendError(f"{name} must hold int32 or int64 indices", _capi.ERR_ARG)
+    return t.element_size()
+
+
+def _stream(stream) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None and t.numel() > 0 else None)
+
+
+def csr_vector_length(nrows: int, nnz: int, max_vector_length: int = 32) -> int:
+    """The reference's CSR vector-length hint (loop_mapping.py:224-246)."""
+    return int(_capi.lib().lapis_b200_csr_vector_length(nrows, nnz, max_vector_length))
+
+
+def _check_values(values, x, y):
+    if not (values.dtype == x.dtype == y.dtype):
+        raise BackendError("values/x/y element types must match (dialect.py:811)", _capi.ERR_ARG)
+
+
+def spmv_csr(rowptr, colind, values, x, y=None, *, vector_length: int = 0, nnz: int | None = None,
+             stream=None) -> torch.Tensor:
+    """y = A x for CSR A (sparse.spmv_csr, interp.py:798-812).  y is overwritten
+    and returned (allocated when None).  ``nnz`` may be passed to avoid reading
+    rowptr[N] back from the device."""
+    for t, n in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (x, "x")):
+        _dev(t, n)
+    nrows = rowptr.numel() - 1
+    if y is None:
+        y = torch.empty(max(nrows, 0), dtype=values.dtype, device=values.device)
+    _dev(y, "y")
+    _check_values(values, x, y)
+    if nrows < 0:
+        raise BackendError("rowptr must have at least one entry", _capi.ERR_ARG)
+    if y.numel() != nrows:
+        raise BackendError(f"y has extent {y.numel()}, rowptr implies {nrows} rows", _capi.ERR_ARG)
+    if nnz is None:
+        nnz = int(rowptr[-1].item() - rowptr[0].item()) if nrows >= 0 else 0
+    check(_capi.lib().lapis_b200_spmv_csr(
+        nrows, x.numel(), nnz, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"), _ptr(colind),
+        _idx_bytes(colind, "colind"), _ptr(values), _ptr(x), _ptr(y), _dtype(values, "values"),
+        vector_length, _stream(stream)), "spmv_csr")
+    return y
+
+
+class CsrPlan:
+    """Structure-only analysis of one rowptr (tile -> first-row table), reused
+    by every SpMV on that structure.  Holds a device allocation."""
+
+    def __init__(self, rowptr: torch.Tensor, nnz: int | None = None, stream=None):
+        _dev(rowptr, "rowptr")
+        self.nrows = rowptr.numel() - 1
+        self.nnz = int(rowptr[-1].item() - rowptr[0].item()) if nnz is None else int(nnz)
+        self.rowptr = rowptr
+        handle = C.c_void_p()
+        check(_capi.lib().lapis_b200_csr_plan_create(
+            self.nrows, self.nnz, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"), _stream(stream),
+            C.byref(handle)), "csr_plan_create")
+        self._handle = handle
+
+    def spmv(self, colind, values, x, y=None, *, stream=None) -> torch.Tensor:
+        for t, n in ((colind, "colind"), (values, "values"), (x, "x")):
+            _dev(t, n)
+        if y is None:
+            y = torch.empty(self.nrows, dtype=values.dtype, device=values.device)
+        _dev(y, "y")
+        _check_values(values, x, y)
+        check(_capi.lib().lapis_b200_spmv_csr_plan(
+            self._handle, _ptr(self.rowptr), _idx_bytes(self.rowptr, "rowptr"), _ptr(colind),
+            _idx_bytes(colind, "colind"), _ptr(values), _ptr(x), _ptr(y),
+            _dtype(values, "values"), _stream(stream)), "spmv_csr_plan")
+        return y
+
+    def close(self) -> None:
+        if getattr(self, "_handle", None) is not None and self._handle.value:
+            check(_capi.lib().lapis_b200_csr_plan_destroy(self._handle), "csr_plan_destroy")
+            self._handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def spmm_csr(rowptr, colind, values, X, Y=None, *, nnz: int | None = None, stream=None):
+    """Y = A X for CSR A and row-major dense X [ncols, k] (oracle/ir/spmm.mlir)."""
+    for t, n in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (X, "X")):
+        _dev(t, n)
+    if X.dim() != 2:
+        raise BackendError("X must be rank 2", _capi.ERR_ARG)
+    nrows = rowptr.numel() - 1
+    k = X.shape[1]
+    if Y is None:
+        Y = torch.empty((nrows, k), dtype=values.dtype, device=values.device)
+    _dev(Y, "Y")
+    _check_values(values, X, Y)
+    if tuple(Y.shape) != (nrows, k):
+        raise BackendError(f"Y has shape {tuple(Y.shape)}, expected {(nrows, k)}", _capi.ERR_ARG)
+    if nnz is None:
+        nnz = int(rowptr[-1].item() - rowptr[0].item())
+    check(_capi.lib().lapis_b200_spmm_csr(
+        nrows, X.shape[0], nnz, k, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"), _ptr(colind),
+        _idx_bytes(colind, "colind"), _ptr(values), _ptr(X), k, _ptr(Y), k,
+        _dtype(values, "values"), _stream(stream)), "spmm_csr")
+    return Y
+
+
+def gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
+    """C = A B (LAPIS::gemm, runtime_header.py:249-266; linalg.matmul)."""
+    _dev(A, "A"); _dev(B, "B")
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0]:
+        raise BackendError(f"matmul shape mismatch {tuple(A.shape)} x {tuple(B.shape)}",
+                           _capi.ERR_ARG)
+    if A.dtype != B.dtype:
+        raise BackendError("element types must match", _capi.ERR_ARG)
+    m, k = A.shape
+    n = B.shape[1]
+    if C_out is None:
+        C_out = torch.empty((m, n), dtype=A.dtype, device=A.device)
+    _dev(C_out, "C")
+    if tuple(C_out.shape) != (m, n) or C_out.dtype != A.dtype:
+        raise BackendError("C has the wrong shape or dtype", _capi.ERR_ARG)
+    check(_capi.lib().lapis_b200_gemm(m, n, k, _ptr(A), k, _ptr(B), n, _ptr(C_out), n,
+                                      _dtype(A, "A"), _MODES[mode], _stream(stream)), "gemm")
+    return C_out
+
+
+def batch_gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
+    """C[b] = A[b] B[b] (linalg.batch_matmul, interp.py:746-763)."""
+    _dev(A, "A"); _dev(B, "B")
+    if A.dim() != 3 or B.dim() != 3 or A.shape[0] != B.shape[0] or A.shape[2] != B.shape[1]:
+        raise BackendError("batch_matmul shape mismatch", _capi.ERR_ARG)
+    nb, m, k = A.shape
+    n = B.shape[2]
+    if C_out is None:
+        C_out = torch.empty((nb, m, n), dtype=A.dtype, device=A.device)
+    _dev(C_out, "C")
+    check(_capi.lib().lapis_b200_batch_gemm(nb, m, n, k, _ptr(A), _ptr(B), _ptr(C_out),
+                                            _dtype(A, "A"), _MODES[mode], _stream(stream)),
+          "batch_gemm")
+    return C_out
+
+
+def gemv(A, x, y=None, *, stream=None):
+    """y = A x (LAPIS::gemv, runtime_header.py:268-282; linalg.matvec)."""
+    _dev(A, "A"); _dev(x, "x")
+    if A.dim() != 2 or x.dim() != 1 or A.shape[1] != x.shape[0]:
+        raise BackendError("matvec shape mismatch", _capi.ERR_ARG)
+    m, n = A.shape
+    if y is None:
+        y = torch.empty(m, dtype=A.dtype, device=A.device)
+    _dev(y, "y")
+    check(_capi.lib().lapis_b200_gemv(m, n, _ptr(A), n, _ptr(x), _ptr(y), _dtype(A, "A"),
+                                      _stream(stream)), "gemv")
+    return y
+
+
+def reduce2d(src, axis: int, combiner: str = "add", out=None, *, stream=None):
+    """linalg.reduce over one axis of a rank-2 array (interp.py:779-795)."""
+    _dev(src, "src")
+    if src.dim() != 2:
+        raise BackendError("reduce2d expects a rank-2 source", _capi.ERR_ARG)
+    rows, cols = src.shape
+    if out is None:
+        out = torch.empty(rows if axis == 1 else cols, dtype=src.dtype, device=src.device)
+    _dev(out, "out")
+    check(_capi.lib().lapis_b200_reduce_2d(rows, cols, _ptr(src), _ptr(out), axis,
+                                           _COMBINERS[combiner], _dtype(src, "src"),
+                                           _stream(stream)), "reduce_2d")
+    return out
+
+
+def relu(x, y=None, *, stream=None):
+    """y = (x > 0) ? x : 0 (linalg.elementwise cmpf ogt + select)."""
+    _dev(x, "x")
+    if y is None:
+        y = torch.empty_like(x)
+    _dev(y, "y")
+    check(_capi.lib().lapis_b200_relu(x.numel(), _ptr(x), _ptr(y), _dtype(x, "x"),
+                                      _stream(stream)), "relu")
+    return y
+
+
+def synth_stencil(points: int, n: int, row_begin: int = 0, row_end: int | None = None,
+                  device="cuda", stream=None):
+    """Generate rows [row_begin, row_end) of the 5-point (2-D) or 27-point (3-D)
+    stencil matrix on the device: (rowptr int64 rebased, colind int32, values f64)."""
+    N = n * n if points == 5 else n ** 3
+    row_end = N if row_end is None else row_end
+    rows = row_end - row_begin
+    rowptr = torch.empty(rows + 1, dtype=torch.int64, device=device)
+    _dev(rowptr, "rowptr")
+    check(_capi.lib().lapis_b200_synth_stencil(points, n, row_begin, row_end, _ptr(rowptr), None,
+                                               None, _stream(stream)), "synth_stencil(rowptr)")
+    nnz = int(rowptr[-1].item())
+    colind = torch.empty(nnz, dtype=torch.int32, device=device)
+    values = torch.empty(nnz, dtype=torch.float64, device=device)
+    check(_capi.lib().lapis_b200_synth_stencil(points, n, row_begin, row_end, _ptr(rowptr),
+                                               _ptr(colind), _ptr(values), _stream(stream)),
+          "synth_stencil")
+    return rowptr, colind, values

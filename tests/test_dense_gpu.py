@@ -1,0 +1,89 @@
+"""Parity of the dense kernels (matmul, matvec, batch_matmul, parallel_reduce,
+ReLU) with the reference fixtures; the EXACT mode and the row-sequential
+kernels follow the reference order and must be bit-identical."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2509_25605_b200 as lb
+from conftest import bits_equal, golden_names, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["matmul_i32", "matmul_f64", "matmul_f64_kl", "matmul_dyn_f32",
+                                  "matmul_dyn_f64"])
+def test_golden_matmul_exact_mode(cuda_device, name):
+    g = load_golden(name)
+    A, B = g["inputs"][:2]
+    assert bits_equal(host(lb.gemm(cu(A), cu(B), mode="exact")), g["outputs"][0])
+
+
+@pytest.mark.parametrize("name", ["matmul_f64", "matmul_dyn_f32", "matmul_dyn_f64", "matmul_i32"])
+def test_golden_matmul_auto_mode(cuda_device, name):
+    g = load_golden(name)
+    A, B = g["inputs"][:2]
+    got = host(lb.gemm(cu(A), cu(B)))
+    want = g["outputs"][0]
+    tol = {np.dtype(np.float64): 1e-12, np.dtype(np.float32): 1e-5}.get(want.dtype, 0)
+    ok, msg = O.diff_outputs([got], [want], tol)
+    assert ok, msg
+
+
+@pytest.mark.parametrize("name", ["matvec_f64", "matvec_f64_kl", "matvec_dyn"])
+def test_golden_matvec_bitexact(cuda_device, name):
+    g = load_golden(name)
+    A, x = g["inputs"][:2]
+    assert bits_equal(host(lb.gemv(cu(A), cu(x))), g["outputs"][0])
+
+
+def test_golden_batch_matmul_bitexact(cuda_device):
+    g = load_golden("batch_matmul_f32")
+    A, B = g["inputs"]
+    assert bits_equal(host(lb.batch_gemm(cu(A), cu(B), mode="exact")), g["outputs"][0])
+
+
+@pytest.mark.parametrize("name", golden_names("reduce_"))
+def test_golden_reduce_bitexact(cuda_device, name):
+    g = load_golden(name)
+    if name == "reduce_add_f64":
+        comb, axis = "add", 1
+    else:
+        _, comb, ax, _ = name.split("_")
+        axis = int(ax[2:])
+    assert bits_equal(host(lb.reduce2d(cu(g["inputs"][0]), axis, comb)), g["outputs"][0])
+
+
+def test_relu_select_semantics(cuda_device):
+    x = np.array([1.5, -2.0, 0.0, -0.0, np.nan, np.inf, -np.inf, 3e-310])
+    assert bits_equal(host(lb.relu(cu(x))), O.relu(x))
+    assert bits_equal(host(lb.relu(cu(x.astype(np.float32)))), O.relu(x.astype(np.float32)))
+
+
+@pytest.mark.parametrize("m,n,k", [(129, 65, 257), (1, 300, 5), (64, 64, 64)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int32, np.int64])
+def test_exact_gemm_random_shapes(cuda_device, m, n, k, dtype):
+    rng = np.random.default_rng(m * n + k)
+    if np.issubdtype(dtype, np.integer):
+        A = rng.integers(-2**20, 2**20, (m, k)).astype(dtype)
+        B = rng.integers(-2**20, 2**20, (k, n)).astype(dtype)
+    else:
+        A = rng.uniform(-1, 1, (m, k)).astype(dtype)
+        B = rng.uniform(-1, 1, (k, n)).astype(dtype)
+    assert bits_equal(host(lb.gemm(cu(A), cu(B), mode="exact")), O.matmul(A, B))
+
+
+def test_gemv_large_bitexact(cuda_device):
+    rng = np.random.default_rng(2)
+    A = rng.uniform(-1, 1, (3001, 777))
+    x = rng.uniform(-1, 1, 777)
+    assert bits_equal(host(lb.gemv(cu(A), cu(x))), O.matvec(A, x))

@@ -1,0 +1,175 @@
+"""Parity of the sm_100a CSR SpMV kernels with the reference.
+
+* every reference-generated fixture (tests/golden/spmv*.npz): bit-exact for the
+  default row-stream kernel, within diff_outputs tolerance (interp.py:1050) for
+  the emitted-mapping vector kernels (VL = 1 is sequential, hence bit-exact);
+* larger seeded ragged / power-law / stencil matrices against the C oracle:
+  rows of <= 512 entries bit-exact, longer rows within tolerance;
+* the 1M-row 5-point Laplacian (config 1) against the reference's OWN emitted
+  C++ on its serial stub (oracle/_ref), bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2509_25605_b200 as lb
+from conftest import bits_equal, golden_names, load_golden
+from matrices import powerlaw_csr, ragged_csr, stencil_csr
+from oracle import oracle as O
+from oracle import ref as R
+
+pytestmark = pytest.mark.gpu
+TOL = {np.dtype(np.float64): 1e-12, np.dtype(np.float32): 1e-5}
+LONG_ROW = 512
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def assert_close(got, want, rowptr=None):
+    """Ints exact; floats within diff_outputs tolerance; rows <= LONG_ROW bit-exact."""
+    got, want = np.asarray(got), np.asarray(want)
+    if want.dtype.kind in "iu":
+        assert np.array_equal(got, want)
+        return
+    ok, msg = O.diff_outputs([got], [want], TOL[want.dtype])
+    assert ok, msg
+    if rowptr is not None:
+        short = np.diff(rowptr) <= LONG_ROW
+        assert bits_equal(got[short], want[short])
+
+
+@pytest.mark.parametrize("name", golden_names("spmv"))
+def test_golden_tile_kernel_bitexact(cuda_device, name):
+    g = load_golden(name)
+    rowptr, colind, values, x, _ = g["inputs"]
+    y = lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x))
+    assert bits_equal(host(y), g["outputs"][0]), name
+
+
+@pytest.mark.parametrize("name", golden_names("spmv"))
+@pytest.mark.parametrize("vl", [1, 2, 4, 8, 16, 32])
+def test_golden_vector_kernel(cuda_device, name, vl):
+    g = load_golden(name)
+    rowptr, colind, values, x, _ = g["inputs"]
+    y = host(lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x), vector_length=vl))
+    if vl == 1:
+        assert bits_equal(y, g["outputs"][0])
+    else:
+        assert_close(y, g["outputs"][0])
+
+
+def test_golden_hint_drives_vector_kernel(cuda_device):
+    # the emitted code computes VL from rowptr (golden/cpp/spmv.hpp:17-33)
+    for name in golden_names("spmv"):
+        g = load_golden(name)
+        rowptr = g["inputs"][0]
+        n = rowptr.shape[0] - 1
+        assert lb.csr_vector_length(n, int(rowptr[-1])) == g["hints"][0]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("idx", ["i64/i32", "i64/i64", "i32/i32"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int64, np.int32])
+def test_ragged_with_long_rows(cuda_device, seed, idx, dtype):
+    rng = np.random.default_rng(seed)
+    rowptr, colind, values = ragged_csr(rng, 5000, 3000, max_len=60, empty_every=13,
+                                        long_rows={7: 2999, 4000: 700, 4001: 513, 4999: 1500},
+                                        dtype=dtype)
+    x = (rng.integers(-9, 9, 3000) if np.issubdtype(dtype, np.integer)
+         else rng.uniform(-1, 1, 3000)).astype(dtype)
+    rp_t, ci_t = idx.split("/")
+    rp = rowptr.astype(np.int64 if rp_t == "i64" else np.int32)
+    ci = colind.astype(np.int64 if ci_t == "i64" else np.int32)
+    want = O.spmv_csr(rowptr, colind, values, x)
+    got = host(lb.spmv_csr(cu(rp), cu(ci), cu(values), cu(x)))
+    assert_close(got, want, rowptr)
+    got8 = host(lb.spmv_csr(cu(rp), cu(ci), cu(values), cu(x), vector_length=8))
+    assert_close(got8, want)
+
+
+def test_plan_reuse_and_offset_rowptr(cuda_device):
+    rng = np.random.default_rng(5)
+    rowptr, colind, values = powerlaw_csr(rng, 20000, mean=12.0)
+    x = rng.uniform(-1, 1, 20000)
+    want = O.spmv_csr(rowptr, colind, values, x)
+    rp = cu(rowptr)
+    plan = lb.CsrPlan(rp)
+    ci, v = cu(colind), cu(values)
+    for _ in range(3):
+        assert_close(host(plan.spmv(ci, v, cu(x))), want, rowptr)
+    x2 = rng.uniform(-1, 1, 20000)
+    assert_close(host(plan.spmv(ci, v, cu(x2))), O.spmv_csr(rowptr, colind, values, x2), rowptr)
+    plan.close()
+    # a row-block window: rowptr not starting at 0 (subview semantics)
+    r0, r1 = 3000, 9000
+    sub = lb.spmv_csr(cu(rowptr[r0:r1 + 1]), ci, v, cu(x))
+    assert bits_equal(host(sub)[np.diff(rowptr[r0:r1 + 1]) <= LONG_ROW],
+                      want[r0:r1][np.diff(rowptr[r0:r1 + 1]) <= LONG_ROW])
+
+
+def test_empty_and_degenerate(cuda_device):
+    y = lb.spmv_csr(cu(np.zeros(1, np.int64)), cu(np.zeros(0, np.int32)), cu(np.zeros(0)),
+                    cu(np.zeros(3)))
+    assert y.numel() == 0
+    y = lb.spmv_csr(cu(np.zeros(6, np.int64)), cu(np.zeros(0, np.int32)), cu(np.zeros(0)),
+                    cu(np.ones(5)))
+    assert host(y).tolist() == [0.0] * 5
+    # 100k empty rows then one row: ownership of empty rows spans many tiles
+    rowptr = np.zeros(100_002, np.int64)
+    rowptr[-1] = 3
+    y = host(lb.spmv_csr(cu(rowptr), cu(np.array([0, 1, 2], np.int32)), cu(np.ones(3)),
+                         cu(np.array([1.0, 2.0, 3.0]))))
+    assert y[-1] == 6.0 and not y[:-1].any()
+
+
+def test_errors_are_raised_not_aborted(cuda_device):
+    rp, ci, v, x = cu(np.array([0, 1], np.int64)), cu(np.array([0], np.int32)), cu(np.ones(1)), cu(np.ones(1))
+    with pytest.raises(lb.BackendError):
+        lb.spmv_csr(rp, ci, v, x, torch.empty(5, dtype=torch.float64, device="cuda"))
+    with pytest.raises(lb.BackendError):
+        lb.spmv_csr(rp, ci, v, x, vector_length=3)
+    with pytest.raises(lb.BackendError):
+        lb.spmv_csr(rp, ci, v, x.float())
+
+
+def test_device_stencil_matches_host_structure(cuda_device):
+    for points, n in ((5, 37), (27, 11), (27, 1), (5, 2)):
+        rowptr, colind, values = stencil_csr(points, n)
+        drp, dci, dv = lb.synth_stencil(points, n)
+        assert np.array_equal(host(drp), rowptr)
+        assert np.array_equal(host(dci), colind)
+        assert bits_equal(host(dv), values)
+        # a row block, rebased
+        N = rowptr.size - 1
+        r0, r1 = N // 3, 2 * N // 3
+        brp, bci, bv = lb.synth_stencil(points, n, r0, r1)
+        assert np.array_equal(host(brp), rowptr[r0:r1 + 1] - rowptr[r0])
+        assert np.array_equal(host(bci), colind[rowptr[r0]:rowptr[r1]])
+
+
+def test_stencil27_1m_rows_bitexact_vs_oracle(cuda_device):
+    n = 100
+    rp, ci, v = lb.synth_stencil(27, n)
+    x = np.random.default_rng(5).uniform(-1, 1, n ** 3)
+    y = host(lb.spmv_csr(rp, ci, v, cu(x)))
+    want = O.spmv_csr(host(rp), host(ci), host(v), x)
+    assert bits_equal(y, want)
+    y32 = host(lb.spmv_csr(rp, ci, v, cu(x), vector_length=32))
+    assert_close(y32, want)
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
+def test_config1_laplacian_bitexact_vs_reference_emitted_cpp(cuda_device):
+    # config 1: 1M rows, 4,996,000 nnz, the reference's own CPU path
+    rp, ci, v = lb.synth_stencil(5, 1000)
+    assert int(rp[-1]) == 4_996_000
+    x = np.random.default_rng(1).uniform(-1, 1, 1_000_000)
+    y = host(lb.spmv_csr(rp, ci, v, cu(x)))
+    yref, _ = R.spmv_csr(host(rp), host(ci).astype(np.int64), host(v), x, threads=4)
+    assert bits_equal(y, yref)
