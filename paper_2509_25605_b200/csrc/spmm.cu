@@ -16,9 +16,12 @@
 //   warp order) into slot (q, 0 = row began earlier | 1 = row begins here).
 // Kernel 3 (spmm_combine_kernel): for each long row, sums its chunk partials
 //   in chunk order.  Deterministic (fixed association), parity by tolerance.
+//   fp32 long rows take spmm_seq_long_kernel instead (exact reference order).
 // This splits power-law hub rows (config 3: max 117,686 entries) over many
 // SMs without atomics.
 #include "common.cuh"
+
+#include <type_traits>
 
 namespace lapis_b200 {
 
@@ -99,6 +102,31 @@ __device__ __forceinline__ int64_t first_row_ending_after(int64_t nrows, const R
     if ((int64_t)rowptr[mid + 1] > value) hi = mid; else lo = mid + 1;
   }
   return lo;
+}
+
+// fp32 long rows instead follow the reference's exact sequential order (a
+// reassociated fp32 sum of thousands of terms can move by more than the 1e-5
+// contract): the CTA of the chunk where such a row BEGINS walks the whole row,
+// one thread per dense column, and writes Y directly.
+template <class T, class RP, class CI>
+__global__ void __launch_bounds__(SPMM_WARPS * 32)
+spmm_seq_long_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+                     const CI* __restrict__ colind, const T* __restrict__ values,
+                     const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  const int64_t q = blockIdx.x;
+  const int64_t base = (int64_t)rowptr[0];
+  const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
+  const int64_t r = first_row_ending_after(nrows, rowptr, hi - 1);
+  if (r >= nrows) return;
+  const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
+  if (b < lo || b >= hi || e - b <= SPLIT) return;
+  for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
+    T acc = Arith<T>::zero();
+#pragma unroll 8
+    for (int64_t j = b; j < e; ++j)
+      acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(X + (int64_t)colind[j] * ldx + col)));
+    Y[r * ldy + col] = acc;
+  }
 }
 
 template <class T, class RP, class CI>
@@ -184,6 +212,12 @@ struct SpmmOp {
     LB_TRY(check_launch("spmm_row_kernel"));
     if (nnz <= SPLIT) return LAPIS_B200_OK;  // no row can be long
     const int64_t nchunks = (nnz + SPLIT - 1) / SPLIT;
+    if constexpr (std::is_same<T, float>::value) {
+      spmm_seq_long_kernel<T, RP, CI><<<(unsigned)nchunks, SPMM_WARPS * 32, 0, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+          (T*)Y, ldy);
+      return check_launch("spmm_seq_long_kernel");
+    }
     T* part = nullptr;
     int64_t* slot_row = nullptr;
     LB_TRY(check_cuda(cudaMallocAsync((void**)&part, nchunks * 2 * k * sizeof(T), st), "alloc(part)"));

@@ -27,26 +27,37 @@
 //    a shuffle tree, single(PerThread) store by lane 0.
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace lapis_b200 {
 
 constexpr int TILE_THREADS = 256;
-constexpr int TILE_KEYS = 1024;                   // rows + nonzeros owned per tile
+constexpr int TILE_KEYS = 2048;                   // rows + nonzeros owned per tile
 constexpr int LONG_ROW = 512;                     // last-row length handled in shared memory
 constexpr int TILE_CAP = TILE_KEYS + LONG_ROW;    // products staged per tile
+constexpr int TILE_GROUPS = (TILE_CAP / 4 + 1 + TILE_THREADS - 1) / TILE_THREADS;  // 4-wide groups per thread
 
 // ---------------------------------------------------------------- plan
+// tile_row[c]  = first row owned by tile c (c in [0, ntiles]; tile_row[ntiles] = nrows)
+// tile_nnz[c]  = rowptr[tile_row[c]] (absolute), so a tile can start streaming
+//                its nonzeros without first reading rowptr
 template <class RP>
 __global__ void tile_partition_kernel(int64_t nrows, const RP* __restrict__ rowptr,
-                                      int64_t ntiles, int64_t* __restrict__ tile_row) {
+                                      int64_t ntiles, int64_t* __restrict__ tile_row,
+                                      int64_t* __restrict__ tile_nnz) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r > nrows) return;
   const int64_t base = (int64_t)rowptr[0];
-  const int64_t key = (int64_t)rowptr[r] - base + r;
+  const int64_t rp = (int64_t)rowptr[r];
+  const int64_t key = rp - base + r;
   const int64_t keyprev = (r == 0) ? -1 : (int64_t)rowptr[r - 1] - base + (r - 1);
   // tile c starts at row r iff c*TILE_KEYS lies in (keyprev, key]
   const int64_t c0 = (keyprev < 0) ? 0 : keyprev / TILE_KEYS + 1;
   const int64_t c1 = (r == nrows) ? ntiles : key / TILE_KEYS;
-  for (int64_t c = c0; c <= c1 && c <= ntiles; ++c) tile_row[c] = r;
+  for (int64_t c = c0; c <= c1 && c <= ntiles; ++c) {
+    tile_row[c] = r;
+    tile_nnz[c] = rp;
+  }
 }
 
 // ------------------------------------------------------------ vector loads
@@ -68,7 +79,7 @@ __device__ __forceinline__ void load4(const T* p, T out[4]) {
 
 template <class T>
 __device__ __forceinline__ T block_sum(T part, T* scratch) {
-  // fixed-order tree: xor butterfly inside each warp, then warp 0 folds the
+  // fixed-order tree: xor butterfly inside each warp, then thread 0 folds the
   // per-warp partials in ascending warp order
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) part = Arith<T>::add(part, shfl_xor(part, off));
@@ -82,49 +93,99 @@ __device__ __forceinline__ T block_sum(T part, T* scratch) {
   return tot;
 }
 
+// long row (> LONG_ROW entries) owned by this CTA.  fp64 / ints: strided
+// partials + fixed tree (ints are order-independent; fp64 stays far inside the
+// 1e-12 contract).  fp32: the reference's exact sequential order — products
+// staged chunk by chunk, thread 0 folds them in ascending order — because a
+// reassociated fp32 sum of thousands of terms can differ from the reference's
+// own rounding by more than 1e-5.
+template <class T, class CI>
+__device__ void long_row(int64_t rs, int64_t e, const CI* __restrict__ colind,
+                         const T* __restrict__ values, const T* __restrict__ x, T* prod,
+                         T* __restrict__ yout) {
+  if constexpr (sizeof(T) == 4 && !std::is_integral<T>::value) {
+    T acc = Arith<T>::zero();
+    for (int64_t c0 = rs; c0 < e; c0 += TILE_CAP) {
+      const int64_t c1 = (c0 + TILE_CAP < e) ? c0 + TILE_CAP : e;
+      __syncthreads();
+      for (int64_t j = c0 + threadIdx.x; j < c1; j += TILE_THREADS)
+        prod[j - c0] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int64_t j = 0; j < c1 - c0; ++j) acc = Arith<T>::add(acc, prod[j]);
+    }
+    if (threadIdx.x == 0) *yout = acc;
+  } else {
+    T part = Arith<T>::zero();
+#pragma unroll 4
+    for (int64_t j = rs + threadIdx.x; j < e; j += TILE_THREADS)
+      part = Arith<T>::add(part, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
+    T tot = block_sum(part, prod);
+    if (threadIdx.x == 0) *yout = tot;
+  }
+}
+
 // ------------------------------------------------------------ tile kernel
 template <class T, class RP, class CI, bool VEC>
-__global__ void __launch_bounds__(TILE_THREADS)
+__global__ void __launch_bounds__(TILE_THREADS, 4)
 spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                  const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
-                 const int64_t* __restrict__ tile_row) {
+                 const int64_t* __restrict__ tile_row, const int64_t* __restrict__ tile_nnz) {
   __shared__ T prod[TILE_CAP];
-  __shared__ int64_t rps[TILE_KEYS + 1];
+  __shared__ int32_t rps[TILE_KEYS + 1];   // rowptr[r_begin + i] - s, i < nr
   const int64_t c = blockIdx.x;
   const int64_t r_begin = tile_row[c], r_end = tile_row[c + 1];
   const int nr = (int)(r_end - r_begin);
   if (nr <= 0) return;
-  for (int i = threadIdx.x; i <= nr; i += TILE_THREADS) rps[i] = (int64_t)rowptr[r_begin + i];
-  __syncthreads();
-  const int64_t s = rps[0];
-  const int64_t e = rps[nr];
-  const bool long_last = (e - rps[nr - 1]) > LONG_ROW;
-  const int64_t et = long_last ? rps[nr - 1] : e;
+  const int64_t s = tile_nnz[c];       // = rowptr[r_begin]
+  const int64_t e = tile_nnz[c + 1];   // = rowptr[r_end]
+  const int64_t et = (e - s > TILE_CAP) ? s + TILE_CAP : e;   // streamed range [s, et)
 
-  // ---- phase A: stream [s, et), products -> shared memory
+  // row offsets of the owned rows (independent of the stream below)
+  for (int i = threadIdx.x; i < nr; i += TILE_THREADS) {
+    const int64_t v = (int64_t)rowptr[r_begin + i] - s;
+    rps[i] = (int32_t)(v < TILE_CAP ? v : TILE_CAP);
+  }
+
+  // ---- phase A: stream [s, et): every load of the thread issued before use
   if (VEC) {
     const int64_t g0 = s >> 2, g1 = (et + 3) >> 2;
-    for (int64_t g = g0 + threadIdx.x; g < g1; g += TILE_THREADS) {
+    CI ci[TILE_GROUPS][4];
+    T v[TILE_GROUPS][4];
+#pragma unroll
+    for (int u = 0; u < TILE_GROUPS; ++u) {
+      const int64_t g = g0 + threadIdx.x + (int64_t)u * TILE_THREADS;
       const int64_t j0 = g << 2;
-      if (j0 >= s && j0 + 4 <= et) {
-        CI ci[4];
-        T v[4];
-        load4(colind + j0, ci);
-        load4(values + j0, v);
-        T xv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) xv[q] = __ldg(x + (int64_t)ci[q]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) prod[j0 - s + q] = Arith<T>::mul(v[q], xv[q]);
+      if (g < g1 && j0 >= s && j0 + 4 <= et) {
+        load4(colind + j0, ci[u]);
+        load4(values + j0, v[u]);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int64_t j = j0 + q;
-          if (j >= s && j < et)
-            prod[j - s] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
+          const bool in = g < g1 && j >= s && j < et;
+          ci[u][q] = in ? colind[j] : CI(0);
+          v[u][q] = in ? values[j] : T(0);
         }
       }
     }
+    T xv[TILE_GROUPS][4];
+#pragma unroll
+    for (int u = 0; u < TILE_GROUPS; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t g = g0 + threadIdx.x + (int64_t)u * TILE_THREADS;
+        const int64_t j = (g << 2) + q;
+        xv[u][q] = (g < g1 && j >= s && j < et) ? __ldg(x + (int64_t)ci[u][q]) : T(0);
+      }
+#pragma unroll
+    for (int u = 0; u < TILE_GROUPS; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t g = g0 + threadIdx.x + (int64_t)u * TILE_THREADS;
+        const int64_t j = (g << 2) + q;
+        if (g < g1 && j >= s && j < et) prod[j - s] = Arith<T>::mul(v[u][q], xv[u][q]);
+      }
   } else {
     for (int64_t j = s + threadIdx.x; j < et; j += TILE_THREADS)
       prod[j - s] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
@@ -132,25 +193,19 @@ spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
   __syncthreads();
 
   // ---- phase B: one thread per row, ascending sequential sum (reference order)
+  const int64_t last_b = (nr > 0) ? (int64_t)rps[nr - 1] : 0;
+  const bool long_last = (e - s) - last_b > LONG_ROW;
   const int nshort = long_last ? nr - 1 : nr;
   for (int i = threadIdx.x; i < nshort; i += TILE_THREADS) {
-    const int64_t b = rps[i] - s;
-    const int64_t len = rps[i + 1] - rps[i];
+    const int b = rps[i];
+    const int end = (i + 1 < nr) ? rps[i + 1] : (int)(e - s);
     T acc = Arith<T>::zero();
-    for (int64_t q = 0; q < len; ++q) acc = Arith<T>::add(acc, prod[b + q]);
+    for (int q = b; q < end; ++q) acc = Arith<T>::add(acc, prod[q]);
     y[r_begin + i] = acc;
   }
 
-  // ---- long last row: whole-CTA strided partials + fixed tree
-  if (long_last) {
-    const int64_t rs = rps[nr - 1];
-    T part = Arith<T>::zero();
-#pragma unroll 4
-    for (int64_t j = rs + threadIdx.x; j < e; j += TILE_THREADS)
-      part = Arith<T>::add(part, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
-    T tot = block_sum(part, prod);
-    if (threadIdx.x == 0) y[r_end - 1] = tot;
-  }
+  if (long_last)
+    long_row<T, CI>(s + last_b, e, colind, values, x, prod, y + r_end - 1);
 }
 
 // ---------------------------------------------------------- vector kernel
@@ -182,7 +237,7 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
 // ================================================================ host side
 struct CsrPlanImpl {
   int64_t nrows = 0, nnz = 0, ntiles = 0;
-  int64_t* tile_row = nullptr;  // device, ntiles + 1 entries
+  int64_t* tile_row = nullptr;  // device, 2 * (ntiles + 1): tile_row then tile_nnz
   int device = 0;
 };
 
@@ -195,12 +250,13 @@ int launch_partition(int64_t nrows, const void* rowptr, int rp_bytes, int64_t nt
                      int64_t* tile_row, cudaStream_t st) {
   const int threads = 256;
   const int64_t blocks = (nrows + 1 + threads - 1) / threads;
+  int64_t* tile_nnz = tile_row + (ntiles + 1);
   if (rp_bytes == 8)
     tile_partition_kernel<int64_t><<<(unsigned)blocks, threads, 0, st>>>(
-        nrows, (const int64_t*)rowptr, ntiles, tile_row);
+        nrows, (const int64_t*)rowptr, ntiles, tile_row, tile_nnz);
   else
     tile_partition_kernel<int32_t><<<(unsigned)blocks, threads, 0, st>>>(
-        nrows, (const int32_t*)rowptr, ntiles, tile_row);
+        nrows, (const int32_t*)rowptr, ntiles, tile_row, tile_nnz);
   return check_launch("tile_partition_kernel");
 }
 
@@ -210,12 +266,15 @@ static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
                          cudaStream_t st) {
   const bool vec = ((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0);
   if (ntiles > 0x7fffffffLL) return fail(LAPIS_B200_ERR_ARG, "spmv: too many tiles");
+  const int64_t* tile_nnz = tile_row + (ntiles + 1);
   if (vec)
     spmv_tile_kernel<T, RP, CI, true><<<(unsigned)ntiles, TILE_THREADS, 0, st>>>(
-        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row);
+        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row,
+        tile_nnz);
   else
     spmv_tile_kernel<T, RP, CI, false><<<(unsigned)ntiles, TILE_THREADS, 0, st>>>(
-        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row);
+        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row,
+        tile_nnz);
   return check_launch("spmv_tile_kernel");
 }
 
@@ -304,7 +363,7 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
                                             values, x, y, st);
   const int64_t ntiles = ntiles_for(nrows, nnz);
   int64_t* tile_row = nullptr;
-  LB_TRY(check_cuda(cudaMallocAsync((void**)&tile_row, (ntiles + 1) * sizeof(int64_t), st),
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&tile_row, 2 * (ntiles + 1) * sizeof(int64_t), st),
                     "cudaMallocAsync(tile_row)"));
   int rc = launch_partition(nrows, rowptr, rp_bytes, ntiles, tile_row, st);
   if (rc == LAPIS_B200_OK)
@@ -325,7 +384,7 @@ int csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes
   p->nnz = nnz;
   p->ntiles = ntiles_for(nrows, nnz);
   cudaGetDevice(&p->device);
-  int rc = check_cuda(cudaMalloc((void**)&p->tile_row, (p->ntiles + 1) * sizeof(int64_t)),
+  int rc = check_cuda(cudaMalloc((void**)&p->tile_row, 2 * (p->ntiles + 1) * sizeof(int64_t)),
                       "cudaMalloc(plan)");
   if (rc == LAPIS_B200_OK && nrows > 0)
     rc = launch_partition(nrows, rowptr, rp_bytes, p->ntiles, p->tile_row, st);
