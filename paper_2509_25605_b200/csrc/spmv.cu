@@ -31,11 +31,11 @@
 
 namespace lapis_b200 {
 
-constexpr int TILE_THREADS = 256;
-constexpr int TILE_KEYS = 2048;                   // rows + nonzeros owned per tile
+constexpr int TILE_THREADS = 128;
+constexpr int TILE_KEYS = 1024;                   // rows + nonzeros owned per tile
 constexpr int LONG_ROW = 512;                     // last-row length handled in shared memory
 constexpr int TILE_CAP = TILE_KEYS + LONG_ROW;    // products staged per tile
-constexpr int TILE_GROUPS = (TILE_CAP / 4 + 1 + TILE_THREADS - 1) / TILE_THREADS;  // 4-wide groups per thread
+constexpr int STAGES = 3;                         // TMA ring depth (tiles in flight per CTA)
 
 // ---------------------------------------------------------------- plan
 // tile_row[c]  = first row owned by tile c (c in [0, ntiles]; tile_row[ntiles] = nrows)
@@ -102,7 +102,7 @@ __device__ __forceinline__ T block_sum(T part, T* scratch) {
 template <class T, class CI>
 __device__ void long_row(int64_t rs, int64_t e, const CI* __restrict__ colind,
                          const T* __restrict__ values, const T* __restrict__ x, T* prod,
-                         T* __restrict__ yout) {
+                         T* scratch, T* __restrict__ yout) {
   if constexpr (sizeof(T) == 4 && !std::is_integral<T>::value) {
     T acc = Arith<T>::zero();
     for (int64_t c0 = rs; c0 < e; c0 += TILE_CAP) {
@@ -120,92 +120,154 @@ __device__ void long_row(int64_t rs, int64_t e, const CI* __restrict__ colind,
 #pragma unroll 4
     for (int64_t j = rs + threadIdx.x; j < e; j += TILE_THREADS)
       part = Arith<T>::add(part, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
-    T tot = block_sum(part, prod);
+    T tot = block_sum(part, scratch);
     if (threadIdx.x == 0) *yout = tot;
   }
 }
 
 // ------------------------------------------------------------ tile kernel
-template <class T, class RP, class CI, bool VEC>
-__global__ void __launch_bounds__(TILE_THREADS, 4)
+// Persistent: CTA b processes tiles b, b + G, b + 2G, ... (G = gridDim.x).
+// Thread 0 keeps STAGES tiles' nonzero streams (colind and values ranges,
+// 16-byte aligned) in flight with cp.async.bulk (TMA engine) into a shared
+// memory ring, completion counted on one mbarrier per stage; the tile plan for
+// the tile STAGES ahead is prefetched into registers one iteration early.  All
+// 128 threads then gather x for the landed tile (read-only path), write the
+// products in place, and sum rows sequentially (reference order).
+template <class T, class CI>
+struct StreamSmem {
+  static constexpr int CI_ELEMS = TILE_CAP + 16 / sizeof(CI) * 2;  // + alignment slack
+  static constexpr int V_ELEMS = TILE_CAP + 16 / sizeof(T) * 2;
+  static constexpr size_t CI_BYTES = (CI_ELEMS * sizeof(CI) + 127) / 128 * 128;
+  static constexpr size_t V_BYTES = (V_ELEMS * sizeof(T) + 127) / 128 * 128;
+  static constexpr size_t STAGE_BYTES = CI_BYTES + V_BYTES;
+  static constexpr size_t TOTAL = STAGES * STAGE_BYTES;
+};
+
+template <class T, class RP, class CI>
+__global__ void __launch_bounds__(TILE_THREADS)
 spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                  const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
-                 const int64_t* __restrict__ tile_row, const int64_t* __restrict__ tile_nnz) {
-  __shared__ T prod[TILE_CAP];
-  __shared__ int32_t rps[TILE_KEYS + 1];   // rowptr[r_begin + i] - s, i < nr
-  const int64_t c = blockIdx.x;
-  const int64_t r_begin = tile_row[c], r_end = tile_row[c + 1];
-  const int nr = (int)(r_end - r_begin);
-  if (nr <= 0) return;
-  const int64_t s = tile_nnz[c];       // = rowptr[r_begin]
-  const int64_t e = tile_nnz[c + 1];   // = rowptr[r_end]
-  const int64_t et = (e - s > TILE_CAP) ? s + TILE_CAP : e;   // streamed range [s, et)
+                 const int64_t* __restrict__ tile_row, const int64_t* __restrict__ tile_nnz,
+                 int64_t ntiles, int tma_ok) {
+  using L = StreamSmem<T, CI>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[STAGES];
+  __shared__ int64_t meta[STAGES][4];     // r_begin, r_end, s, e
+  __shared__ int32_t moff[STAGES][3];     // colind offset, values offset, direct flag
+  __shared__ int32_t rps[TILE_KEYS + 1];  // row starts relative to s
+  __shared__ T scratch[TILE_THREADS / 32];
+  const int tid = threadIdx.x;
+  constexpr int64_t CA = 16 / sizeof(CI), VA = 16 / sizeof(T);
 
-  // row offsets of the owned rows (independent of the stream below)
-  for (int i = threadIdx.x; i < nr; i += TILE_THREADS) {
-    const int64_t v = (int64_t)rowptr[r_begin + i] - s;
-    rps[i] = (int32_t)(v < TILE_CAP ? v : TILE_CAP);
-  }
+  auto sci = [&](int st) { return reinterpret_cast<CI*>(smem + st * L::STAGE_BYTES); };
+  auto sv = [&](int st) { return reinterpret_cast<T*>(smem + st * L::STAGE_BYTES + L::CI_BYTES); };
 
-  // ---- phase A: stream [s, et): every load of the thread issued before use
-  if (VEC) {
-    const int64_t g0 = s >> 2, g1 = (et + 3) >> 2;
-    CI ci[TILE_GROUPS][4];
-    T v[TILE_GROUPS][4];
-#pragma unroll
-    for (int u = 0; u < TILE_GROUPS; ++u) {
-      const int64_t g = g0 + threadIdx.x + (int64_t)u * TILE_THREADS;
-      const int64_t j0 = g << 2;
-      if (g < g1 && j0 >= s && j0 + 4 <= et) {
-        load4(colind + j0, ci[u]);
-        load4(values + j0, v[u]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t j = j0 + q;
-          const bool in = g < g1 && j >= s && j < et;
-          ci[u][q] = in ? colind[j] : CI(0);
-          v[u][q] = in ? values[j] : T(0);
-        }
-      }
+  // the streams end at rowptr[nrows]; an aligned-up bulk copy must not pass it
+  const int64_t nnz_end = tid == 0 ? tile_nnz[ntiles] : 0;
+  // thread 0 only: put tile (rb, re, s0, e0) in flight on `st`
+  auto issue = [&](int st, int64_t rb, int64_t re, int64_t s0, int64_t e0) {
+    const int64_t et = (e0 - s0 > TILE_CAP) ? s0 + TILE_CAP : e0;
+    const int64_t sc = s0 & ~(CA - 1), ec = (et + CA - 1) & ~(CA - 1);
+    const int64_t sv0 = s0 & ~(VA - 1), ev = (et + VA - 1) & ~(VA - 1);
+    const bool direct = !tma_ok || re <= rb || et <= s0 || ec > nnz_end || ev > nnz_end;
+    meta[st][0] = rb; meta[st][1] = re; meta[st][2] = s0; meta[st][3] = e0;
+    moff[st][0] = direct ? 0 : (int32_t)(s0 - sc);
+    moff[st][1] = direct ? 0 : (int32_t)(s0 - sv0);
+    moff[st][2] = direct;
+    if (direct) {
+      mbar_arrive(&full[st]);
+    } else {
+      const uint32_t bc = (uint32_t)((ec - sc) * sizeof(CI)), bv = (uint32_t)((ev - sv0) * sizeof(T));
+      mbar_arrive_expect_tx(&full[st], bc + bv);
+      bulk_g2s(sci(st), colind + sc, bc, &full[st]);
+      bulk_g2s(sv(st), values + sv0, bv, &full[st]);
     }
-    T xv[TILE_GROUPS][4];
-#pragma unroll
-    for (int u = 0; u < TILE_GROUPS; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t g = g0 + threadIdx.x + (int64_t)u * TILE_THREADS;
-        const int64_t j = (g << 2) + q;
-        xv[u][q] = (g < g1 && j >= s && j < et) ? __ldg(x + (int64_t)ci[u][q]) : T(0);
-      }
-#pragma unroll
-    for (int u = 0; u < TILE_GROUPS; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t g = g0 + threadIdx.x + (int64_t)u * TILE_THREADS;
-        const int64_t j = (g << 2) + q;
-        if (g < g1 && j >= s && j < et) prod[j - s] = Arith<T>::mul(v[u][q], xv[u][q]);
-      }
-  } else {
-    for (int64_t j = s + threadIdx.x; j < et; j += TILE_THREADS)
-      prod[j - s] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+    fence_barrier_init();
+    for (int st = 0; st < STAGES; ++st) {
+      const int64_t c = blockIdx.x + (int64_t)st * gridDim.x;
+      if (c < ntiles) issue(st, tile_row[c], tile_row[c + 1], tile_nnz[c], tile_nnz[c + 1]);
+    }
   }
   __syncthreads();
 
-  // ---- phase B: one thread per row, ascending sequential sum (reference order)
-  const int64_t last_b = (nr > 0) ? (int64_t)rps[nr - 1] : 0;
-  const bool long_last = (e - s) - last_b > LONG_ROW;
-  const int nshort = long_last ? nr - 1 : nr;
-  for (int i = threadIdx.x; i < nshort; i += TILE_THREADS) {
-    const int b = rps[i];
-    const int end = (i + 1 < nr) ? rps[i + 1] : (int)(e - s);
-    T acc = Arith<T>::zero();
-    for (int q = b; q < end; ++q) acc = Arith<T>::add(acc, prod[q]);
-    y[r_begin + i] = acc;
-  }
+  for (int64_t it = 0;; ++it) {
+    const int64_t c = blockIdx.x + it * gridDim.x;
+    if (c >= ntiles) break;
+    const int st = (int)(it % STAGES);
+    const uint32_t parity = (uint32_t)((it / STAGES) & 1);
+    // plan of the tile STAGES ahead (consumed at the end of this iteration)
+    const int64_t cn = c + (int64_t)STAGES * gridDim.x;
+    int64_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+    if (tid == 0 && cn < ntiles) { p0 = tile_row[cn]; p1 = tile_row[cn + 1]; p2 = tile_nnz[cn]; p3 = tile_nnz[cn + 1]; }
 
-  if (long_last)
-    long_row<T, CI>(s + last_b, e, colind, values, x, prod, y + r_end - 1);
+    const int64_t rb = meta[st][0], re = meta[st][1], s0 = meta[st][2], e0 = meta[st][3];
+    const int nr = (int)(re - rb);
+    const int64_t et = (e0 - s0 > TILE_CAP) ? s0 + TILE_CAP : e0;
+    // row starts for phase B (global loads, in flight while the stream lands)
+    for (int i = tid; i < nr; i += TILE_THREADS) {
+      const int64_t v = (int64_t)rowptr[rb + i] - s0;
+      rps[i] = (int32_t)(v < TILE_CAP ? v : TILE_CAP);
+    }
+    mbar_wait(&full[st], parity);
+    const int dc = moff[st][0], dv = moff[st][1], direct = moff[st][2];
+    T* prod = sv(st) + dv;          // product of entry j lives at prod[j - s0]
+    if (nr > 0) {
+      const int n = (int)(et - s0);
+      if (!direct) {
+        const CI* cbuf = sci(st) + dc;
+        constexpr int PER = (TILE_CAP + TILE_THREADS - 1) / TILE_THREADS;
+        CI ci[PER];
+        T v[PER];
+        T xv[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int q = tid + u * TILE_THREADS;
+          ci[u] = q < n ? cbuf[q] : CI(0);
+          v[u] = q < n ? prod[q] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int q = tid + u * TILE_THREADS;
+          xv[u] = q < n ? __ldg(x + (int64_t)ci[u]) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int q = tid + u * TILE_THREADS;
+          if (q < n) prod[q] = Arith<T>::mul(v[u], xv[u]);
+        }
+      } else {
+        for (int q = tid; q < n; q += TILE_THREADS)
+          prod[q] = Arith<T>::mul(values[s0 + q], __ldg(x + (int64_t)colind[s0 + q]));
+      }
+    }
+    __syncthreads();
+    if (nr > 0) {
+      // ---- phase B: one thread per row, ascending sequential sum (reference order)
+      const int64_t last_b = rps[nr - 1];
+      const bool long_last = (e0 - s0) - last_b > LONG_ROW;
+      const int nshort = long_last ? nr - 1 : nr;
+      for (int i = tid; i < nshort; i += TILE_THREADS) {
+        const int b = rps[i];
+        const int end = (i + 1 < nr) ? rps[i + 1] : (int)(e0 - s0);
+        T acc = Arith<T>::zero();
+        for (int q = b; q < end; ++q) acc = Arith<T>::add(acc, prod[q]);
+        y[rb + i] = acc;
+      }
+      if (long_last) {
+        __syncthreads();
+        long_row<T, CI>(s0 + last_b, e0, colind, values, x, prod, scratch, y + re - 1);
+      }
+    }
+    __syncthreads();  // every read of stage st is done
+    if (tid == 0 && cn < ntiles) {
+      fence_proxy_async();
+      issue(st, p0, p1, p2, p3);
+    }
+  }
 }
 
 // ---------------------------------------------------------- vector kernel
@@ -264,17 +326,28 @@ template <class T, class RP, class CI>
 static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
                          const void* values, const void* x, void* y, const int64_t* tile_row,
                          cudaStream_t st) {
-  const bool vec = ((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0);
-  if (ntiles > 0x7fffffffLL) return fail(LAPIS_B200_ERR_ARG, "spmv: too many tiles");
+  using L = StreamSmem<T, CI>;
+  auto kern = spmv_tile_kernel<T, RP, CI>;
+  static thread_local int configured_dev = -1;
+  static thread_local int ctas_per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)L::TOTAL), "smem attr (spmv_tile_kernel)"));
+    LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, TILE_THREADS,
+                                                                    L::TOTAL), "occupancy"));
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+    configured_dev = dev;
+  }
+  const int tma_ok = ((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0);
+  int64_t grid = (int64_t)num_sms() * ctas_per_sm;
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
   const int64_t* tile_nnz = tile_row + (ntiles + 1);
-  if (vec)
-    spmv_tile_kernel<T, RP, CI, true><<<(unsigned)ntiles, TILE_THREADS, 0, st>>>(
-        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row,
-        tile_nnz);
-  else
-    spmv_tile_kernel<T, RP, CI, false><<<(unsigned)ntiles, TILE_THREADS, 0, st>>>(
-        (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row,
-        tile_nnz);
+  kern<<<(unsigned)grid, TILE_THREADS, L::TOTAL, st>>>(
+      (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row,
+      tile_nnz, ntiles, tma_ok);
   return check_launch("spmv_tile_kernel");
 }
 
@@ -326,8 +399,8 @@ static int dispatch_types(int dtype, int rp_bytes, int ci_bytes, Args&&... args)
 
 template <class T, class RP, class CI>
 struct TileOp {
-  static int run(int64_t ntiles, const void* rp, const void* ci, const void* v, const void* x,
-                 void* y, const int64_t* tr, cudaStream_t st) {
+  static int run(int64_t ntiles, const void* rp, const void* ci, const void* v,
+                 const void* x, void* y, const int64_t* tr, cudaStream_t st) {
     return launch_tile_t<T, RP, CI>(ntiles, rp, ci, v, x, y, tr, st);
   }
 };
