@@ -27,15 +27,14 @@
 //    a shuffle tree, single(PerThread) store by lane 0.
 #include "common.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace lapis_b200 {
 
-constexpr int TILE_THREADS = 128;
-constexpr int TILE_KEYS = 1024;                   // rows + nonzeros owned per tile
+constexpr int TILE_KEYS = 1024;                   // rows + nonzeros owned per tile (plan grain)
 constexpr int LONG_ROW = 512;                     // last-row length handled in shared memory
 constexpr int TILE_CAP = TILE_KEYS + LONG_ROW;    // products staged per tile
-constexpr int STAGES = 3;                         // TMA ring depth (tiles in flight per CTA)
 
 // ---------------------------------------------------------------- plan
 // tile_row[c]  = first row owned by tile c (c in [0, ntiles]; tile_row[ntiles] = nrows)
@@ -77,7 +76,7 @@ __device__ __forceinline__ void load4(const T* p, T out[4]) {
   }
 }
 
-template <class T>
+template <class T, int NT>
 __device__ __forceinline__ T block_sum(T part, T* scratch) {
   // fixed-order tree: xor butterfly inside each warp, then thread 0 folds the
   // per-warp partials in ascending warp order
@@ -89,7 +88,7 @@ __device__ __forceinline__ T block_sum(T part, T* scratch) {
   __syncthreads();
   T tot = Arith<T>::zero();
   if (threadIdx.x == 0)
-    for (int w = 0; w < TILE_THREADS / 32; ++w) tot = Arith<T>::add(tot, scratch[w]);
+    for (int w = 0; w < NT / 32; ++w) tot = Arith<T>::add(tot, scratch[w]);
   return tot;
 }
 
@@ -99,7 +98,7 @@ __device__ __forceinline__ T block_sum(T part, T* scratch) {
 // staged chunk by chunk, thread 0 folds them in ascending order — because a
 // reassociated fp32 sum of thousands of terms can differ from the reference's
 // own rounding by more than 1e-5.
-template <class T, class CI>
+template <class T, class CI, int NT>
 __device__ void long_row(int64_t rs, int64_t e, const CI* __restrict__ colind,
                          const T* __restrict__ values, const T* __restrict__ x, T* prod,
                          T* scratch, T* __restrict__ yout) {
@@ -108,7 +107,7 @@ __device__ void long_row(int64_t rs, int64_t e, const CI* __restrict__ colind,
     for (int64_t c0 = rs; c0 < e; c0 += TILE_CAP) {
       const int64_t c1 = (c0 + TILE_CAP < e) ? c0 + TILE_CAP : e;
       __syncthreads();
-      for (int64_t j = c0 + threadIdx.x; j < c1; j += TILE_THREADS)
+      for (int64_t j = c0 + threadIdx.x; j < c1; j += NT)
         prod[j - c0] = Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j]));
       __syncthreads();
       if (threadIdx.x == 0)
@@ -118,53 +117,56 @@ __device__ void long_row(int64_t rs, int64_t e, const CI* __restrict__ colind,
   } else {
     T part = Arith<T>::zero();
 #pragma unroll 4
-    for (int64_t j = rs + threadIdx.x; j < e; j += TILE_THREADS)
+    for (int64_t j = rs + threadIdx.x; j < e; j += NT)
       part = Arith<T>::add(part, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
-    T tot = block_sum(part, scratch);
+    T tot = block_sum<T, NT>(part, scratch);
     if (threadIdx.x == 0) *yout = tot;
   }
 }
 
 // ------------------------------------------------------------ tile kernel
 // Persistent: CTA b processes tiles b, b + G, b + 2G, ... (G = gridDim.x).
-// Thread 0 keeps STAGES tiles' nonzero streams (colind and values ranges,
-// 16-byte aligned) in flight with cp.async.bulk (TMA engine) into a shared
-// memory ring, completion counted on one mbarrier per stage; the tile plan for
-// the tile STAGES ahead is prefetched into registers one iteration early.  All
-// 128 threads then gather x for the landed tile (read-only path), write the
-// products in place, and sum rows sequentially (reference order).
-template <class T, class CI>
+// Three things overlap in every iteration `it`:
+//   * the TMA engine streams the nonzeros (colind, values; 16-byte aligned
+//     cp.async.bulk into a ST-deep shared-memory ring, one mbarrier per stage)
+//     of tiles it+2 .. it+ST;
+//   * the x gathers of tile it+1 (read-only path, registers) are in flight;
+//   * tile it's rows are summed sequentially from its staged products.
+// Thread 0 prefetches the plan of tile it+ST into registers at the top of the
+// iteration and refills tile it's stage at the bottom.
+template <class T, class CI, int ST>
 struct StreamSmem {
   static constexpr int CI_ELEMS = TILE_CAP + 16 / sizeof(CI) * 2;  // + alignment slack
   static constexpr int V_ELEMS = TILE_CAP + 16 / sizeof(T) * 2;
   static constexpr size_t CI_BYTES = (CI_ELEMS * sizeof(CI) + 127) / 128 * 128;
   static constexpr size_t V_BYTES = (V_ELEMS * sizeof(T) + 127) / 128 * 128;
   static constexpr size_t STAGE_BYTES = CI_BYTES + V_BYTES;
-  static constexpr size_t TOTAL = STAGES * STAGE_BYTES;
+  static constexpr size_t TOTAL = ST * STAGE_BYTES;
 };
 
-template <class T, class RP, class CI>
-__global__ void __launch_bounds__(TILE_THREADS)
+template <class T, class RP, class CI, int NT, int ST>
+__global__ void __launch_bounds__(NT)
 spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                  const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
                  const int64_t* __restrict__ tile_row, const int64_t* __restrict__ tile_nnz,
                  int64_t ntiles, int tma_ok) {
-  using L = StreamSmem<T, CI>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[STAGES];
-  __shared__ int64_t meta[STAGES][4];     // r_begin, r_end, s, e
-  __shared__ int32_t moff[STAGES][3];     // colind offset, values offset, direct flag
-  __shared__ int32_t rps[TILE_KEYS + 1];  // row starts relative to s
-  __shared__ T scratch[TILE_THREADS / 32];
-  const int tid = threadIdx.x;
+  using L = StreamSmem<T, CI, ST>;
+  constexpr int PER = (TILE_CAP + NT - 1) / NT;        // streamed entries per thread
+  constexpr int RPER = (TILE_KEYS + NT - 1) / NT;      // owned rows per thread
   constexpr int64_t CA = 16 / sizeof(CI), VA = 16 / sizeof(T);
-
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[ST];
+  __shared__ int64_t meta[ST][4];            // r_begin, r_end, s, e
+  __shared__ int32_t moff[ST][3];            // colind offset, values offset, direct flag
+  __shared__ int32_t rps[2][TILE_KEYS + 1];  // row starts relative to s (double-buffered)
+  __shared__ T scratch[NT / 32];
+  const int tid = threadIdx.x;
   auto sci = [&](int st) { return reinterpret_cast<CI*>(smem + st * L::STAGE_BYTES); };
   auto sv = [&](int st) { return reinterpret_cast<T*>(smem + st * L::STAGE_BYTES + L::CI_BYTES); };
 
   // the streams end at rowptr[nrows]; an aligned-up bulk copy must not pass it
   const int64_t nnz_end = tid == 0 ? tile_nnz[ntiles] : 0;
-  // thread 0 only: put tile (rb, re, s0, e0) in flight on `st`
+  // thread 0 only: put tile (rb, re, s0, e0) in flight on stage `st`
   auto issue = [&](int st, int64_t rb, int64_t re, int64_t s0, int64_t e0) {
     const int64_t et = (e0 - s0 > TILE_CAP) ? s0 + TILE_CAP : e0;
     const int64_t sc = s0 & ~(CA - 1), ec = (et + CA - 1) & ~(CA - 1);
@@ -184,88 +186,112 @@ spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
     }
   };
 
+  // gather state of the tile being prepared (held across the row sums of the previous one)
+  T xg[PER];
+  int64_t rpv[RPER];
+  // stage A: wait for tile `k`'s stream, issue its x gathers and rowptr loads
+  auto gather = [&](int64_t k) {
+    const int st = (int)(k % ST);
+    const uint32_t parity = (uint32_t)((k / ST) & 1);
+    const int64_t rb = meta[st][0], re = meta[st][1], s0 = meta[st][2], e0 = meta[st][3];
+    const int nr = (int)(re - rb);
+#pragma unroll
+    for (int u = 0; u < RPER; ++u) {
+      const int i = tid + u * NT;
+      rpv[u] = i < nr ? (int64_t)rowptr[rb + i] : 0;
+    }
+    mbar_wait(&full[st], parity);
+    const int n = nr > 0 ? (int)(((e0 - s0 > TILE_CAP) ? TILE_CAP : e0 - s0)) : 0;
+    const int dc = moff[st][0], direct = moff[st][2];
+    const CI* cbuf = sci(st) + dc;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int q = tid + u * NT;
+      int64_t col = 0;
+      if (q < n) col = direct ? (int64_t)colind[s0 + q] : (int64_t)cbuf[q];
+      xg[u] = q < n ? __ldg(x + col) : T(0);
+    }
+  };
+  // stage C: products of tile `k` in place (values slot) and its row starts
+  auto finish = [&](int64_t k) {
+    const int st = (int)(k % ST);
+    const int64_t rb = meta[st][0], re = meta[st][1], s0 = meta[st][2], e0 = meta[st][3];
+    const int nr = (int)(re - rb);
+    const int n = nr > 0 ? (int)(((e0 - s0 > TILE_CAP) ? TILE_CAP : e0 - s0)) : 0;
+    const int dv = moff[st][1], direct = moff[st][2];
+    T* prod = sv(st) + dv;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int q = tid + u * NT;
+      if (q < n) prod[q] = Arith<T>::mul(direct ? values[s0 + q] : prod[q], xg[u]);
+    }
+    int32_t* rp = rps[k & 1];
+#pragma unroll
+    for (int u = 0; u < RPER; ++u) {
+      const int i = tid + u * NT;
+      if (i < nr) {
+        const int64_t v = rpv[u] - s0;
+        rp[i] = (int32_t)(v < TILE_CAP ? v : TILE_CAP);
+      }
+    }
+  };
+  // stage B: sequential row sums of tile `k` (reference order), long last row
+  auto rows = [&](int64_t k) {
+    const int st = (int)(k % ST);
+    const int64_t rb = meta[st][0], re = meta[st][1], s0 = meta[st][2], e0 = meta[st][3];
+    const int nr = (int)(re - rb);
+    if (nr <= 0) return;
+    const int32_t* rp = rps[k & 1];
+    T* prod = sv(st) + moff[st][1];
+    const int64_t last_b = rp[nr - 1];
+    const bool long_last = (e0 - s0) - last_b > LONG_ROW;
+    const int nshort = long_last ? nr - 1 : nr;
+    for (int i = tid; i < nshort; i += NT) {
+      int q = rp[i];
+      const int end = (i + 1 < nr) ? rp[i + 1] : (int)(e0 - s0);
+      T acc = Arith<T>::zero();
+      for (; q + 4 <= end; q += 4) {
+        const T p0 = prod[q], p1 = prod[q + 1], p2 = prod[q + 2], p3 = prod[q + 3];
+        acc = Arith<T>::add(acc, p0);
+        acc = Arith<T>::add(acc, p1);
+        acc = Arith<T>::add(acc, p2);
+        acc = Arith<T>::add(acc, p3);
+      }
+      for (; q < end; ++q) acc = Arith<T>::add(acc, prod[q]);
+      y[rb + i] = acc;
+    }
+    if (long_last) long_row<T, CI, NT>(s0 + last_b, e0, colind, values, x, prod, scratch, y + re - 1);
+  };
+
   if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < ST; ++st) mbar_init(&full[st], 1);
     fence_barrier_init();
-    for (int st = 0; st < STAGES; ++st) {
+    for (int st = 0; st < ST; ++st) {
       const int64_t c = blockIdx.x + (int64_t)st * gridDim.x;
       if (c < ntiles) issue(st, tile_row[c], tile_row[c + 1], tile_nnz[c], tile_nnz[c + 1]);
     }
+  }
+  __syncthreads();
+  if ((int64_t)blockIdx.x < ntiles) {
+    gather(0);
+    finish(0);
   }
   __syncthreads();
 
   for (int64_t it = 0;; ++it) {
     const int64_t c = blockIdx.x + it * gridDim.x;
     if (c >= ntiles) break;
-    const int st = (int)(it % STAGES);
-    const uint32_t parity = (uint32_t)((it / STAGES) & 1);
-    // plan of the tile STAGES ahead (consumed at the end of this iteration)
-    const int64_t cn = c + (int64_t)STAGES * gridDim.x;
+    const int64_t cn = c + (int64_t)ST * gridDim.x;   // tile refilled at the bottom
     int64_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
     if (tid == 0 && cn < ntiles) { p0 = tile_row[cn]; p1 = tile_row[cn + 1]; p2 = tile_nnz[cn]; p3 = tile_nnz[cn + 1]; }
-
-    const int64_t rb = meta[st][0], re = meta[st][1], s0 = meta[st][2], e0 = meta[st][3];
-    const int nr = (int)(re - rb);
-    const int64_t et = (e0 - s0 > TILE_CAP) ? s0 + TILE_CAP : e0;
-    // row starts for phase B (global loads, in flight while the stream lands)
-    for (int i = tid; i < nr; i += TILE_THREADS) {
-      const int64_t v = (int64_t)rowptr[rb + i] - s0;
-      rps[i] = (int32_t)(v < TILE_CAP ? v : TILE_CAP);
-    }
-    mbar_wait(&full[st], parity);
-    const int dc = moff[st][0], dv = moff[st][1], direct = moff[st][2];
-    T* prod = sv(st) + dv;          // product of entry j lives at prod[j - s0]
-    if (nr > 0) {
-      const int n = (int)(et - s0);
-      if (!direct) {
-        const CI* cbuf = sci(st) + dc;
-        constexpr int PER = (TILE_CAP + TILE_THREADS - 1) / TILE_THREADS;
-        CI ci[PER];
-        T v[PER];
-        T xv[PER];
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int q = tid + u * TILE_THREADS;
-          ci[u] = q < n ? cbuf[q] : CI(0);
-          v[u] = q < n ? prod[q] : T(0);
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int q = tid + u * TILE_THREADS;
-          xv[u] = q < n ? __ldg(x + (int64_t)ci[u]) : T(0);
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int q = tid + u * TILE_THREADS;
-          if (q < n) prod[q] = Arith<T>::mul(v[u], xv[u]);
-        }
-      } else {
-        for (int q = tid; q < n; q += TILE_THREADS)
-          prod[q] = Arith<T>::mul(values[s0 + q], __ldg(x + (int64_t)colind[s0 + q]));
-      }
-    }
+    const bool has_next = c + gridDim.x < ntiles;
+    if (has_next) gather(it + 1);   // A: gathers of tile it+1 in flight
+    rows(it);                       // B: row sums of tile it
+    if (has_next) finish(it + 1);   // C: products of tile it+1
     __syncthreads();
-    if (nr > 0) {
-      // ---- phase B: one thread per row, ascending sequential sum (reference order)
-      const int64_t last_b = rps[nr - 1];
-      const bool long_last = (e0 - s0) - last_b > LONG_ROW;
-      const int nshort = long_last ? nr - 1 : nr;
-      for (int i = tid; i < nshort; i += TILE_THREADS) {
-        const int b = rps[i];
-        const int end = (i + 1 < nr) ? rps[i + 1] : (int)(e0 - s0);
-        T acc = Arith<T>::zero();
-        for (int q = b; q < end; ++q) acc = Arith<T>::add(acc, prod[q]);
-        y[rb + i] = acc;
-      }
-      if (long_last) {
-        __syncthreads();
-        long_row<T, CI>(s0 + last_b, e0, colind, values, x, prod, scratch, y + re - 1);
-      }
-    }
-    __syncthreads();  // every read of stage st is done
     if (tid == 0 && cn < ntiles) {
       fence_proxy_async();
-      issue(st, p0, p1, p2, p3);
+      issue((int)(it % ST), p0, p1, p2, p3);
     }
   }
 }
@@ -322,12 +348,12 @@ int launch_partition(int64_t nrows, const void* rowptr, int rp_bytes, int64_t nt
   return check_launch("tile_partition_kernel");
 }
 
-template <class T, class RP, class CI>
-static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
-                         const void* values, const void* x, void* y, const int64_t* tile_row,
-                         cudaStream_t st) {
-  using L = StreamSmem<T, CI>;
-  auto kern = spmv_tile_kernel<T, RP, CI>;
+template <class T, class RP, class CI, int NT, int ST>
+static int launch_tile_cfg(int64_t ntiles, const void* rowptr, const void* colind,
+                           const void* values, const void* x, void* y, const int64_t* tile_row,
+                           cudaStream_t st) {
+  using L = StreamSmem<T, CI, ST>;
+  auto kern = spmv_tile_kernel<T, RP, CI, NT, ST>;
   static thread_local int configured_dev = -1;
   static thread_local int ctas_per_sm = 0;
   int dev = 0;
@@ -335,7 +361,7 @@ static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
   if (configured_dev != dev) {
     LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)L::TOTAL), "smem attr (spmv_tile_kernel)"));
-    LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, TILE_THREADS,
+    LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, NT,
                                                                     L::TOTAL), "occupancy"));
     if (ctas_per_sm < 1) ctas_per_sm = 1;
     configured_dev = dev;
@@ -345,10 +371,32 @@ static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
   const int64_t* tile_nnz = tile_row + (ntiles + 1);
-  kern<<<(unsigned)grid, TILE_THREADS, L::TOTAL, st>>>(
-      (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, tile_row,
-      tile_nnz, ntiles, tma_ok);
+  kern<<<(unsigned)grid, NT, L::TOTAL, st>>>((const RP*)rowptr, (const CI*)colind,
+                                             (const T*)values, (const T*)x, (T*)y, tile_row,
+                                             tile_nnz, ntiles, tma_ok);
   return check_launch("spmv_tile_kernel");
+}
+
+// kernel shape (threads per CTA, ring depth); LAPIS_B200_SPMV_CFG selects a
+// variant for tuning runs (0 = default)
+static int spmv_cfg() {
+  static int cfg = [] {
+    const char* e = getenv("LAPIS_B200_SPMV_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return cfg;
+}
+
+template <class T, class RP, class CI>
+static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
+                         const void* values, const void* x, void* y, const int64_t* tile_row,
+                         cudaStream_t st) {
+  switch (spmv_cfg()) {
+    case 1: return launch_tile_cfg<T, RP, CI, 128, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st);
+    case 2: return launch_tile_cfg<T, RP, CI, 256, 3>(ntiles, rowptr, colind, values, x, y, tile_row, st);
+    case 3: return launch_tile_cfg<T, RP, CI, 128, 3>(ntiles, rowptr, colind, values, x, y, tile_row, st);
+    default: return launch_tile_cfg<T, RP, CI, 256, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st);
+  }
 }
 
 template <class T, class RP, class CI, int VL>
