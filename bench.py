@@ -190,7 +190,18 @@ class Stencil27Spmv:
     def launches_per_step(self):
         return self.op.launches_per_multiply
 
+    def kernel_name(self):
+        if self.args.vl:
+            return f"spmv_vector_kernel<VL={self.args.vl}> (emitted mapping, tree reduce)"
+        infos = [p.info() for p in self.op.plans.values()]
+        return "; ".join(sorted({i["kernel"] for i in infos})) + " <double,int64,int32>"
+
     def step(self):
+        if self.args.vl:
+            # emitted TeamPolicy mapping with an explicit vector length (no plan)
+            self.lb.spmv_csr(self.rowptr, self.colind, self.values, self.x, self.y,
+                             vector_length=self.args.vl, nnz=self.nnz_local)
+            return
         self.op.multiply(self.x, self.y, stream=self.stream)
 
     # e2e through the public API with host buffers: DualView lazy sync of x's
@@ -305,6 +316,8 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--vl", type=int, default=0,
+                    help="time the emitted-mapping vector kernel with this vector length")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_setup(args)
@@ -365,7 +378,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
                      "traffic": traffic, "peak_source": pk["source"],
-                     "kernel": "spmv_tile_kernel<double,int64,int32>",
+                     "kernel": wl.kernel_name(),
                      "algorithmic_bytes_per_launch": local_bytes},
         "e2e": {"value": round(total_bytes / e2e_dt / 1e9, 2), "unit": "GB/s",
                 "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,

@@ -97,6 +97,12 @@ int lapis_b200_csr_plan_destroy(lapis_b200_csr_plan plan);
 int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int rowptr_bytes,
                              const void* colind, int colind_bytes, const void* values,
                              const void* x, void* y, int dtype, void* stream);
+/* What the analysis chose: out[0] = longest row, out[1] = vector length of the
+ * exact vector kernel (0 = row-stream tile kernel), out[2] = number of tiles.
+ * Regular structures (longest row <= max(64, 8 x mean)) run the vector-lane
+ * kernel in exact mode (each step's lane products folded in ascending order,
+ * bit-identical for every row); others run the tile kernel. */
+int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out3);
 
 /* ------------------------------------------------------------- CSR x dense SpMM
  * Y[i, c] = sum_j values[j] * X[colind[j], c],  c in [0, k)

@@ -27,6 +27,7 @@
 //    a shuffle tree, single(PerThread) store by lane 0.
 #include "common.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -297,15 +298,26 @@ spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
 }
 
 // ---------------------------------------------------------- vector kernel
-template <class T, class RP, class CI, int VL>
+// One row per VL lanes (Kokkos thread -> sub-warp, vector -> lane), row groups
+// walked grid-stride with a warp-uniform trip count.
+//   EXACT = false: the emitted TeamPolicy mapping (golden/cpp/spmv.hpp:45-66):
+//     lane-strided partials, ThreadVectorRange reduce as a shuffle tree.
+//   EXACT = true: same load pattern, but each step's VL products (entries
+//     j0 .. j0+VL-1) are folded into the accumulator in ascending j through
+//     in-group shuffles, so the row sum is the reference's sequential sum bit
+//     for bit (out-of-row lanes contribute +0.0, which leaves any accumulator
+//     that can arise unchanged: the running sum starts at +0.0 and can never
+//     become -0.0).  Two steps are unrolled to keep 2*VL loads per row in flight.
+template <class T, class RP, class CI, int VL, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                    const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
   const int lane = threadIdx.x & (VL - 1);
+  const unsigned gmask = (VL == 32) ? 0xffffffffu
+                                    : (((1u << VL) - 1u) << ((threadIdx.x & 31) & ~(VL - 1)));
   const int64_t groups_per_grid = (int64_t)gridDim.x * (blockDim.x / VL);
   const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VL;
   const int64_t my_off = (threadIdx.x & 31) / VL;
-  // warp-uniform trip count so every lane reaches the shuffles
   for (int64_t wrow = warp_first; wrow < nrows; wrow += groups_per_grid) {
     const int64_t row = wrow + my_off;
     T acc = Arith<T>::zero();
@@ -313,13 +325,55 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
       const int64_t b = (int64_t)rowptr[row];
       int64_t e = (int64_t)rowptr[row + 1];
       if (e < b) e = b;  // interp.py:808 range(begin, max(begin, end))
-      for (int64_t j = b + lane; j < e; j += VL)
-        acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
-    }
+      if constexpr (EXACT) {
+        int64_t j0 = b;
+        for (; j0 + VL < e; j0 += 2 * VL) {
+          const int64_t ja = j0 + lane, jb = j0 + VL + lane;
+          const T pa = Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja]));
+          const T pb = jb < e ? Arith<T>::mul(values[jb], __ldg(x + (int64_t)colind[jb])) : T(0);
 #pragma unroll
-    for (int off = VL / 2; off >= 1; off >>= 1) acc = Arith<T>::add(acc, shfl_xor(acc, off, VL));
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
+#pragma unroll
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pb : __shfl_sync(gmask, pb, s2, VL));
+        }
+        if (j0 < e) {
+          const int64_t ja = j0 + lane;
+          const T pa = ja < e ? Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja])) : T(0);
+#pragma unroll
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
+        }
+      } else {
+        for (int64_t j = b + lane; j < e; j += VL)
+          acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
+      }
+    }
+    if constexpr (!EXACT) {
+#pragma unroll
+      for (int off = VL / 2; off >= 1; off >>= 1) acc = Arith<T>::add(acc, shfl_xor(acc, off, VL));
+    }
     if (lane == 0 && row < nrows) y[row] = acc;
   }
+}
+
+// structure analysis for the plan: longest row
+template <class RP>
+__global__ void row_stats_kernel(int64_t nrows, const RP* __restrict__ rowptr,
+                                 unsigned long long* __restrict__ max_len) {
+  int64_t local = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = (int64_t)rowptr[r + 1] - (int64_t)rowptr[r];
+    local = len > local ? len : local;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const int64_t o = __shfl_xor_sync(0xffffffffu, local, off);
+    local = o > local ? o : local;
+  }
+  if ((threadIdx.x & 31) == 0 && local > 0) atomicMax(max_len, (unsigned long long)local);
 }
 
 // ================================================================ host side
@@ -327,6 +381,8 @@ struct CsrPlanImpl {
   int64_t nrows = 0, nnz = 0, ntiles = 0;
   int64_t* tile_row = nullptr;  // device, 2 * (ntiles + 1): tile_row then tile_nnz
   int device = 0;
+  int64_t max_len = 0;          // longest row
+  int exact_vl = 0;             // > 0: regular structure -> exact vector kernel with this VL
 };
 
 static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
@@ -399,7 +455,7 @@ static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
   }
 }
 
-template <class T, class RP, class CI, int VL>
+template <class T, class RP, class CI, int VL, bool EXACT>
 static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind,
                            const void* values, const void* x, void* y, cudaStream_t st) {
   const int threads = 256;
@@ -407,21 +463,21 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
   const int64_t cap = (int64_t)num_sms() * 64;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  spmv_vector_kernel<T, RP, CI, VL><<<(unsigned)blocks, threads, 0, st>>>(
+  spmv_vector_kernel<T, RP, CI, VL, EXACT><<<(unsigned)blocks, threads, 0, st>>>(
       nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y);
   return check_launch("spmv_vector_kernel");
 }
 
-template <class T, class RP, class CI>
+template <class T, class RP, class CI, bool EXACT>
 static int dispatch_vl(int vl, int64_t nrows, const void* rowptr, const void* colind,
                        const void* values, const void* x, void* y, cudaStream_t st) {
   switch (vl) {
-    case 1: return launch_vector_t<T, RP, CI, 1>(nrows, rowptr, colind, values, x, y, st);
-    case 2: return launch_vector_t<T, RP, CI, 2>(nrows, rowptr, colind, values, x, y, st);
-    case 4: return launch_vector_t<T, RP, CI, 4>(nrows, rowptr, colind, values, x, y, st);
-    case 8: return launch_vector_t<T, RP, CI, 8>(nrows, rowptr, colind, values, x, y, st);
-    case 16: return launch_vector_t<T, RP, CI, 16>(nrows, rowptr, colind, values, x, y, st);
-    case 32: return launch_vector_t<T, RP, CI, 32>(nrows, rowptr, colind, values, x, y, st);
+    case 1: return launch_vector_t<T, RP, CI, 1, EXACT>(nrows, rowptr, colind, values, x, y, st);
+    case 2: return launch_vector_t<T, RP, CI, 2, EXACT>(nrows, rowptr, colind, values, x, y, st);
+    case 4: return launch_vector_t<T, RP, CI, 4, EXACT>(nrows, rowptr, colind, values, x, y, st);
+    case 8: return launch_vector_t<T, RP, CI, 8, EXACT>(nrows, rowptr, colind, values, x, y, st);
+    case 16: return launch_vector_t<T, RP, CI, 16, EXACT>(nrows, rowptr, colind, values, x, y, st);
+    case 32: return launch_vector_t<T, RP, CI, 32, EXACT>(nrows, rowptr, colind, values, x, y, st);
   }
   return fail(LAPIS_B200_ERR_ARG, "spmv: vector_length must be 0 or a power of two <= 32");
 }
@@ -456,7 +512,14 @@ template <class T, class RP, class CI>
 struct VecOp {
   static int run(int vl, int64_t nrows, const void* rp, const void* ci, const void* v,
                  const void* x, void* y, cudaStream_t st) {
-    return dispatch_vl<T, RP, CI>(vl, nrows, rp, ci, v, x, y, st);
+    return dispatch_vl<T, RP, CI, false>(vl, nrows, rp, ci, v, x, y, st);
+  }
+};
+template <class T, class RP, class CI>
+struct VecExactOp {
+  static int run(int vl, int64_t nrows, const void* rp, const void* ci, const void* v,
+                 const void* x, void* y, cudaStream_t st) {
+    return dispatch_vl<T, RP, CI, true>(vl, nrows, rp, ci, v, x, y, st);
   }
 };
 
@@ -494,6 +557,38 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
   return rc;
 }
 
+// Regular structures (longest row within 8x the mean, or <= 64) take the exact
+// vector kernel with VL = pow2floor(mean / 6) in [1, 8]; anything else the
+// key-balanced tile kernel.  One device->host read at plan creation.
+static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&d, sizeof(unsigned long long), st), "alloc(stats)"));
+  int rc = check_cuda(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st), "memset(stats)");
+  if (rc == LAPIS_B200_OK) {
+    const int64_t blocks = std::min<int64_t>((p->nrows + 255) / 256, (int64_t)num_sms() * 8);
+    if (rp_bytes == 8)
+      row_stats_kernel<int64_t><<<(unsigned)blocks, 256, 0, st>>>(p->nrows, (const int64_t*)rowptr, d);
+    else
+      row_stats_kernel<int32_t><<<(unsigned)blocks, 256, 0, st>>>(p->nrows, (const int32_t*)rowptr, d);
+    rc = check_launch("row_stats_kernel");
+  }
+  unsigned long long h = 0;
+  if (rc == LAPIS_B200_OK)
+    rc = check_cuda(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "stats D2H");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaStreamSynchronize(st), "stats sync");
+  cudaFreeAsync(d, st);
+  if (rc != LAPIS_B200_OK) return rc;
+  p->max_len = (int64_t)h;
+  const double mean = p->nrows > 0 ? (double)p->nnz / (double)p->nrows : 0.0;
+  int vl = 1;
+  while (vl < 8 && (double)(vl * 2) * 6.0 <= mean) vl *= 2;
+  const char* force = getenv("LAPIS_B200_SPMV_VL");
+  if (force) vl = atoi(force);
+  const bool regular = p->max_len <= 64 || (double)p->max_len <= 8.0 * mean;
+  p->exact_vl = (force && vl > 0) ? vl : (regular ? vl : 0);
+  return LAPIS_B200_OK;
+}
+
 int csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes,
                     cudaStream_t st, void** out) {
   if (!out) return fail(LAPIS_B200_ERR_ARG, "plan: null out pointer");
@@ -509,12 +604,22 @@ int csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes
                       "cudaMalloc(plan)");
   if (rc == LAPIS_B200_OK && nrows > 0)
     rc = launch_partition(nrows, rowptr, rp_bytes, p->ntiles, p->tile_row, st);
+  if (rc == LAPIS_B200_OK && nrows > 0) rc = analyse_rows(p, rowptr, rp_bytes, st);
   if (rc != LAPIS_B200_OK) {
     if (p->tile_row) cudaFree(p->tile_row);
     delete p;
     return rc;
   }
   *out = p;
+  return LAPIS_B200_OK;
+}
+
+int csr_plan_info(void* plan, int64_t* out3) {
+  auto* p = static_cast<CsrPlanImpl*>(plan);
+  if (!p || !out3) return fail(LAPIS_B200_ERR_ARG, "plan_info: null argument");
+  out3[0] = p->max_len;
+  out3[1] = p->exact_vl;
+  out3[2] = p->ntiles;
   return LAPIS_B200_OK;
 }
 
@@ -532,6 +637,9 @@ int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
   if (!p) return fail(LAPIS_B200_ERR_ARG, "spmv: null plan");
   LB_TRY(validate(p->nrows, 0, p->nnz, rowptr, rp_bytes, colind, ci_bytes, values, x, y, dtype));
   if (p->nrows == 0) return LAPIS_B200_OK;
+  if (p->exact_vl > 0)
+    return dispatch_types<VecExactOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,
+                                      colind, values, x, y, st);
   return dispatch_types<TileOp>(dtype, rp_bytes, ci_bytes, p->ntiles, rowptr, colind, values, x,
                                 y, (const int64_t*)p->tile_row, st);
 }

@@ -110,6 +110,14 @@ class CsrPlan:
             C.byref(handle)), "csr_plan_create")
         self._handle = handle
 
+    def info(self) -> dict:
+        """The analysis result: longest row and the kernel the plan dispatches to."""
+        out = (C.c_int64 * 3)()
+        check(_capi.lib().lapis_b200_csr_plan_info(self._handle, out), "csr_plan_info")
+        vl = int(out[1])
+        return {"max_row_len": int(out[0]), "exact_vector_length": vl, "ntiles": int(out[2]),
+                "kernel": f"spmv_vector_kernel<VL={vl}, exact>" if vl else "spmv_tile_kernel"}
+
     def spmv(self, colind, values, x, y=None, *, stream=None) -> torch.Tensor:
         for t, n in ((colind, "colind"), (values, "values"), (x, "x")):
             _dev(t, n)

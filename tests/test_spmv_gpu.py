@@ -173,3 +173,33 @@ def test_config1_laplacian_bitexact_vs_reference_emitted_cpp(cuda_device):
     y = host(lb.spmv_csr(rp, ci, v, cu(x)))
     yref, _ = R.spmv_csr(host(rp), host(ci).astype(np.int64), host(v), x, threads=4)
     assert bits_equal(y, yref)
+
+
+@pytest.mark.parametrize("vl", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int64])
+def test_exact_vector_kernel_bitexact_all_rows(cuda_device, monkeypatch, vl, dtype):
+    # the plan's exact vector mode: every row (long ones included) bit-identical
+    monkeypatch.setenv("LAPIS_B200_SPMV_VL", str(vl))
+    rng = np.random.default_rng(vl)
+    rowptr, colind, values = ragged_csr(rng, 3000, 2500, max_len=70, empty_every=9,
+                                        long_rows={5: 2499, 2999: 1300}, dtype=dtype)
+    x = (rng.integers(-9, 9, 2500) if np.issubdtype(dtype, np.integer)
+         else rng.uniform(-1, 1, 2500)).astype(dtype)
+    plan = lb.CsrPlan(cu(rowptr))
+    assert plan.info()["exact_vector_length"] == vl
+    y = host(plan.spmv(cu(colind), cu(values), cu(x)))
+    assert bits_equal(y, O.spmv_csr(rowptr, colind, values, x))
+
+
+def test_plan_picks_exact_vector_for_stencils(cuda_device):
+    for points, n, vl in ((27, 20, 4), (5, 60, 1)):
+        rp, ci, v = lb.synth_stencil(points, n)
+        plan = lb.CsrPlan(rp)
+        info = plan.info()
+        assert info["exact_vector_length"] == vl, info
+        x = np.random.default_rng(0).uniform(-1, 1, rp.numel() - 1)
+        y = host(plan.spmv(ci, v, cu(x)))
+        assert bits_equal(y, O.spmv_csr(host(rp), host(ci), host(v), x))
+    rng = np.random.default_rng(5)
+    rowptr, colind, values = powerlaw_csr(rng, 20000, mean=12.0)
+    assert lb.CsrPlan(cu(rowptr)).info()["exact_vector_length"] == 0  # irregular -> tile kernel
