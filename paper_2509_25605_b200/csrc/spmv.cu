@@ -303,21 +303,55 @@ spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
 //   EXACT = false: the emitted TeamPolicy mapping (golden/cpp/spmv.hpp:45-66):
 //     lane-strided partials, ThreadVectorRange reduce as a shuffle tree.
 //   EXACT = true: same load pattern, but each step's VL products (entries
-//     j0 .. j0+VL-1) are folded into the accumulator in ascending j through
-//     in-group shuffles, so the row sum is the reference's sequential sum bit
-//     for bit (out-of-row lanes contribute +0.0, which leaves any accumulator
-//     that can arise unchanged: the running sum starts at +0.0 and can never
-//     become -0.0).  Two steps are unrolled to keep 2*VL loads per row in flight.
+//     j0 .. j0+VL-1) go through a warp-private shared-memory slot and every
+//     lane of the group folds them into the accumulator in ascending j, so the
+//     row sum is the reference's sequential sum bit for bit (out-of-row lanes
+//     contribute +0.0, which leaves any accumulator that can arise unchanged:
+//     the running sum starts at +0.0 and can never become -0.0).  Two steps per
+//     trip keep 2*VL loads per row in flight.  (Shuffles would cost two SHFL
+//     per 64-bit product; the slot costs one STS and a broadcast LDS.128.)
+template <class T, int VL>
+__device__ __forceinline__ T fold_slots(T acc, const T* slot) {
+  // ascending fold of VL consecutive shared-memory slots (16-byte reads when aligned)
+  if constexpr (sizeof(T) == 8 && VL >= 2) {
+#pragma unroll
+    for (int q = 0; q < VL; q += 2) {
+      const double2 w = *reinterpret_cast<const double2*>(slot + q);
+      T a, b;
+      memcpy(&a, &w.x, 8);
+      memcpy(&b, &w.y, 8);
+      acc = Arith<T>::add(acc, a);
+      acc = Arith<T>::add(acc, b);
+    }
+  } else if constexpr (sizeof(T) == 4 && VL >= 4) {
+#pragma unroll
+    for (int q = 0; q < VL; q += 4) {
+      const float4 w = *reinterpret_cast<const float4*>(slot + q);
+      T v[4];
+      memcpy(v, &w, 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = Arith<T>::add(acc, v[u]);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < VL; ++q) acc = Arith<T>::add(acc, slot[q]);
+  }
+  return acc;
+}
+
 template <class T, class RP, class CI, int VL, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                    const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
+  // exact mode: per-warp product slots, 2 steps x 32 lanes
+  __shared__ __align__(16) T slots[EXACT ? 8 : 1][EXACT ? 64 : 1];
   const int lane = threadIdx.x & (VL - 1);
-  const unsigned gmask = (VL == 32) ? 0xffffffffu
-                                    : (((1u << VL) - 1u) << ((threadIdx.x & 31) & ~(VL - 1)));
+  const int wl = threadIdx.x & 31;
+  const unsigned gmask = (VL == 32) ? 0xffffffffu : (((1u << VL) - 1u) << (wl & ~(VL - 1)));
   const int64_t groups_per_grid = (int64_t)gridDim.x * (blockDim.x / VL);
   const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VL;
-  const int64_t my_off = (threadIdx.x & 31) / VL;
+  const int64_t my_off = wl / VL;
+  T* ws = EXACT ? slots[(threadIdx.x >> 5) & 7] : nullptr;
   for (int64_t wrow = warp_first; wrow < nrows; wrow += groups_per_grid) {
     const int64_t row = wrow + my_off;
     T acc = Arith<T>::zero();
@@ -326,24 +360,22 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
       int64_t e = (int64_t)rowptr[row + 1];
       if (e < b) e = b;  // interp.py:808 range(begin, max(begin, end))
       if constexpr (EXACT) {
-        int64_t j0 = b;
-        for (; j0 + VL < e; j0 += 2 * VL) {
-          const int64_t ja = j0 + lane, jb = j0 + VL + lane;
-          const T pa = Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja]));
-          const T pb = jb < e ? Arith<T>::mul(values[jb], __ldg(x + (int64_t)colind[jb])) : T(0);
-#pragma unroll
-          for (int s2 = 0; s2 < VL; ++s2)
-            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
-#pragma unroll
-          for (int s2 = 0; s2 < VL; ++s2)
-            acc = Arith<T>::add(acc, VL == 1 ? pb : __shfl_sync(gmask, pb, s2, VL));
-        }
-        if (j0 < e) {
-          const int64_t ja = j0 + lane;
-          const T pa = ja < e ? Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja])) : T(0);
-#pragma unroll
-          for (int s2 = 0; s2 < VL; ++s2)
-            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
+        if constexpr (VL == 1) {
+          for (int64_t j = b; j < e; ++j)
+            acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
+        } else {
+          const T* gslot = ws + (wl & ~(VL - 1));
+          for (int64_t j0 = b; j0 < e; j0 += 2 * VL) {
+            const int64_t ja = j0 + lane, jb = j0 + VL + lane;
+            const T pa = ja < e ? Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja])) : T(0);
+            const T pb = jb < e ? Arith<T>::mul(values[jb], __ldg(x + (int64_t)colind[jb])) : T(0);
+            ws[wl] = pa;
+            ws[32 + wl] = pb;
+            __syncwarp(gmask);
+            acc = fold_slots<T, VL>(acc, gslot);
+            acc = fold_slots<T, VL>(acc, gslot + 32);
+            __syncwarp(gmask);
+          }
         }
       } else {
         for (int64_t j = b + lane; j < e; j += VL)
