@@ -10,14 +10,17 @@ the one the metric's multi-GPU scaling is quoted on): CSR SpMV fp64 on the
 int64 rowptr / int32 colind, row-block sharded over the ranks with the halo
 exchange of x (paper_2509_25605_b200/sharded.py).  A step is one SpMV over the
 whole matrix.  Inputs (69 GB) exceed L2 (126 MB) many times, so no flush is
-needed between steps.
+needed between steps.  Other workloads (--workload) are config 1 (SpMV, 5-point
+Laplacian, L2 flushed between steps), config 3 (SpMM, K = 64, power-law
+matrix) and config 2 (dense matmul 4096^3, f32 or f64).
 
-`value` is device-resident throughput (algorithmic bytes / step time, max over
-ranks); `e2e` repeats the step through the public DualView + C-ABI path with
-the x slice copied host->device and y device->host every step (pinned host
-buffers).  `cpu_baseline` runs the reference's own emitted Kokkos C++ on its
-serial stub (oracle/_ref) on a bounded row block of the same matrix with all
-host threads, and doubles as the parity check of that row block (bit-exact).
+`value` is device-resident throughput (algorithmic bytes or flops / step time,
+max over ranks); `e2e` repeats the step through the public DualView + C-ABI
+path with the step's inputs copied host->device and the result device->host
+every step (pinned host buffers).  `cpu_baseline` runs the reference's own
+emitted Kokkos C++ on its serial stub (oracle/_ref) on a bounded sample of the
+same workload with the host's threads, and doubles as the parity check of that
+sample against the GPU result.
 """
 from __future__ import annotations
 
@@ -131,32 +134,67 @@ def barrier(world):
         dist.barrier()
 
 
+def timed_e2e(one, steps, warmup, world):
+    for _ in range(warmup):
+        one()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / steps
+
+
+def parity_report(got, want, tol):
+    got, want = np.asarray(got), np.asarray(want)
+    if want.dtype.kind == "f":
+        iv = np.uint64 if want.dtype.itemsize == 8 else np.uint32
+        bitexact = bool(np.array_equal(got.view(iv), want.view(iv)))
+        denom = np.maximum(np.maximum(np.abs(got), np.abs(want)), 1.0)
+        maxrel = float(np.max(np.abs(got - want) / denom)) if got.size else 0.0
+    else:
+        bitexact = bool(np.array_equal(got, want))
+        maxrel = 0.0 if bitexact else float("inf")
+    return {"bitexact_vs_reference": bitexact, "max_rel_err": maxrel, "tolerance": tol,
+            "within_tolerance": bool(bitexact or maxrel <= tol)}
+
+
 # ------------------------------------------------------------------- workloads
-class Stencil27Spmv:
+class Workload:
+    unit = "GB/s"
+    bound = "hbm"
+    dtype = "f64"
+    flush = None
+    scaling = "strong"
+
+    def launches_per_step(self) -> int:
+        return 1
+
+
+class StencilSpmv(Workload):
     """Config 5 (default) / config 1: CSR SpMV fp64 on a stencil matrix."""
 
     def __init__(self, args, rank, world, points=27, n=585, x_seed=5):
         import paper_2509_25605_b200 as lb
         from paper_2509_25605_b200 import sharded
         self.lb, self.args, self.rank, self.world = lb, args, rank, world
-        self.points, self.n = points, n
+        self.points, self.n, self.x_seed = points, n, x_seed
         self.N = n ** 3 if points == 27 else n * n
         self.ranges = sharded.balanced_row_ranges(self.N, world)
         self.r0, self.r1 = self.ranges[rank]
         self.stream = torch.cuda.current_stream()
         self.rowptr, self.colind, self.values = lb.synth_stencil(points, n, self.r0, self.r1)
         self.nnz_local = int(self.rowptr[-1].item())
-        rng = np.random.default_rng(x_seed)
-        x_host = rng.uniform(-1.0, 1.0, self.N)
-        self.x_host = x_host
-        self.x = torch.from_numpy(x_host).cuda()          # indexed by global column
+        self.x_host = np.random.default_rng(x_seed).uniform(-1.0, 1.0, self.N)
+        self.x = torch.from_numpy(self.x_host).cuda()          # indexed by global column
         self.y = torch.empty(self.r1 - self.r0, dtype=torch.float64, device="cuda")
         self.op = sharded.RowBlockSpmv(self.rowptr, self.colind, self.values, self.r0, self.r1,
                                        self.N, self.ranges, rank, world)
         self.halo_bytes = 8 * self.op.plan.recv_elems
         # config 1 (80 MB) fits in L2: flush it between timed steps
-        self.flush = (torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-                      if self.bytes_per_step_local() < (512 << 20) else None)
+        if self.work_local() < (512 << 20):
+            self.flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
         torch.cuda.synchronize()
 
     @property
@@ -164,31 +202,28 @@ class Stencil27Spmv:
         return (f"config5: CSR SpMV fp64, 3-D 27-point stencil n={self.n}" if self.points == 27
                 else f"config1: CSR SpMV fp64, 2-D 5-point Laplacian n={self.n}")
 
-    def config(self):
-        return {"workload": self.name, "rows": self.N, "nnz": self.total_nnz(),
-                "index_layout": "rowptr int64, colind int32", "x": f"U(-1,1) seed 5",
-                "sharding": f"row blocks x{self.world}, halo exchange of x (NCCL P2P)",
-                "l2": "inputs >> L2 (126 MB), no flush needed" if self.points == 27 else
-                      "L2 flushed between steps (256 MB write)",
-                "parallelism": f"rowblock{self.world}"}
-
-    def total_nnz(self):
-        return self._global_nnz()
-
-    def _global_nnz(self):
+    def nnz_global(self):
         n = self.n
         return (3 * n - 2) ** 3 if self.points == 27 else 5 * n * n - 4 * n
 
-    def bytes_per_step_global(self) -> int:
-        # SURVEY 8(d): nnz*(s_v+s_i) + (N+1)*s_p + Ncols*s_v + N*s_v, int32 colind layout
-        return self._global_nnz() * 12 + (self.N + 1) * 8 + self.N * 8 + self.N * 8
+    def config(self):
+        return {"workload": self.name, "rows": self.N, "nnz": self.nnz_global(),
+                "index_layout": "rowptr int64, colind int32", "x": f"U(-1,1) seed {self.x_seed}",
+                "sharding": f"row blocks x{self.world}, halo exchange of x (NCCL P2P)",
+                "l2": "inputs >> L2 (126 MB), no flush needed" if self.flush is None else
+                      "L2 flushed between steps (256 MB write, outside the step events)",
+                "parallelism": f"rowblock{self.world}"}
 
-    def bytes_per_step_local(self) -> int:
+    def work_global(self) -> float:
+        # SURVEY 8(d): nnz*(s_v+s_i) + (N+1)*s_p + Ncols*s_v + N*s_v, int32 colind layout
+        return self.nnz_global() * 12 + (self.N + 1) * 8 + self.N * 8 + self.N * 8
+
+    def work_local(self) -> float:
         rows = self.r1 - self.r0
         return self.nnz_local * 12 + (rows + 1) * 8 + rows * 8 * 2 + self.halo_bytes
 
     def launches_per_step(self):
-        return self.op.launches_per_multiply
+        return 1 if self.args.vl else self.op.launches_per_multiply
 
     def kernel_name(self):
         if self.args.vl:
@@ -204,11 +239,10 @@ class Stencil27Spmv:
             return
         self.op.multiply(self.x, self.y, stream=self.stream)
 
-    # e2e through the public API with host buffers: DualView lazy sync of x's
-    # owned slice (host modified every step), kernels, y read back on the host
     def e2e(self, steps, warmup):
+        """DualView lazy sync of this rank's x slice (host-modified every step),
+        the sharded multiply, y read back on the host."""
         from paper_2509_25605_b200.dualview import DualView
-        # the DualView's device side IS the owned slice of the global-indexed x
         xs = DualView.from_host(self.x_host[self.r0:self.r1], "x",
                                 device_buffer=self.x[self.r0:self.r1])
         ys = DualView.allocate((self.r1 - self.r0,), torch.float64, "y")
@@ -220,86 +254,258 @@ class Stencil27Spmv:
             ys.modify_device()
             ys.sync_host(self.stream)
 
-        for _ in range(warmup):
-            one()
-        barrier(self.world)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            one()
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / steps
-        return dt, xs.nbytes, ys.nbytes
+        return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
 
-    # reference's own CPU path on a row block of the same matrix (rank 0, N=1)
-    def cpu_sample(self, rows_sample):
+    def cpu_reference(self, rows_sample, threads, reps):
+        """Reference emitted spmv on rows [a, b) of the same matrix."""
+        from oracle import ref as R
         mid = self.N // 2
         a, b = max(0, mid - rows_sample // 2), min(self.N, mid + rows_sample // 2)
         rp, ci, v = self.lb.synth_stencil(self.points, self.n, a, b)
-        return a, b, rp.cpu().numpy(), ci.cpu().numpy().astype(np.int64), v.cpu().numpy()
+        rp, ci, v = rp.cpu().numpy(), ci.cpu().numpy().astype(np.int64), v.cpu().numpy()
+        nnz = int(rp[-1])
+        yref, times = R.spmv_csr(rp, ci, v, self.x_host, reps=reps, threads=threads)
+        work = nnz * 12 + (b - a + 1) * 8 + (b - a) * 8 * 2
+        desc = (f"rows [{a}, {b}) of the same matrix ({nnz} nnz): reference emitted Kokkos C++ "
+                f"(tests/fixtures/spmv.mlir, index colind) on its serial stub, {threads} row "
+                f"blocks on std::threads")
+        got = self.y[a - self.r0:b - self.r0].cpu().numpy()
+        return yref, got, times, work, desc, 1e-12
 
-    def sample_bytes(self, a, b, nnz):
-        rows = b - a
-        return nnz * 12 + (rows + 1) * 8 + rows * 8 * 2
 
-    def gpu_rows(self, a, b):
-        return self.y[a - self.r0:b - self.r0].cpu().numpy()
+class PowerLawSpmm(Workload):
+    """Config 3: CSR x dense SpMM fp64, K = 64, Chung-Lu power-law matrix."""
+
+    name = "config3: CSR x dense SpMM fp64, K=64, power-law (Chung-Lu, Pareto 2.5) 10M rows"
+    scaling = "weak"
+
+    def __init__(self, args, rank, world, n=10_000_000, k=64, mean=10.0, seed=1):
+        import paper_2509_25605_b200 as lb
+        self.lb, self.args, self.world = lb, args, world
+        self.N, self.k, self.seed = n, k, seed
+        self.stream = torch.cuda.current_stream()
+        self.rowptr, self.colind, self.values = powerlaw_csr_device(n, mean, 2.5, seed)
+        self.nnz = int(self.rowptr[-1].item())
+        g = torch.Generator(device="cuda").manual_seed(seed + 100)
+        self.X = torch.rand((n, k), generator=g, dtype=torch.float64, device="cuda") * 2 - 1
+        self.Y = torch.empty((n, k), dtype=torch.float64, device="cuda")
+        lens = (self.rowptr[1:] - self.rowptr[:-1])
+        self.max_len = int(lens.max().item())
+        self.median_len = float(lens.double().median().item())
+        torch.cuda.synchronize()
+
+    def config(self):
+        return {"workload": self.name, "rows": self.N, "nnz": self.nnz, "k": self.k,
+                "max_row": self.max_len, "median_row": self.median_len,
+                "index_layout": "rowptr int64, colind int32",
+                "generator": f"torch CUDA generator seed {self.seed} (device)",
+                "l2": "inputs >> L2", "parallelism": "replica"}
+
+    def work_global(self):
+        return self.work_local() * self.world
+
+    def work_local(self):
+        return self.nnz * 12 + (self.N + 1) * 8 + self.N * self.k * 8 * 2
+
+    def launches_per_step(self):
+        return 4 if self.max_len > 2048 else 1
+
+    def kernel_name(self):
+        return "spmm_row_kernel<double,int64,int32,2> (+ hub-row chunk/combine)"
+
+    def step(self):
+        self.lb.spmm_csr(self.rowptr, self.colind, self.values, self.X, self.Y, nnz=self.nnz)
+
+    def e2e(self, steps, warmup):
+        """X (the dense operand) host-modified every step, Y read back."""
+        from paper_2509_25605_b200.dualview import DualView
+        xs = DualView.from_host(self.X.cpu(), "X", device_buffer=self.X)
+        ys = DualView.allocate(tuple(self.Y.shape), torch.float64, "Y")
+
+        def one():
+            xs.modify_host()
+            xs.sync_device(self.stream)
+            self.lb.spmm_csr(self.rowptr, self.colind, self.values, xs.device_view(),
+                             ys.device_view(), nnz=self.nnz)
+            ys.modify_device()
+            ys.sync_host(self.stream)
+
+        return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
+
+    def cpu_reference(self, rows_sample, threads, reps):
+        from oracle import ref as R
+        a, b = 0, min(self.N, max(1, rows_sample // 40))
+        rp = self.rowptr[a:b + 1].cpu().numpy()
+        ci = self.colind[rp[0]:rp[-1]].cpu().numpy()
+        v = self.values[rp[0]:rp[-1]].cpu().numpy()
+        rp = rp - rp[0]
+        X = self.X.cpu().numpy()
+        threads = min(threads, 2)   # each thread block replicates X (5 GB) on the stub
+        Yref, times = R.spmm_csr(rp, ci, v, X, reps=reps, threads=threads)
+        nnz = int(rp[-1])
+        work = nnz * 12 + (b - a + 1) * 8 + (b - a) * self.k * 8 * 2
+        desc = (f"rows [{a}, {b}) ({nnz} nnz) of the same matrix: reference emitted Kokkos C++ "
+                f"of oracle/ir/spmm.mlir on its serial stub, {threads} row blocks")
+        got = self.Y[a:b].cpu().numpy()
+        return Yref, got, times, work, desc, 1e-12
+
+
+class DenseMatmul(Workload):
+    """Config 2: dense linalg.matmul 4096^3 (f32: 3xTF32 / exact; f64: DMMA / exact)."""
+
+    unit = "TFLOP/s"
+    bound = "tensor"
+    scaling = "weak"
+
+    def __init__(self, args, rank, world, dt=torch.float32, n=4096):
+        import paper_2509_25605_b200 as lb
+        self.lb, self.args, self.world, self.n, self.dt = lb, args, world, n, dt
+        self.dtype = "f32" if dt == torch.float32 else "f64"
+        self.stream = torch.cuda.current_stream()
+        g = torch.Generator(device="cuda").manual_seed(3 if dt == torch.float32 else 2)
+        lo = 0.0 if dt == torch.float32 else -1.0   # SURVEY 8(d): f32 U(0,1), f64 U(-1,1)
+        self.A = (torch.rand((n, n), generator=g, dtype=dt, device="cuda") * (1 - lo) + lo)
+        self.B = (torch.rand((n, n), generator=g, dtype=dt, device="cuda") * (1 - lo) + lo)
+        self.C = torch.empty((n, n), dtype=dt, device="cuda")
+        self.mode = args.gemm_mode
+        if 3 * n * n * (4 if dt == torch.float32 else 8) < (256 << 20):
+            self.flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+
+    @property
+    def name(self):
+        return f"config2: dense linalg.matmul {self.n}^3 {self.dtype} (mode {self.mode})"
+
+    def config(self):
+        return {"workload": self.name, "m": self.n, "n": self.n, "k": self.n,
+                "inputs": "U(0,1)" if self.dt == torch.float32 else "U(-1,1)",
+                "l2": "L2 flushed between steps" if self.flush is not None else "working set > L2",
+                "parallelism": "replica"}
+
+    def work_global(self):
+        return 2.0 * self.n ** 3 * self.world
+
+    def work_local(self):
+        return 2.0 * self.n ** 3
+
+    def kernel_name(self):
+        return f"gemm<{self.dtype}> mode={self.mode}"
+
+    def step(self):
+        self.lb.gemm(self.A, self.B, self.C, mode=self.mode)
+
+    def e2e(self, steps, warmup):
+        from paper_2509_25605_b200.dualview import DualView
+        a = DualView.from_host(self.A.cpu(), "A", device_buffer=self.A)
+        b = DualView.from_host(self.B.cpu(), "B", device_buffer=self.B)
+        c = DualView.allocate(tuple(self.C.shape), self.dt, "C")
+
+        def one():
+            a.modify_host()
+            b.modify_host()
+            a.sync_device(self.stream)
+            b.sync_device(self.stream)
+            self.lb.gemm(a.device_view(), b.device_view(), c.device_view(), mode=self.mode)
+            c.modify_device()
+            c.sync_host(self.stream)
+
+        return timed_e2e(one, steps, warmup, self.world), a.nbytes + b.nbytes, c.nbytes
+
+    def cpu_reference(self, rows_sample, threads, reps):
+        from oracle import ref as R
+        rows = max(threads, min(self.n, rows_sample // 250_000))
+        A = self.A[:rows].cpu().numpy()
+        B = self.B.cpu().numpy()
+        Cref, times = R.matmul(A, B, reps=reps, threads=threads)
+        desc = (f"rows [0, {rows}) of C: reference emitted Kokkos C++ of oracle/ir/matmul_"
+                f"{self.dtype}.mlir (TeamPolicy nest) on its serial stub, {threads} row blocks")
+        got = self.C[:rows].cpu().numpy()
+        tol = 1e-5 if self.dt == torch.float32 else 1e-12
+        return Cref, got, times, 2.0 * rows * self.n * self.n, desc, tol
+
+
+def powerlaw_csr_device(n, mean, alpha, seed):
+    """Chung-Lu power-law CSR built on the device: Pareto(alpha) row
+    weights, rows and columns drawn in proportion to the weights, hubs scattered
+    by a permutation, sorted and deduplicated; int64 rowptr, int32 colind,
+    values U(-1, 1)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dev = "cuda"
+    w = (1.0 - torch.rand(n, generator=g, dtype=torch.float64, device=dev)) ** (-1.0 / (alpha - 1.0))
+    cdf = torch.cumsum(w, 0)
+    total = int(mean * n)
+    perm = torch.randperm(n, generator=g, device=dev)
+    keys = []
+    chunk = 25_000_000
+    for c0 in range(0, total, chunk):
+        m = min(chunk, total - c0)
+        r = torch.searchsorted(cdf, torch.rand(m, generator=g, dtype=torch.float64, device=dev) * cdf[-1])
+        c = torch.searchsorted(cdf, torch.rand(m, generator=g, dtype=torch.float64, device=dev) * cdf[-1])
+        r = perm[r.clamp_(max=n - 1)]
+        c = perm[c.clamp_(max=n - 1)]
+        keys.append(r.to(torch.int64) * n + c.to(torch.int64))
+        del r, c
+    key = torch.unique(torch.cat(keys))
+    del keys
+    rows = torch.div(key, n, rounding_mode="floor")
+    cols = (key - rows * n).to(torch.int32)
+    counts = torch.bincount(rows, minlength=n)
+    rowptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    rowptr[1:] = torch.cumsum(counts, 0)
+    values = torch.rand(key.numel(), generator=g, dtype=torch.float64, device=dev) * 2 - 1
+    return rowptr, cols.contiguous(), values
 
 
 WORKLOADS = {
-    "c5": lambda args, r, w: Stencil27Spmv(args, r, w, 27, args.n or 585),
-    "c1": lambda args, r, w: Stencil27Spmv(args, r, w, 5, args.n or 1000, x_seed=1),
+    "c5": lambda args, r, w: StencilSpmv(args, r, w, 27, args.n or 585, x_seed=5),
+    "c1": lambda args, r, w: StencilSpmv(args, r, w, 5, args.n or 1000, x_seed=1),
+    "c3": lambda args, r, w: PowerLawSpmm(args, r, w, args.n or 10_000_000),
+    "c2f32": lambda args, r, w: DenseMatmul(args, r, w, torch.float32, args.n or 4096),
+    "c2f64": lambda args, r, w: DenseMatmul(args, r, w, torch.float64, args.n or 4096),
 }
 
 
 def cpu_baseline(wl, args, threads):
-    """The reference's emitted C++ on its serial stub (oracle/_ref), all host
-    threads, on a bounded row block; also the bit-exact parity check of it."""
+    """The reference's emitted C++ on its serial stub (oracle/_ref) on a bounded
+    sample of the workload; also the parity check of that sample."""
     from oracle import ref as R
     if not R.available():
         return {"unavailable": "oracle/_ref not built"}, None
-    a, b, rp, ci, v = wl.cpu_sample(args.cpu_rows)
-    nnz = int(rp[-1])
-    yref, times = R.spmv_csr(rp, ci, v, wl.x_host, reps=args.cpu_reps, threads=threads)
+    want, got, times, work, desc, tol = wl.cpu_reference(args.cpu_rows, threads, args.cpu_reps)
     t = float(np.median(times))
-    value = wl.sample_bytes(a, b, nnz) / t / 1e9
-    got = wl.gpu_rows(a, b)
-    bitexact = bool(np.array_equal(got.view(np.uint64), yref.view(np.uint64)))
-    maxrel = float(np.max(np.abs(got - yref) / np.maximum(np.abs(yref), 1.0))) if got.size else 0.0
-    base = {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-            "sample": (f"rows [{a}, {b}) of the same matrix ({nnz} nnz), reference emitted "
-                       f"Kokkos C++ (tests/fixtures/spmv.mlir, index colind) on its serial stub, "
-                       f"{threads} row blocks on std::threads, median of {args.cpu_reps} reps"),
+    scale = 1e9 if wl.unit == "GB/s" else 1e12
+    base = {"value": round(work / t / scale, 4), "unit": wl.unit, "cores": threads,
+            "kind": "reference", "sample": desc + f", median of {len(times)} reps",
             "seconds_per_rep": t}
-    parity = {"rows_checked": b - a, "bitexact_vs_reference": bitexact, "max_rel_err": maxrel}
+    parity = {"sample_elements": int(np.asarray(want).size), **parity_report(got, want, tol)}
     return base, parity
 
 
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
     from oracle import ref as R
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
+    threads = os.cpu_count() or 1
     torch.cuda.set_device(0)
-    wl = WORKLOADS[args.workload](args, 0, 1) if torch.cuda.is_available() else None
-    a, b, rp, ci, v = wl.cpu_sample(args.cpu_rows)
-    nnz = int(rp[-1])
-    _, times = R.spmv_csr(rp, ci, v, wl.x_host, reps=args.warmup + args.steps, threads=threads)
+    wl = WORKLOADS[args.workload](args, 0, 1)
+    wl.step()
+    torch.cuda.synchronize()
+    _, _, times, work, desc, _ = wl.cpu_reference(args.cpu_rows, threads,
+                                                  args.warmup + args.steps)
     times = times[args.warmup:]
     t = float(np.mean(times))
-    value = wl.sample_bytes(a, b, nnz) / t / 1e9
-    out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+    scale = 1e9 if wl.unit == "GB/s" else 1e12
+    value = work / t / scale
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": wl.unit,
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": wl.config(),
-           "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
-                            "kind": "reference",
-                            "sample": f"rows [{a}, {b}) ({nnz} nnz) of the workload matrix"},
-           "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+           "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": wl.scaling,
+           "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic", "config": wl.config(),
+           "cpu_baseline": {"value": round(value, 4), "unit": wl.unit, "cores": threads,
+                            "kind": "reference", "sample": desc},
+           "e2e": {"value": round(value, 4), "unit": wl.unit, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -311,13 +517,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="grid size override")
+    ap.add_argument("--n", type=int, default=0, help="problem size override")
     ap.add_argument("--cpu-rows", type=int, default=4_000_000)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--vl", type=int, default=0,
-                    help="time the emitted-mapping vector kernel with this vector length")
+                    help="SpMV: time the emitted-mapping vector kernel with this vector length")
+    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "tf32x3", "dmma", "exact"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_setup(args)
@@ -357,12 +564,19 @@ def main():
                else float(np.mean(kern)))
     t = max_over_ranks(t_local, world)
     kern_avg = max_over_ranks(float(np.mean(kern)), world)
-    total_bytes = wl.bytes_per_step_global()
-    value = total_bytes / t / 1e9
+    scale = 1e9 if wl.unit == "GB/s" else 1e12
+    value = wl.work_global() / t / scale
     pk = peaks()
-    # roofline of the dominant kernel (the tile SpMV): this rank's algorithmic bytes
-    local_bytes = wl.bytes_per_step_local()
-    achieved = local_bytes / kern_avg / 1e9
+    if wl.bound == "hbm":
+        peak, punit, psrc = pk["hbm_gbs"], "GB/s", pk["source"] + " hbm_gbs (copy)"
+    else:
+        # tensor-bound: nominal B200 dense peaks (MEASURED_PEAKS has bf16 only)
+        if wl.dtype == "f32":
+            peak, psrc = 1100.0 / 3.0, "nominal TF32 dense 1.1 PF / 3 (3xTF32)"
+        else:
+            peak, psrc = 40.0, "nominal FP64 tensor 40 TF"
+        punit = "TFLOP/s"
+    achieved = wl.work_local() / kern_avg / scale
     traffic = None
     tfile = ROOT / "profiles" / f"traffic_{args.workload}.json"
     if tfile.exists():
@@ -370,20 +584,20 @@ def main():
     e2e_dt, hb, db = wl.e2e(args.e2e_steps, 2)
     e2e_dt = max_over_ranks(e2e_dt, world)
     out = {
-        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "metric": METRIC, "value": round(value, 3), "unit": wl.unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (device-generated stencil, numpy-seeded x)",
+        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype,
+        "data": "synthetic (device-generated inputs, seeded)",
         "config": wl.config(),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-                     "traffic": traffic, "peak_source": pk["source"],
-                     "kernel": wl.kernel_name(),
-                     "algorithmic_bytes_per_launch": local_bytes},
-        "e2e": {"value": round(total_bytes / e2e_dt / 1e9, 2), "unit": "GB/s",
+        "roofline": {"bound": wl.bound, "achieved": round(achieved, 2), "peak": peak,
+                     "unit": punit, "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": psrc, "kernel": wl.kernel_name(),
+                     "algorithmic_work_per_launch": wl.work_local()},
+        "e2e": {"value": round(wl.work_global() / e2e_dt / scale, 3), "unit": wl.unit,
                 "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
                 "ms_per_step": round(e2e_dt * 1e3, 3),
-                "path": "DualView lazy sync (x host-modified each step) + C-ABI plan SpMV + y read"},
+                "path": "DualView lazy sync (inputs host-modified each step) + C-ABI kernels + "
+                        "result read on the host"},
         "gpu_launches": args.steps * wl.launches_per_step(),
         "clocks": clk.summary(),
     }
