@@ -141,3 +141,48 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 }  // namespace lapis_b200
+
+// ------------------------------------------------------ L2 cache-policy loads
+// Streams read once (colind, values) are loaded with an L2 evict_first policy so
+// they do not push out data with reuse (the gathered x); gathers use evict_last.
+namespace lapis_b200 {
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <class T> __device__ __forceinline__ T ld_hint(const T* p, uint64_t pol);
+template <> __device__ __forceinline__ double ld_hint<double>(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <> __device__ __forceinline__ float ld_hint<float>(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <> __device__ __forceinline__ long long ld_hint<long long>(const long long* p, uint64_t pol) {
+  long long v;
+  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <> __device__ __forceinline__ int ld_hint<int>(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <> __device__ __forceinline__ long ld_hint<long>(const long* p, uint64_t pol) {
+  long v;
+  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+}  // namespace lapis_b200

@@ -343,15 +343,18 @@ template <class T, class RP, class CI, int VL, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                    const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
-  // exact mode: per-warp product slots, 2 steps x 32 lanes
-  __shared__ __align__(16) T slots[EXACT ? 8 : 1][EXACT ? 64 : 1];
+  constexpr int U = 4;                       // exact mode: steps per trip
+  constexpr bool SLOTS = EXACT && VL > 1;
+  // exact mode: per-warp double-buffered product slots [2][U][32]
+  __shared__ __align__(16) T slots[SLOTS ? 8 : 1][SLOTS ? 2 * U * 32 : 1];
   const int lane = threadIdx.x & (VL - 1);
   const int wl = threadIdx.x & 31;
   const unsigned gmask = (VL == 32) ? 0xffffffffu : (((1u << VL) - 1u) << (wl & ~(VL - 1)));
   const int64_t groups_per_grid = (int64_t)gridDim.x * (blockDim.x / VL);
   const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VL;
   const int64_t my_off = wl / VL;
-  T* ws = EXACT ? slots[(threadIdx.x >> 5) & 7] : nullptr;
+  const uint64_t pol_stream = policy_evict_first(), pol_x = policy_evict_last();
+  T* ws = SLOTS ? slots[(threadIdx.x >> 5) & 7] : nullptr;
   for (int64_t wrow = warp_first; wrow < nrows; wrow += groups_per_grid) {
     const int64_t row = wrow + my_off;
     T acc = Arith<T>::zero();
@@ -360,26 +363,51 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
       int64_t e = (int64_t)rowptr[row + 1];
       if (e < b) e = b;  // interp.py:808 range(begin, max(begin, end))
       if constexpr (EXACT) {
-        if constexpr (VL == 1) {
-          for (int64_t j = b; j < e; ++j)
-            acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
-        } else {
-          const T* gslot = ws + (wl & ~(VL - 1));
-          for (int64_t j0 = b; j0 < e; j0 += 2 * VL) {
-            const int64_t ja = j0 + lane, jb = j0 + VL + lane;
-            const T pa = ja < e ? Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja])) : T(0);
-            const T pb = jb < e ? Arith<T>::mul(values[jb], __ldg(x + (int64_t)colind[jb])) : T(0);
-            ws[wl] = pa;
-            ws[32 + wl] = pb;
-            __syncwarp(gmask);
-            acc = fold_slots<T, VL>(acc, gslot);
-            acc = fold_slots<T, VL>(acc, gslot + 32);
-            __syncwarp(gmask);
+        // raw operands of one trip (U steps of VL entries), prefetched one trip ahead
+        T va[U], xa[U];
+        auto issue = [&](int64_t jb) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t j = jb + u * VL + lane;
+            if (j < e) {
+              const int64_t c = (int64_t)ld_hint<CI>(colind + j, pol_stream);
+              va[u] = ld_hint<T>(values + j, pol_stream);
+              xa[u] = ld_hint<T>(x + c, pol_x);
+            } else {
+              va[u] = T(0);   // +0.0 product: leaves the running sum unchanged
+              xa[u] = T(0);
+            }
           }
+        };
+        int buf = 0;
+        int64_t j0 = b;
+        if (j0 < e) issue(j0);
+        while (j0 < e) {
+          T p[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) p[u] = Arith<T>::mul(va[u], xa[u]);
+          const int64_t j1 = j0 + U * VL;
+          if constexpr (SLOTS) {
+            T* sb = ws + buf * (U * 32);
+#pragma unroll
+            for (int u = 0; u < U; ++u) sb[u * 32 + wl] = p[u];
+            __syncwarp(gmask);
+            if (j1 < e) issue(j1);         // next trip's loads in flight during the fold
+            const T* gs = sb + (wl & ~(VL - 1));
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = fold_slots<T, VL>(acc, gs + u * 32);
+            buf ^= 1;
+          } else {
+            if (j1 < e) issue(j1);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = Arith<T>::add(acc, p[u]);
+          }
+          j0 = j1;
         }
       } else {
         for (int64_t j = b + lane; j < e; j += VL)
-          acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
+          acc = Arith<T>::add(acc, Arith<T>::mul(ld_hint<T>(values + j, pol_stream),
+                                                 ld_hint<T>(x + (int64_t)ld_hint<CI>(colind + j, pol_stream), pol_x)));
       }
     }
     if constexpr (!EXACT) {
