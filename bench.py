@@ -239,6 +239,30 @@ class StencilSpmv(Workload):
             return
         self.op.multiply(self.x, self.y, stream=self.stream)
 
+    def exact_variant(self, steps):
+        """The same multiply with every row folded in the reference order (plan
+        exact mode, bit-identical); device-resident throughput."""
+        from paper_2509_25605_b200 import sharded
+        op = sharded.RowBlockSpmv(self.rowptr, self.colind, self.values, self.r0, self.r1,
+                                  self.N, self.ranges, self.rank, self.world, exact=True)
+        for _ in range(3):
+            op.multiply(self.x, self.y, stream=self.stream)
+        evs = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if self.flush is not None:
+                self.flush.fill_(1)
+            a.record(self.stream)
+            op.multiply(self.x, self.y, stream=self.stream)
+            b.record(self.stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        t = max_over_ranks(float(np.mean([a.elapsed_time(b) / 1e3 for a, b in evs])), self.world)
+        names = sorted({p.info()["kernel"] for p in op.plans.values()})
+        return {"value": round(self.work_global() / t / 1e9, 3), "unit": "GB/s",
+                "frac": round(self.work_local() / t / 1e9 / peaks()["hbm_gbs"], 4),
+                "kernel": "; ".join(names), "note": "bit-identical to the reference"}
+
     def e2e(self, steps, warmup):
         """DualView lazy sync of this rank's x slice (host-modified every step),
         the sharded multiply, y read back on the host."""
@@ -581,6 +605,8 @@ def main():
     tfile = ROOT / "profiles" / f"traffic_{args.workload}.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    exact_variant = (wl.exact_variant(max(3, args.steps // 2))
+                     if hasattr(wl, "exact_variant") and not args.vl else None)
     e2e_dt, hb, db = wl.e2e(args.e2e_steps, 2)
     e2e_dt = max_over_ranks(e2e_dt, world)
     out = {
@@ -599,6 +625,7 @@ def main():
                 "path": "DualView lazy sync (inputs host-modified each step) + C-ABI kernels + "
                         "result read on the host"},
         "gpu_launches": args.steps * wl.launches_per_step(),
+        **({"exact_mode": exact_variant} if exact_variant else {}),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:

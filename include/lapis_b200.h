@@ -98,11 +98,15 @@ int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int r
                              const void* colind, int colind_bytes, const void* values,
                              const void* x, void* y, int dtype, void* stream);
 /* What the analysis chose: out[0] = longest row, out[1] = vector length of the
- * exact vector kernel (0 = row-stream tile kernel), out[2] = number of tiles.
- * Regular structures (longest row <= max(64, 8 x mean)) run the vector-lane
- * kernel in exact mode (each step's lane products folded in ascending order,
- * bit-identical for every row); others run the tile kernel. */
-int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out3);
+ * vector-lane kernel (0 = row-stream tile kernel), out[2] = number of tiles,
+ * out[3] = exact flag.  Regular structures (longest row <= max(64, 8 x mean))
+ * run the vector-lane kernel with VL = pow2floor(mean / 6) in [1, 8]: fp64 and
+ * integer rows as the emitted TeamPolicy mapping (shuffle-tree reduce, the
+ * Kokkos ThreadVectorRange semantics), fp32 rows — and every dtype once
+ * lapis_b200_csr_plan_set_exact(plan, 1) — folded in the reference's
+ * sequential order (bit-identical).  Irregular structures run the tile kernel. */
+int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out4);
+int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact);
 
 /* ------------------------------------------------------------- CSR x dense SpMM
  * Y[i, c] = sum_j values[j] * X[colind[j], c],  c in [0, k)

@@ -45,6 +45,7 @@ _SIGNATURES = {
     "lapis_b200_csr_plan_destroy": ([_VP], _INT),
     "lapis_b200_spmv_csr_plan": ([_VP, _VP, _INT, _VP, _INT, _VP, _VP, _VP, _INT, _VP], _INT),
     "lapis_b200_csr_plan_info": ([_VP, _VP], _INT),
+    "lapis_b200_csr_plan_set_exact": ([_VP, _INT], _INT),
     "lapis_b200_spmm_csr": ([_I64, _I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP,
                              _I64, _INT, _VP], _INT),
     "lapis_b200_gemm": ([_I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _INT, _INT, _VP], _INT),

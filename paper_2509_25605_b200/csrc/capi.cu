@@ -31,6 +31,7 @@ int spmv_csr(int64_t, int64_t, int64_t, const void*, int, const void*, int, cons
 int csr_plan_create(int64_t, int64_t, const void*, int, cudaStream_t, void**);
 int csr_plan_destroy(void*);
 int csr_plan_info(void*, int64_t*);
+int csr_plan_set_exact(void*, int);
 int spmv_csr_plan(void*, const void*, int, const void*, int, const void*, const void*, void*, int,
                   cudaStream_t);
 int spmm_csr(int64_t, int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
@@ -101,8 +102,12 @@ int lapis_b200_csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, i
 
 int lapis_b200_csr_plan_destroy(lapis_b200_csr_plan plan) { return csr_plan_destroy(plan); }
 
-int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out3) {
-  return csr_plan_info(plan, out3);
+int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out4) {
+  return csr_plan_info(plan, out4);
+}
+
+int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact) {
+  return csr_plan_set_exact(plan, exact);
 }
 
 int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int rowptr_bytes,

@@ -303,58 +303,21 @@ spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
 //   EXACT = false: the emitted TeamPolicy mapping (golden/cpp/spmv.hpp:45-66):
 //     lane-strided partials, ThreadVectorRange reduce as a shuffle tree.
 //   EXACT = true: same load pattern, but each step's VL products (entries
-//     j0 .. j0+VL-1) go through a warp-private shared-memory slot and every
-//     lane of the group folds them into the accumulator in ascending j, so the
-//     row sum is the reference's sequential sum bit for bit (out-of-row lanes
-//     contribute +0.0, which leaves any accumulator that can arise unchanged:
-//     the running sum starts at +0.0 and can never become -0.0).  Two steps per
-//     trip keep 2*VL loads per row in flight.  (Shuffles would cost two SHFL
-//     per 64-bit product; the slot costs one STS and a broadcast LDS.128.)
-template <class T, int VL>
-__device__ __forceinline__ T fold_slots(T acc, const T* slot) {
-  // ascending fold of VL consecutive shared-memory slots (16-byte reads when aligned)
-  if constexpr (sizeof(T) == 8 && VL >= 2) {
-#pragma unroll
-    for (int q = 0; q < VL; q += 2) {
-      const double2 w = *reinterpret_cast<const double2*>(slot + q);
-      T a, b;
-      memcpy(&a, &w.x, 8);
-      memcpy(&b, &w.y, 8);
-      acc = Arith<T>::add(acc, a);
-      acc = Arith<T>::add(acc, b);
-    }
-  } else if constexpr (sizeof(T) == 4 && VL >= 4) {
-#pragma unroll
-    for (int q = 0; q < VL; q += 4) {
-      const float4 w = *reinterpret_cast<const float4*>(slot + q);
-      T v[4];
-      memcpy(v, &w, 16);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc = Arith<T>::add(acc, v[u]);
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < VL; ++q) acc = Arith<T>::add(acc, slot[q]);
-  }
-  return acc;
-}
-
+//     j0 .. j0+VL-1) are folded into the accumulator in ascending j through
+//     in-group shuffles, so the row sum is the reference's sequential sum bit
+//     for bit (out-of-row lanes contribute +0.0, which leaves any accumulator
+//     that can arise unchanged: the running sum starts at +0.0 and can never
+//     become -0.0).  Two steps are unrolled to keep 2*VL loads per row in flight.
 template <class T, class RP, class CI, int VL, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                    const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
-  constexpr int U = 4;                       // exact mode: steps per trip
-  constexpr bool SLOTS = EXACT && VL > 1;
-  // exact mode: per-warp double-buffered product slots [2][U][32]
-  __shared__ __align__(16) T slots[SLOTS ? 8 : 1][SLOTS ? 2 * U * 32 : 1];
   const int lane = threadIdx.x & (VL - 1);
-  const int wl = threadIdx.x & 31;
-  const unsigned gmask = (VL == 32) ? 0xffffffffu : (((1u << VL) - 1u) << (wl & ~(VL - 1)));
+  const unsigned gmask = (VL == 32) ? 0xffffffffu
+                                    : (((1u << VL) - 1u) << ((threadIdx.x & 31) & ~(VL - 1)));
   const int64_t groups_per_grid = (int64_t)gridDim.x * (blockDim.x / VL);
   const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VL;
-  const int64_t my_off = wl / VL;
-  const uint64_t pol_stream = policy_evict_first(), pol_x = policy_evict_last();
-  T* ws = SLOTS ? slots[(threadIdx.x >> 5) & 7] : nullptr;
+  const int64_t my_off = (threadIdx.x & 31) / VL;
   for (int64_t wrow = warp_first; wrow < nrows; wrow += groups_per_grid) {
     const int64_t row = wrow + my_off;
     T acc = Arith<T>::zero();
@@ -363,51 +326,28 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
       int64_t e = (int64_t)rowptr[row + 1];
       if (e < b) e = b;  // interp.py:808 range(begin, max(begin, end))
       if constexpr (EXACT) {
-        // raw operands of one trip (U steps of VL entries), prefetched one trip ahead
-        T va[U], xa[U];
-        auto issue = [&](int64_t jb) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int64_t j = jb + u * VL + lane;
-            if (j < e) {
-              const int64_t c = (int64_t)ld_hint<CI>(colind + j, pol_stream);
-              va[u] = ld_hint<T>(values + j, pol_stream);
-              xa[u] = ld_hint<T>(x + c, pol_x);
-            } else {
-              va[u] = T(0);   // +0.0 product: leaves the running sum unchanged
-              xa[u] = T(0);
-            }
-          }
-        };
-        int buf = 0;
         int64_t j0 = b;
-        if (j0 < e) issue(j0);
-        while (j0 < e) {
-          T p[U];
+        for (; j0 + VL < e; j0 += 2 * VL) {
+          const int64_t ja = j0 + lane, jb = j0 + VL + lane;
+          const T pa = Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja]));
+          const T pb = jb < e ? Arith<T>::mul(values[jb], __ldg(x + (int64_t)colind[jb])) : T(0);
 #pragma unroll
-          for (int u = 0; u < U; ++u) p[u] = Arith<T>::mul(va[u], xa[u]);
-          const int64_t j1 = j0 + U * VL;
-          if constexpr (SLOTS) {
-            T* sb = ws + buf * (U * 32);
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
 #pragma unroll
-            for (int u = 0; u < U; ++u) sb[u * 32 + wl] = p[u];
-            __syncwarp(gmask);
-            if (j1 < e) issue(j1);         // next trip's loads in flight during the fold
-            const T* gs = sb + (wl & ~(VL - 1));
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pb : __shfl_sync(gmask, pb, s2, VL));
+        }
+        if (j0 < e) {
+          const int64_t ja = j0 + lane;
+          const T pa = ja < e ? Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja])) : T(0);
 #pragma unroll
-            for (int u = 0; u < U; ++u) acc = fold_slots<T, VL>(acc, gs + u * 32);
-            buf ^= 1;
-          } else {
-            if (j1 < e) issue(j1);
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc = Arith<T>::add(acc, p[u]);
-          }
-          j0 = j1;
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
         }
       } else {
         for (int64_t j = b + lane; j < e; j += VL)
-          acc = Arith<T>::add(acc, Arith<T>::mul(ld_hint<T>(values + j, pol_stream),
-                                                 ld_hint<T>(x + (int64_t)ld_hint<CI>(colind + j, pol_stream), pol_x)));
+          acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(x + (int64_t)colind[j])));
       }
     }
     if constexpr (!EXACT) {
@@ -442,7 +382,8 @@ struct CsrPlanImpl {
   int64_t* tile_row = nullptr;  // device, 2 * (ntiles + 1): tile_row then tile_nnz
   int device = 0;
   int64_t max_len = 0;          // longest row
-  int exact_vl = 0;             // > 0: regular structure -> exact vector kernel with this VL
+  int exact_vl = 0;             // > 0: regular structure -> vector kernel with this VL
+  int exact = 0;                // 1: fp64 / int rows folded in the reference order too
 };
 
 static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
@@ -646,6 +587,8 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
   if (force) vl = atoi(force);
   const bool regular = p->max_len <= 64 || (double)p->max_len <= 8.0 * mean;
   p->exact_vl = (force && vl > 0) ? vl : (regular ? vl : 0);
+  const char* ex = getenv("LAPIS_B200_SPMV_EXACT");
+  p->exact = (ex && atoi(ex) != 0) ? 1 : 0;
   return LAPIS_B200_OK;
 }
 
@@ -674,12 +617,20 @@ int csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes
   return LAPIS_B200_OK;
 }
 
-int csr_plan_info(void* plan, int64_t* out3) {
+int csr_plan_info(void* plan, int64_t* out4) {
   auto* p = static_cast<CsrPlanImpl*>(plan);
-  if (!p || !out3) return fail(LAPIS_B200_ERR_ARG, "plan_info: null argument");
-  out3[0] = p->max_len;
-  out3[1] = p->exact_vl;
-  out3[2] = p->ntiles;
+  if (!p || !out4) return fail(LAPIS_B200_ERR_ARG, "plan_info: null argument");
+  out4[0] = p->max_len;
+  out4[1] = p->exact_vl;
+  out4[2] = p->ntiles;
+  out4[3] = p->exact;
+  return LAPIS_B200_OK;
+}
+
+int csr_plan_set_exact(void* plan, int exact) {
+  auto* p = static_cast<CsrPlanImpl*>(plan);
+  if (!p) return fail(LAPIS_B200_ERR_ARG, "plan_set_exact: null plan");
+  p->exact = exact ? 1 : 0;
   return LAPIS_B200_OK;
 }
 
@@ -697,9 +648,16 @@ int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
   if (!p) return fail(LAPIS_B200_ERR_ARG, "spmv: null plan");
   LB_TRY(validate(p->nrows, 0, p->nnz, rowptr, rp_bytes, colind, ci_bytes, values, x, y, dtype));
   if (p->nrows == 0) return LAPIS_B200_OK;
-  if (p->exact_vl > 0)
-    return dispatch_types<VecExactOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,
-                                      colind, values, x, y, st);
+  if (p->exact_vl > 0) {
+    // fp32 always folds in the reference order (its 1e-5 contract cannot absorb
+    // reassociation on long rows); fp64 / ints take the emitted-mapping tree
+    // (ThreadVectorRange reduce) unless exact mode was requested
+    if (p->exact || dtype == LAPIS_B200_F32)
+      return dispatch_types<VecExactOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,
+                                        colind, values, x, y, st);
+    return dispatch_types<VecOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,
+                                 colind, values, x, y, st);
+  }
   return dispatch_types<TileOp>(dtype, rp_bytes, ci_bytes, p->ntiles, rowptr, colind, values, x,
                                 y, (const int64_t*)p->tile_row, st);
 }

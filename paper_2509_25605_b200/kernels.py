@@ -99,7 +99,8 @@ class CsrPlan:
     """Structure-only analysis of one rowptr (tile -> first-row table), reused
     by every SpMV on that structure.  Holds a device allocation."""
 
-    def __init__(self, rowptr: torch.Tensor, nnz: int | None = None, stream=None):
+    def __init__(self, rowptr: torch.Tensor, nnz: int | None = None, stream=None,
+                 exact: bool | None = None):
         _dev(rowptr, "rowptr")
         self.nrows = rowptr.numel() - 1
         self.nnz = int(rowptr[-1].item() - rowptr[0].item()) if nnz is None else int(nnz)
@@ -109,14 +110,19 @@ class CsrPlan:
             self.nrows, self.nnz, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"), _stream(stream),
             C.byref(handle)), "csr_plan_create")
         self._handle = handle
+        if exact is not None:
+            check(_capi.lib().lapis_b200_csr_plan_set_exact(handle, int(bool(exact))),
+                  "csr_plan_set_exact")
 
     def info(self) -> dict:
         """The analysis result: longest row and the kernel the plan dispatches to."""
-        out = (C.c_int64 * 3)()
+        out = (C.c_int64 * 4)()
         check(_capi.lib().lapis_b200_csr_plan_info(self._handle, out), "csr_plan_info")
-        vl = int(out[1])
-        return {"max_row_len": int(out[0]), "exact_vector_length": vl, "ntiles": int(out[2]),
-                "kernel": f"spmv_vector_kernel<VL={vl}, exact>" if vl else "spmv_tile_kernel"}
+        vl, exact = int(out[1]), bool(out[3])
+        kind = "exact" if exact else "tree (exact for f32)"
+        return {"max_row_len": int(out[0]), "vector_length": vl, "exact": exact,
+                "ntiles": int(out[2]),
+                "kernel": f"spmv_vector_kernel<VL={vl}, {kind}>" if vl else "spmv_tile_kernel"}
 
     def spmv(self, colind, values, x, y=None, *, stream=None) -> torch.Tensor:
         for t, n in ((colind, "colind"), (values, "values"), (x, "x")):

@@ -130,7 +130,7 @@ class RowBlockSpmv:
 
     def __init__(self, rowptr: torch.Tensor, colind: torch.Tensor, values: torch.Tensor,
                  row_begin: int, row_end: int, nrows_global: int, ranges, rank: int, world: int,
-                 group=None):
+                 group=None, exact: bool | None = None):
         from .kernels import CsrPlan
         self.rowptr, self.colind, self.values = rowptr, colind, values
         self.row_begin, self.row_end = row_begin, row_end
@@ -144,7 +144,7 @@ class RowBlockSpmv:
         for lo, hi in self.pieces:
             if hi > lo:
                 rp = rowptr[lo:hi + 1]
-                self.plans[(lo, hi)] = CsrPlan(rp)
+                self.plans[(lo, hi)] = CsrPlan(rp, exact=exact)
         self.comm_stream = torch.cuda.Stream(device=values.device) if world > 1 else None
 
     @property

@@ -185,21 +185,30 @@ def test_exact_vector_kernel_bitexact_all_rows(cuda_device, monkeypatch, vl, dty
                                         long_rows={5: 2499, 2999: 1300}, dtype=dtype)
     x = (rng.integers(-9, 9, 2500) if np.issubdtype(dtype, np.integer)
          else rng.uniform(-1, 1, 2500)).astype(dtype)
-    plan = lb.CsrPlan(cu(rowptr))
-    assert plan.info()["exact_vector_length"] == vl
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
+    assert plan.info()["vector_length"] == vl and plan.info()["exact"]
     y = host(plan.spmv(cu(colind), cu(values), cu(x)))
     assert bits_equal(y, O.spmv_csr(rowptr, colind, values, x))
+    # default (tree) mode: within the diff_outputs contract; fp32 stays exact
+    tree = lb.CsrPlan(cu(rowptr))
+    yt = host(tree.spmv(cu(colind), cu(values), cu(x)))
+    if dtype == np.float32:
+        assert bits_equal(yt, O.spmv_csr(rowptr, colind, values, x))
+    else:
+        assert_close(yt, O.spmv_csr(rowptr, colind, values, x))
 
 
 def test_plan_picks_exact_vector_for_stencils(cuda_device):
     for points, n, vl in ((27, 20, 4), (5, 60, 1)):
         rp, ci, v = lb.synth_stencil(points, n)
-        plan = lb.CsrPlan(rp)
+        plan = lb.CsrPlan(rp, exact=True)
         info = plan.info()
-        assert info["exact_vector_length"] == vl, info
+        assert info["vector_length"] == vl, info
         x = np.random.default_rng(0).uniform(-1, 1, rp.numel() - 1)
         y = host(plan.spmv(ci, v, cu(x)))
-        assert bits_equal(y, O.spmv_csr(host(rp), host(ci), host(v), x))
+        want = O.spmv_csr(host(rp), host(ci), host(v), x)
+        assert bits_equal(y, want)
+        assert_close(host(lb.CsrPlan(rp).spmv(ci, v, cu(x))), want)
     rng = np.random.default_rng(5)
     rowptr, colind, values = powerlaw_csr(rng, 20000, mean=12.0)
-    assert lb.CsrPlan(cu(rowptr)).info()["exact_vector_length"] == 0  # irregular -> tile kernel
+    assert lb.CsrPlan(cu(rowptr)).info()["vector_length"] == 0  # irregular -> tile kernel
