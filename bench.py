@@ -607,6 +607,8 @@ def main():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
     exact_variant = (wl.exact_variant(max(3, args.steps // 2))
                      if hasattr(wl, "exact_variant") and not args.vl else None)
+    wl.step()   # the parity sample below checks the headline kernel's output
+    torch.cuda.synchronize()
     e2e_dt, hb, db = wl.e2e(args.e2e_steps, 2)
     e2e_dt = max_over_ranks(e2e_dt, world)
     out = {
