@@ -1,0 +1,373 @@
+// gemm_tf32x3.cu — fp32 dense matmul on the 5th-generation tensor cores.
+//
+// C = A * B (row-major, LayoutRight) for linalg.matmul / kokkos.gemm
+// (interp.py:711-722, runtime_header.py:249-266) at fp32 accuracy with TF32
+// tensor-core math ("3xTF32"): every operand is split into a TF32 head and a
+// TF32 tail, a = a_hi + a_lo with a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi),
+// and C = A_lo*B_hi + A_hi*B_lo + A_hi*B_hi accumulated in fp32 (the dropped
+// A_lo*B_lo term is ~2^-22 relative).  Plain 1xTF32 misses the 1e-5 contract
+// (SURVEY A.7); 3xTF32 matches fp32 SIMT accuracy.
+//
+// Kernel shape (sm_100a, one CTA per SM, persistent over 128x256 output tiles):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2-D loads of 128x32 A and
+//               256x32 B^T fp32 boxes (SWIZZLE_128B) into a 4-stage ring,
+//               completion on full[stage] (expect_tx)
+//   warp 1      TMEM allocator + MMA issuer: one elected thread issues
+//               tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=256, K=8) from
+//               shared-memory descriptors into a double-buffered TMEM
+//               accumulator (2 x 256 columns); tcgen05.commit frees each stage
+//               (empty[stage]) and publishes a finished tile (tmem_full[acc])
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x16 (warp w reads TMEM lanes
+//               32*(w%4)...), fp32 stores to C, then release the accumulator
+//               (tmem_empty[acc]) so the MMA of the next tile overlaps.
+// The k loop runs 3 phases per tile (lo*hi, hi*lo, hi*hi) over the split
+// operands, i.e. a TF32 GEMM with K' = 3K.  The split (and the transpose that
+// makes B K-major) is a bandwidth-bound prepass.
+#include "common.cuh"
+
+#include <cuda.h>
+
+#include <algorithm>
+
+namespace lapis_b200 {
+
+constexpr int TG_BM = 128, TG_BN = 256, TG_BK = 32, TG_STAGES = 4, TG_UMMA_K = 8;
+constexpr uint32_t TG_A_BYTES = TG_BM * TG_BK * 4;  // 16 KB
+constexpr uint32_t TG_B_BYTES = TG_BN * TG_BK * 4;  // 32 KB
+constexpr uint32_t TG_STAGE_BYTES = TG_A_BYTES + TG_B_BYTES;
+constexpr int TG_THREADS = 192;
+constexpr uint32_t TG_TMEM_COLS = 512;
+constexpr size_t TG_SMEM = (size_t)TG_STAGES * TG_STAGE_BYTES + 1024;
+
+struct Tf32Params {
+  int m, n, nk;       // nk = k blocks of TG_BK
+  int num_m, num_n;   // tile grid
+  float* C;
+  int64_t ldc;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+         "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// K-major operand, SWIZZLE_128B: rows of 128 B, 8-row groups 1024 B apart (SBO);
+// LBO unused for a single 128-B swizzle atom along K; version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  const uint32_t a = smem_u32(p);
+  uint64_t d = 0;
+  d |= (uint64_t)((a & 0x3FFFF) >> 4);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
+__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ----------------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(TG_THREADS, 1)
+gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
+                   const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
+                   Tf32Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[TG_STAGES], empty[TG_STAGES], tmem_full[2], tmem_empty[2];
+  __shared__ uint32_t tmem_base_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = p.num_m * p.num_n;
+  const int kiters = 3 * p.nk;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tA_hi); prefetch_tmap(&tA_lo); prefetch_tmap(&tB_hi); prefetch_tmap(&tB_lo);
+    for (int s = 0; s < TG_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], 128); }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&tmem_base_slot)), "r"(TG_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int mb = tile % p.num_m, nb = tile / p.num_m;
+        for (int it = 0; it < kiters; ++it) {
+          const int ph = it / p.nk, kb = it % p.nk;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * TG_STAGE_BYTES;
+          uint8_t* sb = sa + TG_A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], TG_STAGE_BYTES);
+          tma_load_2d(sa, ph == 0 ? &tA_lo : &tA_hi, kb * TG_BK, mb * TG_BM, &full[stage]);
+          tma_load_2d(sb, ph == 1 ? &tB_lo : &tB_hi, kb * TG_BK, nb * TG_BN, &full[stage]);
+          if (++stage == TG_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc = tf32_idesc(TG_BM, TG_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TG_BN);
+        for (int it = 0; it < kiters; ++it) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint8_t* sa = smem + stage * TG_STAGE_BYTES;
+          const uint64_t adesc = smem_desc_sw128(sa);
+          const uint64_t bdesc = smem_desc_sw128(sa + TG_A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < TG_BK / TG_UMMA_K; ++kk) {
+            // advance the start address by kk * 32 bytes inside the 128-B swizzle atom
+            tc_mma_tf32(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                        (it > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == TG_STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tmem_full[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int lg = warp & 3;                      // TMEM lane group of this warp
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int mb = tile % p.num_m, nb = tile / p.num_m;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * TG_BM + lg * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * TG_BN);
+      float* crow = p.C + (int64_t)row * p.ldc;
+#pragma unroll 1
+      for (int c0 = 0; c0 < TG_BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_x16(tbase + (uint32_t)c0, v);
+        const int col = nb * TG_BN + c0;
+        if (row < p.m) {
+          if (col + 16 <= p.n && (p.ldc % 4 == 0)) {
+            float4* dst = reinterpret_cast<float4*>(crow + col);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                   __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (col + q < p.n) crow[col + q] = __uint_as_float(v[q]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tmem_empty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(tmem_base), "r"(TG_TMEM_COLS));
+  }
+}
+
+// --------------------------------------------------------------- split prepass
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// A [m, k] (lda) -> hi, lo [m, kp], zero padded for k <= j < kp
+__global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float* __restrict__ A,
+                                  int64_t lda, float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = m * kp;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / kp, j = t % kp;
+    const float a = j < k ? A[i * lda + j] : 0.0f;
+    const float h = tf32_rna(a);
+    hi[t] = h;
+    lo[t] = tf32_rna(a - h);
+  }
+}
+
+// B [k, n] (ldb) -> hi, lo [n, kp] (transposed: K-major), zero padded
+__global__ void split_transpose_kernel(int64_t k, int64_t n, int64_t kp, const float* __restrict__ B,
+                                       int64_t ldb, float* __restrict__ hi, float* __restrict__ lo) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t kk = k0 + r, nn = n0 + tx;
+    tile[r][tx] = (kk < k && nn < n) ? B[kk * ldb + nn] : 0.0f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t nn = n0 + r, kk = k0 + tx;
+    if (nn < n && kk < kp) {
+      const float a = tile[tx][r];
+      const float h = tf32_rna(a);
+      hi[nn * kp + kk] = h;
+      lo[nn * kp + kk] = tf32_rna(a - h);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// rows x kp fp32, K-major; box = 32 (k) x box_rows
+static int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t kp,
+                           uint32_t box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)TG_BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return LAPIS_B200_OK;
+}
+
+int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+                int64_t sC, cudaStream_t st) {
+  if (m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
+    return fail(LAPIS_B200_ERR_ARG, "gemm tf32x3: extent too large");
+  const int64_t kp = (k + 3) / 4 * 4;  // 16-byte row pitch for TMA
+  if (k == 0) {
+    for (int64_t b = 0; b < batch; ++b)
+      for (int64_t i = 0; i < m; ++i)
+        LB_TRY(check_cuda(cudaMemsetAsync((float*)C + b * sC + i * ldc, 0, n * sizeof(float), st),
+                          "memset C"));
+    return LAPIS_B200_OK;
+  }
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_tf32x3_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG_SMEM),
+                      "smem attr (gemm_tf32x3_kernel)"));
+    configured_dev = dev;
+  }
+  float* ws = nullptr;
+  const size_t a_elems = (size_t)m * kp, b_elems = (size_t)n * kp;
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, 2 * (a_elems + b_elems) * sizeof(float), st),
+                    "alloc(tf32x3 workspace)"));
+  float* ah = ws;
+  float* al = ah + a_elems;
+  float* bh = al + a_elems;
+  float* bl = bh + b_elems;
+  int rc = LAPIS_B200_OK;
+  for (int64_t b = 0; b < batch && rc == LAPIS_B200_OK; ++b) {
+    const float* Ab = (const float*)A + b * sA;
+    const float* Bb = (const float*)B + b * sB;
+    float* Cb = (float*)C + b * sC;
+    const int64_t sblocks = std::min<int64_t>((m * kp + 255) / 256, (int64_t)num_sms() * 16);
+    split_rows_kernel<<<(unsigned)sblocks, 256, 0, st>>>(m, k, kp, Ab, lda, ah, al);
+    dim3 tg((unsigned)((n + 31) / 32), (unsigned)((kp + 31) / 32));
+    split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl);
+    rc = check_launch("tf32 split");
+    CUtensorMap mah, mal, mbh, mbl;
+    if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mah, ah, m, kp, TG_BM);
+    if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mal, al, m, kp, TG_BM);
+    if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mbh, bh, n, kp, TG_BN);
+    if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mbl, bl, n, kp, TG_BN);
+    if (rc != LAPIS_B200_OK) break;
+    Tf32Params prm;
+    prm.m = (int)m;
+    prm.n = (int)n;
+    prm.nk = (int)((kp + TG_BK - 1) / TG_BK);
+    prm.num_m = (int)((m + TG_BM - 1) / TG_BM);
+    prm.num_n = (int)((n + TG_BN - 1) / TG_BN);
+    prm.C = Cb;
+    prm.ldc = ldc;
+    const int tiles = prm.num_m * prm.num_n;
+    const int grid = std::min(tiles, num_sms());
+    gemm_tf32x3_kernel<<<grid, TG_THREADS, TG_SMEM, st>>>(mah, mal, mbh, mbl, prm);
+    rc = check_launch("gemm_tf32x3_kernel");
+  }
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+}  // namespace lapis_b200

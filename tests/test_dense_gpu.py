@@ -87,3 +87,24 @@ def test_gemv_large_bitexact(cuda_device):
     A = rng.uniform(-1, 1, (3001, 777))
     x = rng.uniform(-1, 1, 777)
     assert bits_equal(host(lb.gemv(cu(A), cu(x))), O.matvec(A, x))
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (129, 65, 257), (1, 300, 5), (300, 257, 1000),
+                                   (1024, 1024, 1024), (45, 70, 130), (7, 9, 3)])
+def test_tf32x3_gemm_fp32_contract(cuda_device, m, n, k):
+    # tcgen05 3xTF32 path: within the fp32 contract (1e-5, diff_outputs) on U(0,1)
+    rng = np.random.default_rng(m + 7 * n + 13 * k)
+    A = rng.uniform(0, 1, (m, k)).astype(np.float32)
+    B = rng.uniform(0, 1, (k, n)).astype(np.float32)
+    got = host(lb.gemm(cu(A), cu(B), mode="tf32x3"))
+    ok, msg = O.diff_outputs([got], [O.matmul(A, B)], 1e-5)
+    assert ok, msg
+
+
+def test_tf32x3_batched(cuda_device):
+    rng = np.random.default_rng(1)
+    A = rng.uniform(0, 1, (3, 70, 90)).astype(np.float32)
+    B = rng.uniform(0, 1, (3, 90, 300)).astype(np.float32)
+    got = host(lb.batch_gemm(cu(A), cu(B), mode="tf32x3"))
+    ok, msg = O.diff_outputs([got], [O.batch_matmul(A, B)], 1e-5)
+    assert ok, msg
