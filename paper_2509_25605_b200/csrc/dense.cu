@@ -238,14 +238,13 @@ int relu(int64_t n, const void* x, void* y, int dtype, cudaStream_t st) {
 
 namespace lapis_b200 {
 
-// tensor-core paths (gemm_tf32x3.cu, gemm_dmma.cu); return UNSUPPORTED when a
-// shape/dtype falls outside what they implement
+// tensor-core paths (gemm_tf32x3.cu, gemm_dmma.cu)
 int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                 const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-                int64_t sC, cudaStream_t st) __attribute__((weak));
+                int64_t sC, cudaStream_t st);
 int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
               const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-              int64_t sC, cudaStream_t st) __attribute__((weak));
+              int64_t sC, cudaStream_t st);
 
 int gemm_dispatch(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
@@ -256,19 +255,19 @@ int gemm_dispatch(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
   if (batch == 0 || m == 0 || n == 0) return LAPIS_B200_OK;
   if (!C || (k > 0 && (!A || !B))) return fail(LAPIS_B200_ERR_ARG, "gemm: null operand");
   if (mode == LAPIS_B200_GEMM_AUTO) {
-    if (dtype == LAPIS_B200_F32 && gemm_tf32x3) mode = LAPIS_B200_GEMM_TF32X3;
-    else if (dtype == LAPIS_B200_F64 && gemm_dmma) mode = LAPIS_B200_GEMM_DMMA;
+    if (dtype == LAPIS_B200_F32) mode = LAPIS_B200_GEMM_TF32X3;
+    else if (dtype == LAPIS_B200_F64) mode = LAPIS_B200_GEMM_DMMA;
     else mode = LAPIS_B200_GEMM_EXACT;
   }
   switch (mode) {
     case LAPIS_B200_GEMM_EXACT:
       return gemm_exact(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, dtype, st);
     case LAPIS_B200_GEMM_TF32X3:
-      if (dtype != LAPIS_B200_F32 || !gemm_tf32x3)
+      if (dtype != LAPIS_B200_F32)
         return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm: TF32X3 is an f32 mode");
       return gemm_tf32x3(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
     case LAPIS_B200_GEMM_DMMA:
-      if (dtype != LAPIS_B200_F64 || !gemm_dmma)
+      if (dtype != LAPIS_B200_F64)
         return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm: DMMA is an f64 mode");
       return gemm_dmma(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
   }

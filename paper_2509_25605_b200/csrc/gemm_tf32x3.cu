@@ -35,7 +35,6 @@ constexpr int TG_BM = 128, TG_BN = 256, TG_BK = 32, TG_STAGES = 4, TG_UMMA_K = 8
 constexpr uint32_t TG_A_BYTES = TG_BM * TG_BK * 4;  // 16 KB
 constexpr uint32_t TG_B_BYTES = TG_BN * TG_BK * 4;  // 32 KB
 constexpr uint32_t TG_STAGE_BYTES = TG_A_BYTES + TG_B_BYTES;
-constexpr int TG_THREADS = 192;
 constexpr uint32_t TG_TMEM_COLS = 512;
 constexpr size_t TG_SMEM = (size_t)TG_STAGES * TG_STAGE_BYTES + 1024;
 
@@ -107,7 +106,17 @@ __device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 // ----------------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(TG_THREADS, 1)
+// Accuracy note: the tensor core adds each MMA into the fp32 accumulator with
+// truncation, so a single accumulator over K' = 3K terms drifts ~#MMA * 2^-25
+// (3e-5 at 4096^3, outside the 1e-5 contract).  The k range is therefore cut
+// into chunks of TG_KC k-blocks; each chunk is accumulated in TMEM (tail
+// phases first, head*head last) and drained by the epilogue into round-to-
+// nearest fp32 register sums, which bounds the drift to ~1e-6.
+constexpr int TG_KC = 8;                 // k-blocks per chunk (256 of K)
+constexpr int TG_EPI_WARPS = 8;          // two per TMEM lane group, 128 columns each
+constexpr int TG_THREADS_V2 = 64 + TG_EPI_WARPS * 32;
+
+__global__ void __launch_bounds__(TG_THREADS_V2, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                    const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                    Tf32Params p) {
@@ -117,12 +126,15 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_const
   __shared__ uint32_t tmem_base_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.num_m * p.num_n;
-  const int kiters = 3 * p.nk;
+  const int nchunks = (p.nk + TG_KC - 1) / TG_KC;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tA_hi); prefetch_tmap(&tA_lo); prefetch_tmap(&tB_hi); prefetch_tmap(&tB_lo);
     for (int s = 0; s < TG_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], 128); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], TG_EPI_WARPS * 32);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -142,15 +154,19 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_const
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const int mb = tile % p.num_m, nb = tile / p.num_m;
-        for (int it = 0; it < kiters; ++it) {
-          const int ph = it / p.nk, kb = it % p.nk;
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * TG_STAGE_BYTES;
-          uint8_t* sb = sa + TG_A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], TG_STAGE_BYTES);
-          tma_load_2d(sa, ph == 0 ? &tA_lo : &tA_hi, kb * TG_BK, mb * TG_BM, &full[stage]);
-          tma_load_2d(sb, ph == 1 ? &tB_lo : &tB_hi, kb * TG_BK, nb * TG_BN, &full[stage]);
-          if (++stage == TG_STAGES) { stage = 0; phase ^= 1; }
+        for (int ch = 0; ch < nchunks; ++ch) {
+          const int kb0 = ch * TG_KC, kb1 = min(kb0 + TG_KC, p.nk);
+          for (int ph = 0; ph < 3; ++ph) {
+            for (int kb = kb0; kb < kb1; ++kb) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* sa = smem + stage * TG_STAGE_BYTES;
+              uint8_t* sb = sa + TG_A_BYTES;
+              mbar_arrive_expect_tx(&full[stage], TG_STAGE_BYTES);
+              tma_load_2d(sa, ph == 0 ? &tA_lo : &tA_hi, kb * TG_BK, mb * TG_BM, &full[stage]);
+              tma_load_2d(sb, ph == 1 ? &tB_lo : &tB_hi, kb * TG_BK, nb * TG_BN, &full[stage]);
+              if (++stage == TG_STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
         }
       }
     }
@@ -163,62 +179,78 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_const
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TG_BN);
-        for (int it = 0; it < kiters; ++it) {
-          mbar_wait(&full[stage], phase);
+        for (int ch = 0; ch < nchunks; ++ch) {
+          const int kb0 = ch * TG_KC, kb1 = min(kb0 + TG_KC, p.nk);
+          mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
           tc_fence_after();
-          const uint8_t* sa = smem + stage * TG_STAGE_BYTES;
-          const uint64_t adesc = smem_desc_sw128(sa);
-          const uint64_t bdesc = smem_desc_sw128(sa + TG_A_BYTES);
+          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TG_BN);
+          bool first = true;
+          for (int ph = 0; ph < 3; ++ph) {
+            for (int kb = kb0; kb < kb1; ++kb) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint8_t* sa = smem + stage * TG_STAGE_BYTES;
+              const uint64_t adesc = smem_desc_sw128(sa);
+              const uint64_t bdesc = smem_desc_sw128(sa + TG_A_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < TG_BK / TG_UMMA_K; ++kk) {
-            // advance the start address by kk * 32 bytes inside the 128-B swizzle atom
-            tc_mma_tf32(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
-                        (it > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < TG_BK / TG_UMMA_K; ++kk) {
+                // advance the start address by kk * 32 bytes inside the 128-B swizzle atom
+                tc_mma_tf32(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2),
+                            idesc, first ? 0u : 1u);
+                first = false;
+              }
+              tc_commit(&empty[stage]);
+              if (++stage == TG_STAGES) { stage = 0; phase ^= 1; }
+            }
           }
-          tc_commit(&empty[stage]);
-          if (++stage == TG_STAGES) { stage = 0; phase ^= 1; }
+          tc_commit(&tmem_full[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        tc_commit(&tmem_full[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int lg = warp & 3;                      // TMEM lane group of this warp
+    const int ew = warp - 2;                 // 0..7
+    const int lg = warp & 3;                 // TMEM lane group this warp may access
+    const int half = ew >> 2;                // columns [128*half, 128*half + 128)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int mb = tile % p.num_m, nb = tile / p.num_m;
-      mbar_wait(&tmem_full[acc], acc_phase);
-      tc_fence_after();
+      float sum[128];
+#pragma unroll
+      for (int q = 0; q < 128; ++q) sum[q] = 0.0f;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        mbar_wait(&tmem_full[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) +
+                               (uint32_t)(acc * TG_BN + half * 128);
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld_x16(tbase + (uint32_t)c0, v);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) sum[c0 + q] = __fadd_rn(sum[c0 + q], __uint_as_float(v[q]));
+        }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
       const int row = mb * TG_BM + lg * 32 + lane;
-      const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * TG_BN);
-      float* crow = p.C + (int64_t)row * p.ldc;
-#pragma unroll 1
-      for (int c0 = 0; c0 < TG_BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_x16(tbase + (uint32_t)c0, v);
-        const int col = nb * TG_BN + c0;
-        if (row < p.m) {
-          if (col + 16 <= p.n && (p.ldc % 4 == 0)) {
-            float4* dst = reinterpret_cast<float4*>(crow + col);
+      const int col0 = nb * TG_BN + half * 128;
+      if (row < p.m) {
+        float* crow = p.C + (int64_t)row * p.ldc;
+        if (col0 + 128 <= p.n && (p.ldc % 4 == 0)) {
+          float4* dst = reinterpret_cast<float4*>(crow + col0);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                   __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-          } else {
+          for (int q = 0; q < 32; ++q)
+            dst[q] = make_float4(sum[4 * q], sum[4 * q + 1], sum[4 * q + 2], sum[4 * q + 3]);
+        } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (col + q < p.n) crow[col + q] = __uint_as_float(v[q]);
-          }
+          for (int q = 0; q < 128; ++q)
+            if (col0 + q < p.n) crow[col0 + q] = sum[q];
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tmem_empty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();
@@ -363,7 +395,7 @@ int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, i
     prm.ldc = ldc;
     const int tiles = prm.num_m * prm.num_n;
     const int grid = std::min(tiles, num_sms());
-    gemm_tf32x3_kernel<<<grid, TG_THREADS, TG_SMEM, st>>>(mah, mal, mbh, mbl, prm);
+    gemm_tf32x3_kernel<<<grid, TG_THREADS_V2, TG_SMEM, st>>>(mah, mal, mbh, mbl, prm);
     rc = check_launch("gemm_tf32x3_kernel");
   }
   cudaFreeAsync(ws, st);

@@ -108,3 +108,15 @@ def test_tf32x3_batched(cuda_device):
     got = host(lb.batch_gemm(cu(A), cu(B), mode="tf32x3"))
     ok, msg = O.diff_outputs([got], [O.batch_matmul(A, B)], 1e-5)
     assert ok, msg
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 128, 16), (130, 66, 258), (1000, 600, 512), (32, 32, 32),
+                                   (2, 2, 2), (257, 129, 33), (64, 4, 1024)])
+def test_dmma_gemm_fp64_contract(cuda_device, m, n, k):
+    # DMMA path (odd extents fall back to the exact kernel): within the 1e-12 contract
+    rng = np.random.default_rng(m * 3 + n * 5 + k)
+    A = rng.uniform(-1, 1, (m, k))
+    B = rng.uniform(-1, 1, (k, n))
+    got = host(lb.gemm(cu(A), cu(B), mode="dmma"))
+    ok, msg = O.diff_outputs([got], [O.matmul(A, B)], 1e-12)
+    assert ok, msg
