@@ -66,6 +66,7 @@ int lapis_b200_init(int device) {
   if (prop.major != 10)
     return fail(LAPIS_B200_ERR_UNSUPPORTED, "init: kernels are built for sm_100a (B200)");
   LB_TRY(check_cuda(cudaFree(nullptr), "context init"));
+  keep_pool_memory();
   return LAPIS_B200_OK;
 }
 
@@ -90,12 +91,14 @@ int lapis_b200_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* r
                         int rowptr_bytes, const void* colind, int colind_bytes,
                         const void* values, const void* x, void* y, int dtype,
                         int vector_length, void* stream) {
+  keep_pool_memory();
   return spmv_csr(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, x, y,
                   dtype, vector_length, S(stream));
 }
 
 int lapis_b200_csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rowptr_bytes,
                                void* stream, lapis_b200_csr_plan* out_plan) {
+  keep_pool_memory();
   return csr_plan_create(nrows, nnz, rowptr, rowptr_bytes, S(stream),
                          reinterpret_cast<void**>(out_plan));
 }
@@ -121,12 +124,14 @@ int lapis_b200_spmm_csr(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, co
                         int rowptr_bytes, const void* colind, int colind_bytes,
                         const void* values, const void* X, int64_t ldx, void* Y, int64_t ldy,
                         int dtype, void* stream) {
+  keep_pool_memory();
   return spmm_csr(nrows, ncols, nnz, k, rowptr, rowptr_bytes, colind, colind_bytes, values, X,
                   ldx, Y, ldy, dtype, S(stream));
 }
 
 int lapis_b200_gemm(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
                     int64_t ldb, void* C, int64_t ldc, int dtype, int mode, void* stream) {
+  keep_pool_memory();
   return gemm_dispatch(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, dtype, mode, S(stream));
 }
 
@@ -140,6 +145,7 @@ int lapis_b200_gemv(int64_t m, int64_t n, const void* A, int64_t lda, const void
 
 int lapis_b200_batch_gemm(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
                           const void* B, void* C, int dtype, int mode, void* stream) {
+  keep_pool_memory();
   if (batch < 0) return fail(LAPIS_B200_ERR_ARG, "batch_gemm: negative batch");
   return gemm_dispatch(batch, m, n, k, A, k, B, n, C, n, m * k, k * n, m * n, dtype, mode,
                        S(stream));
@@ -162,6 +168,7 @@ int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream) 
 
 int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,
                              int64_t* rowptr, int32_t* colind, double* values, void* stream) {
+  keep_pool_memory();
   return synth_stencil(points, n, row_begin, row_end, rowptr, colind, values, S(stream));
 }
 

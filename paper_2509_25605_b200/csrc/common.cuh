@@ -78,6 +78,23 @@ __device__ __forceinline__ longlong2 ld_stream(const longlong2* p) {
   return r;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// memory pool; keep freed blocks cached in the pool instead of returning them
+// to the driver at every synchronisation (the default release threshold of 0
+// turns every per-call workspace into a fresh mapping).
+inline void keep_pool_memory() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 inline int elem_bytes(int dtype) {
   return (dtype == LAPIS_B200_F64 || dtype == LAPIS_B200_I64) ? 8 : 4;
 }
