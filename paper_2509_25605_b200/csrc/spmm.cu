@@ -5,11 +5,11 @@
 // with the per-(i, c) order of interp.py:798-812: j ascending, mul and add
 // each rounded.
 //
-// Kernel 1 (spmm_row_kernel): one warp per row, lanes across the dense
-//   columns (2 per lane, 16-byte vector gathers of each X row), the j loop
-//   walked in ascending order with non-contracted mul/add -> bit-identical to
-//   the reference for every row of <= SPLIT entries.  Rows longer than SPLIT
-//   are left to kernels 2-3.
+// Kernel 1 (spmm_group_kernel; spmm_row_kernel for unaligned operands): G
+//   lanes per row, lanes across the dense columns (16-byte gathers of each X
+//   row slice), the j loop walked in ascending order with non-contracted
+//   mul/add -> bit-identical to the reference for every row of <= SPLIT
+//   entries.  Rows longer than SPLIT are left to kernels 2-3.
 // Kernel 2 (spmm_chunk_kernel): the nonzero stream is cut into fixed chunks of
 //   SPLIT entries; for each long row overlapping chunk q a CTA computes the
 //   partial row over the overlap (8 warps on contiguous sub-ranges, folded in
@@ -88,6 +88,85 @@ spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
 #pragma unroll
     for (int q = 0; q < EPL; ++q)
       if (col + q < k) yr[q] = acc[q];
+  }
+}
+
+// ------------------------------------------------------ kernel 1 (grouped)
+// G lanes per row, 4 consecutive dense columns per lane (fp64: two 16-byte
+// gathers per X row slice), 32/G rows per warp, persistent grid-stride over
+// row groups.  The entries of a row are walked 4 at a time with predication:
+// out-of-row steps contribute value 0 * x 0 = +0.0, which leaves the running
+// per-column sum unchanged, so the ascending sequential order (and the
+// bit-identity with the reference) is kept while 4 X-row gathers per row are
+// in flight.
+template <class T>
+__device__ __forceinline__ void ldg4(const T* p, T (&v)[4]) {
+  if constexpr (sizeof(T) == 8) {
+    const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(p));
+    const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(p + 2));
+    memcpy(&v[0], &a.x, 8); memcpy(&v[1], &a.y, 8); memcpy(&v[2], &b.x, 8); memcpy(&v[3], &b.y, 8);
+  } else {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(p));
+    memcpy(&v[0], &a.x, 4); memcpy(&v[1], &a.y, 4); memcpy(&v[2], &a.z, 4); memcpy(&v[3], &a.w, 4);
+  }
+}
+template <class T>
+__device__ __forceinline__ void stg4(T* p, const T (&v)[4]) {
+  if constexpr (sizeof(T) == 8) {
+    longlong2 a, b;
+    memcpy(&a.x, &v[0], 8); memcpy(&a.y, &v[1], 8); memcpy(&b.x, &v[2], 8); memcpy(&b.y, &v[3], 8);
+    *reinterpret_cast<longlong2*>(p) = a;
+    *reinterpret_cast<longlong2*>(p + 2) = b;
+  } else {
+    int4 a;
+    memcpy(&a.x, &v[0], 4); memcpy(&a.y, &v[1], 4); memcpy(&a.z, &v[2], 4); memcpy(&a.w, &v[3], 4);
+    *reinterpret_cast<int4*>(p) = a;
+  }
+}
+
+template <class T, class RP, class CI, int G>
+__global__ void __launch_bounds__(256)
+spmm_group_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+                  const CI* __restrict__ colind, const T* __restrict__ values,
+                  const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  for (int64_t row = g0; row < nrows; row += groups) {
+    const int64_t b = (int64_t)rowptr[row];
+    int64_t e = (int64_t)rowptr[row + 1];
+    if (e < b) e = b;
+    if (e - b > SPLIT) continue;  // long row: kernels 2-3
+    for (int64_t c0 = 4 * lane; c0 < k; c0 += 4 * G) {
+      T acc[4] = {Arith<T>::zero(), Arith<T>::zero(), Arith<T>::zero(), Arith<T>::zero()};
+      for (int64_t j0 = b; j0 < e; j0 += U) {
+        T v[U];
+        int64_t ci[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = j0 + u < e;
+          v[u] = ok ? values[j0 + u] : T(0);
+          ci[u] = ok ? (int64_t)colind[j0 + u] : -1;
+        }
+        T xv[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (ci[u] >= 0) {
+            ldg4(X + ci[u] * ldx + c0, xv[u]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) xv[u][q] = T(0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v[u], xv[u][q]));
+      }
+      T* yr = Y + row * ldy + c0;
+      stg4(yr, acc);
+    }
   }
 }
 
@@ -200,8 +279,26 @@ struct SpmmOp {
                  cudaStream_t st) {
     const int64_t blocks = (nrows + SPMM_WARPS - 1) / SPMM_WARPS;
     if (blocks > 0x7fffffffLL) return fail(LAPIS_B200_ERR_ARG, "spmm: too many rows");
+    const bool grp = (k % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
+                     ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
     const bool vec = (ldx % 2 == 0) && ((uintptr_t)X % (2 * sizeof(T)) == 0);
-    if (vec)
+    if (grp) {
+      const int64_t lanes_per_row = k >= 64 ? 16 : (k >= 32 ? 8 : (k >= 16 ? 4 : (k >= 8 ? 2 : 1)));
+      int64_t gblocks = (nrows * lanes_per_row + 255) / 256;
+      const int64_t cap = (int64_t)num_sms() * 8;
+      if (gblocks > cap) gblocks = cap;
+      if (gblocks < 1) gblocks = 1;
+#define LB_GRP(GG) spmm_group_kernel<T, RP, CI, GG><<<(unsigned)gblocks, 256, 0, st>>>( \
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy)
+      switch (lanes_per_row) {
+        case 16: LB_GRP(16); break;
+        case 8: LB_GRP(8); break;
+        case 4: LB_GRP(4); break;
+        case 2: LB_GRP(2); break;
+        default: LB_GRP(1); break;
+      }
+#undef LB_GRP
+    } else if (vec)
       spmm_row_kernel<T, RP, CI, 2><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
           (T*)Y, ldy);
