@@ -47,23 +47,17 @@ spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
     T acc[EPL];
 #pragma unroll
     for (int q = 0; q < EPL; ++q) acc[q] = Arith<T>::zero();
-    // predicated 8-deep unroll: out-of-row steps add +0.0 (exact), so the
-    // per-column ascending order is kept with 8 X-row gathers in flight
-    constexpr int U = 8;
-    for (int64_t j0 = b; j0 < e; j0 += U) {
-      T v[U];
-      int64_t ci[U];
+    int64_t j = b;
+    for (; j + 4 <= e; j += 4) {
+      T v[4];
+      int64_t ci[4];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = j0 + u < e;
-        v[u] = ok ? values[j0 + u] : T(0);
-        ci[u] = ok ? (int64_t)colind[j0 + u] : -1;
-      }
-      T xv[U][EPL];
+      for (int u = 0; u < 4; ++u) { v[u] = values[j + u]; ci[u] = (int64_t)colind[j + u]; }
+      T xv[4][EPL];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const T* xr = X + (ci[u] < 0 ? 0 : ci[u]) * ldx + col;
-        if (ci[u] >= 0 && EPL == 2 && full) {
+      for (int u = 0; u < 4; ++u) {
+        const T* xr = X + ci[u] * ldx + col;
+        if (EPL == 2 && full) {
           if constexpr (sizeof(T) == 8) {
             const longlong2 w = __ldg(reinterpret_cast<const longlong2*>(xr));
             memcpy(&xv[u][0], &w.x, 8);
@@ -75,14 +69,20 @@ spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < EPL; ++q)
-            xv[u][q] = (ci[u] >= 0 && col + q < k) ? __ldg(xr + q) : Arith<T>::zero();
+          for (int q = 0; q < EPL; ++q) xv[u][q] = (col + q < k) ? __ldg(xr + q) : Arith<T>::zero();
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int q = 0; q < EPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v[u], xv[u][q]));
+    }
+    for (; j < e; ++j) {
+      const T v = values[j];
+      const T* xr = X + (int64_t)colind[j] * ldx + col;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q)
+        if (col + q < k) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v, __ldg(xr + q)));
     }
     T* yr = Y + row * ldy + col;
 #pragma unroll
