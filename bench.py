@@ -448,6 +448,90 @@ class DenseMatmul(Workload):
         return Cref, got, times, 2.0 * rows * self.n * self.n, desc, tol
 
 
+class GcnLayer(Workload):
+    """Config 4: GCN layer H = relu((A_hat X) W), fp32, A_hat = D^-1/2 A D^-1/2 of the
+    config-3 power-law generator at 1M rows, X [N, 64] U(0,1), W [64, 64]
+    U(-1/8, 1/8) (torch Linear default bound for fan-in 64), seed 4."""
+
+    name = "config4: GCN layer relu((A_hat X) W) fp32, power-law A_hat 1M rows, 64->64"
+    dtype = "f32"
+    scaling = "weak"
+
+    def __init__(self, args, rank, world, n=1_000_000, f=64, seed=4):
+        import paper_2509_25605_b200 as lb
+        self.lb, self.args, self.world, self.N, self.f = lb, args, world, n, f
+        self.stream = torch.cuda.current_stream()
+        rowptr, colind, _ = powerlaw_csr_device(n, 10.0, 2.5, seed)
+        deg = (rowptr[1:] - rowptr[:-1]).clamp(min=1).to(torch.float64)
+        rows = torch.repeat_interleave(torch.arange(n, device="cuda"), rowptr[1:] - rowptr[:-1])
+        vals = (deg[rows] * deg[colind.long()]).rsqrt().to(torch.float32)
+        self.rowptr, self.colind, self.values = rowptr, colind, vals.contiguous()
+        self.nnz = int(rowptr[-1].item())
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        self.X = torch.rand((n, f), generator=g, dtype=torch.float32, device="cuda")
+        self.W = (torch.rand((f, f), generator=g, dtype=torch.float32, device="cuda") * 2 - 1) / 8
+        self.H = torch.empty((n, f), dtype=torch.float32, device="cuda")
+        self.max_len = int((rowptr[1:] - rowptr[:-1]).max().item())
+        torch.cuda.synchronize()
+
+    def config(self):
+        return {"workload": self.name, "rows": self.N, "nnz": self.nnz, "features": self.f,
+                "max_row": self.max_len, "parallelism": "replica",
+                "l2": "inputs > L2 (X 256 MB)"}
+
+    def work_local(self):
+        f, n = self.f, self.N
+        spmm = self.nnz * 8 + (n + 1) * 8 + n * f * 4 + n * f * 4
+        dense = n * f * 4 + f * f * 4 + n * f * 4
+        return spmm + dense
+
+    def work_global(self):
+        return self.work_local() * self.world
+
+    def launches_per_step(self):
+        return 4 if self.max_len > 2048 else 2
+
+    def kernel_name(self):
+        return "spmm_row_kernel<float> + gemm_exact_kernel<float, relu> (reference order)"
+
+    def step(self):
+        self.lb.gcn_layer(self.rowptr, self.colind, self.values, self.X, self.W, self.H,
+                          nnz=self.nnz)
+
+    def e2e(self, steps, warmup):
+        """X (node features) host-modified every step, H read back."""
+        from paper_2509_25605_b200.dualview import DualView
+        xs = DualView.from_host(self.X.cpu(), "X", device_buffer=self.X)
+        hs = DualView.allocate(tuple(self.H.shape), torch.float32, "H")
+
+        def one():
+            xs.modify_host()
+            xs.sync_device(self.stream)
+            self.lb.gcn_layer(self.rowptr, self.colind, self.values, xs.device_view(), self.W,
+                              hs.device_view(), nnz=self.nnz)
+            hs.modify_device()
+            hs.sync_host(self.stream)
+
+        return timed_e2e(one, steps, warmup, self.world), xs.nbytes, hs.nbytes
+
+    def cpu_reference(self, rows_sample, threads, reps):
+        from oracle import ref as R
+        a, b = 0, min(self.N, max(1, rows_sample // 80))
+        rp = self.rowptr[a:b + 1].cpu().numpy()
+        ci = self.colind[rp[0]:rp[-1]].cpu().numpy()
+        v = self.values[rp[0]:rp[-1]].cpu().numpy()
+        rp = rp - rp[0]
+        threads = min(threads, 4)   # each block replicates X (256 MB) on the stub
+        Href, times = R.gcn(rp, ci, v, self.X.cpu().numpy(), self.W.cpu().numpy(), reps=reps,
+                            threads=threads)
+        nnz = int(rp[-1])
+        f = self.f
+        work = nnz * 8 + (b - a + 1) * 8 + (b - a) * f * 4 * 3 + f * f * 4
+        desc = (f"rows [{a}, {b}) ({nnz} nnz): reference emitted Kokkos C++ of "
+                f"oracle/ir/gcn_f32.mlir on its serial stub, {threads} row blocks")
+        return Href, self.H[a:b].cpu().numpy(), times, work, desc, 1e-5
+
+
 def powerlaw_csr_device(n, mean, alpha, seed):
     """Chung-Lu power-law CSR built on the device: Pareto(alpha) row
     weights, rows and columns drawn in proportion to the weights, hubs scattered
@@ -486,6 +570,7 @@ WORKLOADS = {
     "c3": lambda args, r, w: PowerLawSpmm(args, r, w, args.n or 10_000_000),
     "c2f32": lambda args, r, w: DenseMatmul(args, r, w, torch.float32, args.n or 4096),
     "c2f64": lambda args, r, w: DenseMatmul(args, r, w, torch.float64, args.n or 4096),
+    "c4": lambda args, r, w: GcnLayer(args, r, w, args.n or 1_000_000),
 }
 
 

@@ -144,6 +144,18 @@ int lapis_b200_reduce_2d(int64_t rows, int64_t cols, const void* src, void* out,
  * interp.py:520-545, 766-776). */
 int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream);
 
+/* ---------------------------------------------------------------- GCN layer
+ * H = relu((A_hat X) W): config 4, the reference's one-function GCN
+ * (oracle/ir/gcn_f32.mlir: loop-nest SpMM + linalg.matmul + linalg.elementwise
+ * cmpf ogt / select).  X is [ncols, fin], W [fin, fout], H
+ * [nrows, fout], row-major; both stages in the reference's order
+ * (bit-identical).  dtype F32 or F64. */
+int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz,
+                         const void* rowptr, int rowptr_bytes,
+                         const void* colind, int colind_bytes, const void* values,
+                         const void* X, int64_t fin, const void* W, int64_t fout, void* H,
+                         int dtype, void* stream);
+
 /* ------------------------------------------------------- synthetic inputs
  * Not reference interfaces: on-device generators for the benchmark matrices
  * (SURVEY 8(d)), rows [row_begin, row_end) of an n^d-point grid, natural

@@ -53,6 +53,8 @@ _SIGNATURES = {
     "lapis_b200_batch_gemm": ([_I64, _I64, _I64, _I64, _VP, _VP, _VP, _INT, _INT, _VP], _INT),
     "lapis_b200_reduce_2d": ([_I64, _I64, _VP, _VP, _INT, _INT, _INT, _VP], _INT),
     "lapis_b200_relu": ([_I64, _VP, _VP, _INT, _VP], _INT),
+    "lapis_b200_gcn_layer": ([_I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP, _I64,
+                              _VP, _INT, _VP], _INT),
     "lapis_b200_synth_stencil": ([_INT, _I64, _I64, _I64, _VP, _VP, _VP, _VP], _INT),
 }
 

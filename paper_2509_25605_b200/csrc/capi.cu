@@ -41,6 +41,8 @@ int gemm_dispatch(int64_t, int64_t, int64_t, int64_t, const void*, int64_t, cons
 int gemv(int64_t, int64_t, const void*, int64_t, const void*, void*, int, cudaStream_t);
 int reduce_2d(int64_t, int64_t, const void*, void*, int, int, int, cudaStream_t);
 int relu(int64_t, const void*, void*, int, cudaStream_t);
+int gcn_layer(int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
+              const void*, int64_t, const void*, int64_t, void*, int, cudaStream_t);
 int synth_stencil(int, int64_t, int64_t, int64_t, int64_t*, int32_t*, double*, cudaStream_t);
 void release_workspaces();
 
@@ -164,6 +166,15 @@ int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream) 
   if (n < 0) return fail(LAPIS_B200_ERR_ARG, "relu: negative extent");
   if (n > 0 && (!x || !y)) return fail(LAPIS_B200_ERR_ARG, "relu: null operand");
   return relu(n, x, y, dtype, S(stream));
+}
+
+int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr,
+                         int rowptr_bytes, const void* colind, int colind_bytes, const void* values,
+                         const void* X, int64_t fin, const void* W, int64_t fout, void* H,
+                         int dtype, void* stream) {
+  keep_pool_memory();
+  return gcn_layer(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, X, fin,
+                   W, fout, H, dtype, S(stream));
 }
 
 int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,

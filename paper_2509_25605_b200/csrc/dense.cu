@@ -57,7 +57,7 @@ __device__ __forceinline__ T combine(T acc, T v, int comb) {
 constexpr int EG_TILE = 32;   // C tile 32 x 32, K slab 32
 constexpr int EG_ROWS = 4;    // outputs per thread (rows)
 
-template <class T>
+template <class T, bool RELU>
 __global__ void __launch_bounds__(256)
 gemm_exact_kernel(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int64_t lda,
                   const T* __restrict__ B, int64_t ldb, T* __restrict__ C, int64_t ldc,
@@ -94,7 +94,8 @@ gemm_exact_kernel(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int6
 #pragma unroll
   for (int q = 0; q < EG_ROWS; ++q) {
     const int64_t r = row0 + ty * EG_ROWS + q, c = col0 + tx;
-    if (r < m && c < n) C[r * ldc + c] = acc[q];
+    // RELU: the GCN elementwise select (cmpf ogt + select) fused into the store
+    if (r < m && c < n) C[r * ldc + c] = RELU ? ((acc[q] > T(0)) ? acc[q] : T(0)) : acc[q];
   }
 }
 
@@ -152,15 +153,15 @@ __global__ void relu_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ 
 }
 
 // =============================================================== host side
-template <class T>
+template <class T, bool RELU = false>
 static int launch_gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
                              int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                              int64_t sA, int64_t sB, int64_t sC, cudaStream_t st) {
   dim3 grid((unsigned)((n + EG_TILE - 1) / EG_TILE), (unsigned)((m + EG_TILE - 1) / EG_TILE),
             (unsigned)batch);
   if (grid.y > 65535 || grid.z > 65535) return fail(LAPIS_B200_ERR_ARG, "gemm: grid too large");
-  gemm_exact_kernel<T><<<grid, 256, 0, st>>>(m, n, k, (const T*)A, lda, (const T*)B, ldb, (T*)C,
-                                             ldc, sA, sB, sC);
+  gemm_exact_kernel<T, RELU><<<grid, 256, 0, st>>>(m, n, k, (const T*)A, lda, (const T*)B, ldb,
+                                                   (T*)C, ldc, sA, sB, sC);
   return check_launch("gemm_exact_kernel");
 }
 
@@ -183,6 +184,16 @@ static int launch_row_fold(int64_t m, int64_t n, const void* A, int64_t lda, con
   row_fold_kernel<T, DOT><<<(unsigned)blocks, RF_ROWS, 0, st>>>(m, n, (const T*)A, lda,
                                                                   (const T*)x, (T*)y, comb);
   return check_launch("row_fold_kernel");
+}
+
+// C = relu(A B) in the reference order (GCN second stage, oracle/ir/gcn_f32.mlir)
+int gemm_exact_relu(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                    int64_t ldb, void* C, int64_t ldc, int dtype, cudaStream_t st) {
+  if (dtype == LAPIS_B200_F32)
+    return launch_gemm_exact<float, true>(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, st);
+  if (dtype == LAPIS_B200_F64)
+    return launch_gemm_exact<double, true>(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, st);
+  return fail(LAPIS_B200_ERR_UNSUPPORTED, "gcn: floating-point dtypes only");
 }
 
 int gemv(int64_t m, int64_t n, const void* A, int64_t lda, const void* x, void* y, int dtype,

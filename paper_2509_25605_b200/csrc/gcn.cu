@@ -1,0 +1,42 @@
+// gcn.cu — the config-4 GCN layer H = relu((A_hat X) W) as one library call.
+//
+// The reference expresses it as one IR function (oracle/ir/gcn_f32.mlir,
+// SURVEY A.5): a loop-nest SpMM into a device-local temporary, linalg.matmul
+// into a second temporary, and linalg.elementwise ReLU (cmpf ogt + select).
+// Here: the SpMM kernels (reference order per output column, fp32 hub rows
+// included) write A_hat X to a stream-ordered workspace, then the
+// reference-order GEMM applies W with the ReLU select fused into its store.
+// Both stages follow the reference's summation order, so H is bit-identical
+// to the reference interpreter (tests/test_gcn_gpu.py).
+#include "common.cuh"
+
+namespace lapis_b200 {
+
+int spmm_csr(int64_t, int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
+             const void*, int64_t, void*, int64_t, int, cudaStream_t);
+int gemm_exact_relu(int64_t, int64_t, int64_t, const void*, int64_t, const void*, int64_t, void*,
+                    int64_t, int, cudaStream_t);
+
+int gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int rp_bytes,
+              const void* colind, int ci_bytes, const void* values, const void* X, int64_t fin,
+              const void* W, int64_t fout, void* H, int dtype, cudaStream_t st) {
+  if (dtype != LAPIS_B200_F32 && dtype != LAPIS_B200_F64)
+    return fail(LAPIS_B200_ERR_UNSUPPORTED, "gcn: floating-point dtypes only");
+  if (nrows < 0 || fin < 0 || fout < 0) return fail(LAPIS_B200_ERR_ARG, "gcn: negative extent");
+  if (nrows == 0 || fout == 0) return LAPIS_B200_OK;
+  if (!W || !H) return fail(LAPIS_B200_ERR_ARG, "gcn: null operand");
+  const size_t es = (size_t)elem_bytes(dtype);
+  void* ax = nullptr;
+  LB_TRY(check_cuda(cudaMallocAsync(&ax, (size_t)nrows * (size_t)(fin > 0 ? fin : 1) * es, st),
+                    "alloc(gcn A_hat X)"));
+  int rc = LAPIS_B200_OK;
+  if (fin > 0)
+    rc = spmm_csr(nrows, ncols, nnz, fin, rowptr, rp_bytes, colind, ci_bytes, values, X, fin, ax,
+                  fin, dtype, st);
+  if (rc == LAPIS_B200_OK)
+    rc = gemm_exact_relu(nrows, fout, fin, ax, fin, W, fout, H, fout, dtype, st);
+  cudaFreeAsync(ax, st);
+  return rc;
+}
+
+}  // namespace lapis_b200

@@ -192,6 +192,11 @@ __global__ void __launch_bounds__(SPMM_WARPS * 32)
 spmm_seq_long_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                      const CI* __restrict__ colind, const T* __restrict__ values,
                      const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  // products of SEQ_CH entries x KC columns staged per round: every thread gathers
+  // (all loads of a round in flight at once), then one thread per column folds
+  // the round in ascending entry order
+  constexpr int SEQ_CH = 32, KC = 64;
+  __shared__ T stage[SEQ_CH][KC];
   const int64_t q = blockIdx.x;
   const int64_t base = (int64_t)rowptr[0];
   const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
@@ -199,12 +204,23 @@ spmm_seq_long_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
   if (r >= nrows) return;
   const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
   if (b < lo || b >= hi || e - b <= SPLIT) return;
-  for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
+  for (int64_t c0 = 0; c0 < k; c0 += KC) {
+    const int kc = (int)((k - c0) < KC ? (k - c0) : KC);
     T acc = Arith<T>::zero();
-#pragma unroll 8
-    for (int64_t j = b; j < e; ++j)
-      acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(X + (int64_t)colind[j] * ldx + col)));
-    Y[r * ldy + col] = acc;
+    for (int64_t j0 = b; j0 < e; j0 += SEQ_CH) {
+      const int n = (int)((e - j0) < SEQ_CH ? (e - j0) : SEQ_CH);
+      __syncthreads();
+      for (int t = threadIdx.x; t < SEQ_CH * KC; t += blockDim.x) {
+        const int jj = t / KC, cc = t % KC;
+        if (jj < n && cc < kc)
+          stage[jj][cc] = Arith<T>::mul(values[j0 + jj],
+                                        __ldg(X + (int64_t)colind[j0 + jj] * ldx + c0 + cc));
+      }
+      __syncthreads();
+      if (threadIdx.x < kc)
+        for (int jj = 0; jj < n; ++jj) acc = Arith<T>::add(acc, stage[jj][threadIdx.x]);
+    }
+    if (threadIdx.x < kc) Y[r * ldy + c0 + threadIdx.x] = acc;
   }
 }
 

@@ -248,6 +248,27 @@ def relu(x, y=None, *, stream=None):
     return y
 
 
+def gcn_layer(rowptr, colind, values, X, W, H=None, *, nnz: int | None = None, stream=None):
+    """H = relu((A_hat X) W) — config 4 (oracle/ir/gcn_f32.mlir), reference order."""
+    for t, nm in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (X, "X"), (W, "W")):
+        _dev(t, nm)
+    if X.dim() != 2 or W.dim() != 2 or X.shape[1] != W.shape[0]:
+        raise BackendError("gcn: X [ncols, fin] and W [fin, fout] expected", _capi.ERR_ARG)
+    nrows = rowptr.numel() - 1
+    if H is None:
+        H = torch.empty((nrows, W.shape[1]), dtype=values.dtype, device=values.device)
+    _dev(H, "H")
+    if not (values.dtype == X.dtype == W.dtype == H.dtype):
+        raise BackendError("gcn: element types must match", _capi.ERR_ARG)
+    if nnz is None:
+        nnz = int(rowptr[-1].item() - rowptr[0].item())
+    check(_capi.lib().lapis_b200_gcn_layer(
+        nrows, X.shape[0], nnz, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"), _ptr(colind),
+        _idx_bytes(colind, "colind"), _ptr(values), _ptr(X), X.shape[1], _ptr(W), W.shape[1],
+        _ptr(H), _dtype(values, "values"), _stream(stream)), "gcn_layer")
+    return H
+
+
 def synth_stencil(points: int, n: int, row_begin: int = 0, row_end: int | None = None,
                   device="cuda", stream=None):
     """Generate rows [row_begin, row_end) of the 5-point (2-D) or 27-point (3-D)

@@ -1,0 +1,37 @@
+"""Config 4: the GCN layer relu((A_hat X) W) against the reference interpreter
+(fixture gcn_small from oracle/ir/gcn_f32.mlir) and the oracle on a power-law
+graph with hub rows: bit-identical (both stages follow the reference order)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2509_25605_b200 as lb
+from conftest import bits_equal, load_golden
+from matrices import ragged_csr
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def test_golden_gcn_bitexact(cuda_device):
+    g = load_golden("gcn_small")
+    rowptr, colind, values, X, W, _ = g["inputs"]
+    H = lb.gcn_layer(cu(rowptr), cu(colind), cu(values), cu(X), cu(W)).cpu().numpy()
+    assert bits_equal(H, g["outputs"][0])
+
+
+@pytest.mark.parametrize("fin,fout", [(64, 64), (16, 40), (3, 8)])
+def test_gcn_hub_rows_bitexact(cuda_device, fin, fout):
+    rng = np.random.default_rng(fin * fout)
+    rowptr, colind, values = ragged_csr(rng, 3000, 5000, max_len=20, empty_every=17,
+                                        long_rows={4: 4999, 2000: 2600, 2999: 3000},
+                                        dtype=np.float32)
+    values = np.abs(values)
+    X = rng.uniform(0, 1, (5000, fin)).astype(np.float32)
+    W = rng.uniform(-1 / 8, 1 / 8, (fin, fout)).astype(np.float32)
+    H = lb.gcn_layer(cu(rowptr), cu(colind), cu(values), cu(X), cu(W)).cpu().numpy()
+    assert bits_equal(H, O.gcn(rowptr, colind, values, X, W))
