@@ -108,6 +108,17 @@ int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int r
 int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out4);
 int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact);
 
+/* Structure validation (synchronous: reads two flags back).  The reference
+ * interpreter bounds-checks every load (interp.py:269-276); the tuned kernels
+ * do not, so the executor validates a CSR once before using them.
+ * out4[0] = 0 ok, 1 a row range leaves [0, nentries), 2 a column leaves
+ * [0, ncols), 3 rowptr decreases somewhere (legal: such rows are empty, but
+ * the tuned kernels assume monotone rowptr); out4[1] = raw flag bits;
+ * out4[3] = rowptr[nrows] - rowptr[0]. */
+int lapis_b200_csr_check(int64_t nrows, const void* rowptr, int rowptr_bytes,
+                         const void* colind, int colind_bytes, int64_t nentries,
+                         int64_t ncols, int64_t* out4, void* stream);
+
 /* ------------------------------------------------------------- CSR x dense SpMM
  * Y[i, c] = sum_j values[j] * X[colind[j], c],  c in [0, k)
  * No reference op: replaces the emitted loop-nest kernel of
@@ -165,6 +176,24 @@ int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz,
  * fill rowptr only. */
 int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,
                              int64_t* rowptr, int32_t* colind, double* values, void* stream);
+
+/* ------------------------------------------------------- generated kernels
+ * The reference turns every kokkos.{range,thread,team}_parallel nest into a
+ * Kokkos parallel_for / parallel_reduce lambda (emitter.py:596-780) compiled
+ * ahead of time.  Nests with no hand-written kernel above are emitted as CUDA
+ * C++ by the executor (paper_2509_25605_b200/cudagen.py: team -> block, thread
+ * -> group of vector_length lanes, vector -> lane) and compiled here for
+ * sm_100a with NVRTC (--fmad=false: per-op rounding, exact against the
+ * reference).  Kernels are cached per (device, source); the handle stays
+ * valid for the life of the process.  A generated kernel takes ONE by-value
+ * struct parameter of `params_bytes` bytes. */
+int lapis_b200_jit_available(void);
+int lapis_b200_jit_compile(const char* source, const char* kernel_name, void** out_kernel);
+int lapis_b200_jit_launch(void* kernel, int64_t grid_x, int block_x, int smem_bytes,
+                          const void* params, int64_t params_bytes, void* stream);
+int lapis_b200_jit_cache_size(void);
+/* Compile without loading (no device needed); cubin size in *cubin_bytes. */
+int lapis_b200_jit_check(const char* source, const char* kernel_name, int64_t* cubin_bytes);
 
 #ifdef __cplusplus
 }

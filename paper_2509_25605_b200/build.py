@@ -56,7 +56,7 @@ def build(force: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(_compile, srcs))
     if force or _stale(SO, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(SO), *map(str, objs), "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(SO), *map(str, objs), "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -16,6 +16,42 @@ ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = Path(__file__).resolve().parent / "golden"
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+# the reference package (the caller of the drop-in runtime): pip-installed into
+# baseline/_ref by __graft_entry__.build(); travels to the GPU box
+REF_PKG = ROOT / "baseline" / "_ref"
+if REF_PKG.exists() and str(REF_PKG) not in sys.path:
+    sys.path.append(str(REF_PKG))
+RUN_GOLDEN = GOLDEN / "run"
+
+
+def run_cases() -> list[str]:
+    """<program>.<seed> ids of tests/golden/run (make_run_golden.py)."""
+    return sorted(p.name[:-4] for p in RUN_GOLDEN.glob("*.npz"))
+
+
+def load_run_case(case: str) -> dict:
+    import json as _json
+    name, _ = case.rsplit(".", 1)
+    with np.load(RUN_GOLDEN / f"{case}.npz") as z:
+        d = {k: z[k] for k in z.files}
+    import re as _re
+
+    def seq(prefix):
+        n = sum(1 for k in d if _re.fullmatch(prefix + r"\d+", k))
+        return [d[f"{prefix}{i}"] for i in range(n)]
+    return {
+        "name": name,
+        "entry": str(d["entry"]),
+        "inputs": seq("in"),
+        "outputs": seq("out"),
+        "orig_outputs": seq("orig"),
+        "trace": str(d["trace"]), "eager_trace": str(d["eager_trace"]),
+        "orig_trace": str(d["orig_trace"]),
+        "counters": _json.loads(str(d["counters"])),
+        "orig_counters": _json.loads(str(d["orig_counters"])),
+        "lowered": (RUN_GOLDEN / f"{name}.lowered.mlir").read_text(),
+        "orig": (RUN_GOLDEN / f"{name}.orig.mlir").read_text(),
+    }
 
 
 def pytest_configure(config):
