@@ -167,8 +167,10 @@ class _Ctx:
 class NestGen:
     """Generates one kernel (plus an ordered-fold kernel for host results)."""
 
-    def __init__(self, top, name: str, vl: int = 1, ts: int | None = None, path_of=None):
+    def __init__(self, top, name: str, vl: int = 1, ts: int | None = None, path_of=None,
+                 count_loads=()):
         self.top = top
+        self.count_loads = set(count_loads)
         self.k = Kernel(name=name)
         self.vl = max(1, min(32, 1 << int(math.log2(max(1, vl)))))
         self.path_of = path_of or (lambda op: op.name)
@@ -415,8 +417,11 @@ class NestGen:
         flat = " + ".join(f"(long long)({i}) * {s}" for i, s in zip(idx, st)) or "0"
         return ok, flat
 
-    def emit_load(self, op) -> None:
+    def emit_load(self, op, ctx: "_Ctx") -> None:
         view = op.operands[0]
+        if view in self.count_loads:
+            # a relaxed-stale read: the interpreter records one event per load
+            self.emit(f"if ({ctx.canon}) {self.counter('stale', op)}++;")
         r = op.results[0]
         kind = _kind(r)
         base = self.memref(view)[0]
@@ -485,7 +490,7 @@ class NestGen:
         if self.emit_arith(op):
             return
         if name == "memref.load":
-            self.emit_load(op)
+            self.emit_load(op, ctx)
         elif name == "memref.store":
             self.emit_store(op, ctx)
         elif name == "memref.dim":
@@ -856,9 +861,10 @@ class NestGen:
         return "\n".join(lines_head + self.lines + ["}"])
 
 
-def generate(top, name: str, vl: int = 1, ts: int | None = None) -> Kernel:
-    """CUDA source + parameter layout for one top-level nest."""
-    return NestGen(top, name, vl=vl, ts=ts).generate()
+def generate(top, name: str, vl: int = 1, ts: int | None = None, count_loads=()) -> Kernel:
+    """CUDA source + parameter layout for one top-level nest.  Loads from the
+    memref values in ``count_loads`` are counted (category "stale")."""
+    return NestGen(top, name, vl=vl, ts=ts, count_loads=count_loads).generate()
 
 
 # --------------------------------------------------------------- library ops

@@ -439,7 +439,7 @@ class _Machine:
         for counted, dev in self._pending_counts:
             vals = dev.cpu().tolist()
             for (cat, op), n in zip(counted, vals):
-                if n:
+                if n and cat != "stale":
                     key = self.path(op)
                     self.counters[cat][key] = self.counters[cat].get(key, 0) + int(n)
         self._pending_counts.clear()
@@ -556,14 +556,26 @@ class _Machine:
         try:
             reads, writes, first_load = self.kernel_roots(op, env)
             eager_copy = self.eager and space == "device" and prev == "host"
+            stale = []
             if self.config.has_separate_device_memory and not self.eager:
                 for r in reads:
                     if r.space != "dualview":
                         continue
                     if space == "device" and r.modified_host:
-                        self._stale(r, "device", first_load[id(r)])
+                        stale.append((r, "device"))
                     elif space == "host" and r.modified_device:
-                        self._stale(r, "host", first_load[id(r)])
+                        stale.append((r, "host"))
+            if stale and self.config.strict_stale_checking:
+                r, sp = stale[0]
+                self._stale(r, sp, first_load[id(r)])
+            if stale:
+                # relaxed checking: the kernel reads the stale copy and the
+                # trace gets one StaleAccess per executed load of it
+                self.generated(op, env, stale_roots=stale)
+                self.kernel_log.append((self.path(op), "generated"))
+                for w in writes:
+                    self.after_device_write(w)
+                return
             if eager_copy and self.config.has_separate_device_memory:
                 touched = {id(r): r for r in reads}
                 for w in writes:
@@ -597,7 +609,7 @@ class _Machine:
     # -- generated kernels
     _gen_cache: dict = {}
 
-    def generated(self, op, env) -> None:
+    def generated(self, op, env, stale_roots=()) -> None:
         vl, ts = 1, None
         if op.name in ("kokkos.team_parallel", "kokkos.thread_parallel"):
             tsv, vlv = parallel_hint_operands(op)
@@ -605,15 +617,20 @@ class _Machine:
                 vl = int(env[vlv])
             if tsv is not None:
                 ts = int(env[tsv])
-        key = (id(op), vl, ts)
+        stale_ids = {id(r) for r, _ in stale_roots}
+        counted = tuple(v for v in _free_memrefs(op)
+                        if isinstance(env.get(v), View) and id(env[v].root) in stale_ids)
+        key = (id(op), vl, ts, tuple(id(v) for v in counted))
         kern = _Machine._gen_cache.get(key)
         if kern is None or kern[0] is not op:
             try:
                 name = f"lapis_gen_{len(_Machine._gen_cache)}"
                 if op.name in cudagen.LIBRARY_OPS:
+                    if counted:
+                        raise cudagen.GenError("relaxed stale reads inside a library op", op)
                     k = cudagen.generate_library(op, name)
                 else:
-                    k = cudagen.generate(op, name, vl=vl, ts=ts)
+                    k = cudagen.generate(op, name, vl=vl, ts=ts, count_loads=counted)
             except cudagen.GenError as e:
                 raise InterpError(f"no B200 kernel for this nest: {e}",
                                   self.path(e.op if e.op is not None else op)) from None
@@ -622,7 +639,17 @@ class _Machine:
             kern = (op, k, handle, fold)
             _Machine._gen_cache[key] = kern
         _, k, handle, fold = kern
-        self._launch_generated(op, env, k, handle, fold)
+        counts = self._launch_generated(op, env, k, handle, fold)
+        if counted:
+            # the events must sit at this point of the trace: read the counts now
+            self._sync_stream()
+            vals = counts.cpu().tolist()
+            space = dict((id(r), sp) for r, sp in stale_roots)
+            for (cat, lop), c in zip(k.counted, vals):
+                if cat == "stale" and c:
+                    root = env[lop.operands[0]].root
+                    self.trace.extend([TransferEvent("StaleAccess", root.name, space=space[id(root)],
+                                                     path=self.path(lop))] * int(c))
 
     def _launch_generated(self, op, env, k, handle, fold) -> None:
         launch_id = len(self._err_ops)
@@ -695,6 +722,7 @@ class _Machine:
                 vals = [env[init] for (_, _, _, init) in k.top_reduce]
             for r, (kind, _, _, _), v in zip(op.results, k.top_reduce, vals):
                 env[r] = _coerce(v, kind)
+        return counts
 
     def _range_total(self, op, env) -> int:
         if op.name == "scf.parallel":
@@ -711,6 +739,23 @@ class _Machine:
         for v in op.operands[:dims]:
             total *= max(int(env[v]), 0)
         return total
+
+
+def _free_memrefs(op) -> list:
+    """Memref values a nest reads that are defined outside it."""
+    inside = set()
+    for o in walk(op):
+        inside.update(id(r) for r in o.results)
+        for reg in o.regions:
+            inside.update(id(a) for a in reg.args)
+    out, seen = [], set()
+    for o in walk(op):
+        if o.name == "memref.load":
+            v = o.operands[0]
+            if id(v) not in inside and id(v) not in seen:
+                seen.add(id(v))
+                out.append(v)
+    return out
 
 
 def _library_checks(m: _Machine, op, env) -> None:
