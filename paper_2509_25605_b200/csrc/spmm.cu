@@ -21,6 +21,7 @@
 // SMs without atomics.
 #include "common.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace lapis_b200 {
@@ -170,6 +171,143 @@ spmm_group_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
   }
 }
 
+// ------------------------------------------------------ kernel 1 (batched)
+// A warp owns a batch of 32 consecutive rows.  Lane l holds rowptr[r0 + l],
+// so the row structure of the batch costs one coalesced load; colind/values
+// are read 32 entries at a time (coalesced, the next chunk prefetched while the
+// current one is consumed) and broadcast by shuffles; X-row gathers are issued
+// U entries ahead ACROSS row boundaries, so the memory pipeline never waits on
+// a per-row dependency chain (rowptr -> colind -> X) — the limiter of the
+// one-row-per-warp kernel on short power-law rows (median 5 entries).  Each
+// lane owns CPL consecutive dense columns; every column is still summed in
+// ascending entry order with non-contracted mul / add (bit-identical).  A
+// batch holding a row longer than SPLIT walks its rows one by one and leaves
+// the long rows to kernels 2-3.
+template <class T, int CPL>
+struct XVec;
+template <> struct XVec<double, 1> { using V = double; };
+template <> struct XVec<double, 2> { using V = longlong2; };
+template <> struct XVec<double, 4> { using V = longlong4; };
+template <> struct XVec<float, 1> { using V = float; };
+template <> struct XVec<float, 2> { using V = int2; };
+template <> struct XVec<float, 4> { using V = int4; };
+template <> struct XVec<long long, 1> { using V = long long; };
+template <> struct XVec<long long, 2> { using V = longlong2; };
+template <> struct XVec<long long, 4> { using V = longlong4; };
+template <> struct XVec<int, 1> { using V = int; };
+template <> struct XVec<int, 2> { using V = int2; };
+template <> struct XVec<int, 4> { using V = int4; };
+
+template <class T, int CPL>
+__device__ __forceinline__ void ldx_row(const T* p, T (&v)[CPL]) {
+  using V = typename XVec<T, CPL>::V;
+  const V w = *reinterpret_cast<const V*>(p);
+  memcpy(&v[0], &w, sizeof(V));
+}
+template <class T, int CPL>
+__device__ __forceinline__ void sty_row(T* p, const T (&v)[CPL]) {
+  using V = typename XVec<T, CPL>::V;
+  V w;
+  memcpy(&w, &v[0], sizeof(V));
+  *reinterpret_cast<V*>(p) = w;
+}
+
+template <class T, class RP, class CI, int CPL, int U>
+__global__ void __launch_bounds__(256, 4)
+spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+                  const CI* __restrict__ colind, const T* __restrict__ values,
+                  const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nbatch = (nrows + 31) >> 5;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t bt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; bt < nbatch; bt += wstride) {
+    const int64_t r0 = bt << 5;
+    const int nr = (int)((nrows - r0) < 32 ? (nrows - r0) : 32);
+    const int64_t rp_l = (int64_t)rowptr[r0 + (lane < nr ? lane : nr)];
+    const int64_t rp_end = (int64_t)rowptr[r0 + nr];   // one broadcast load
+    // row lengths (monotone rowptr is validated by the executor)
+    const int64_t dn = __shfl_down_sync(0xffffffffu, rp_l, 1);
+    const int64_t nxt_l = (lane + 1 < nr) ? dn : rp_end;
+    const bool has_long = __any_sync(0xffffffffu, lane < nr && (nxt_l - rp_l) > SPLIT);
+    for (int64_t c0 = (int64_t)lane * CPL; c0 - (int64_t)lane * CPL < k; c0 += 32 * CPL) {
+      if (!has_long) {
+        const int64_t jb = __shfl_sync(0xffffffffu, rp_l, 0);
+        int cur = 0;
+        int64_t nxt = __shfl_sync(0xffffffffu, rp_l, nr > 1 ? 1 : nr);
+        if (nr == 1) nxt = rp_end;
+        T acc[CPL];
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
+        int64_t my_col = 0;
+        T my_val = T(0);
+        if (jb + lane < rp_end) { my_col = (int64_t)colind[jb + lane]; my_val = values[jb + lane]; }
+        for (int64_t j0 = jb; j0 < rp_end; j0 += 32) {
+          const int cnt = (int)((rp_end - j0) < 32 ? (rp_end - j0) : 32);
+          // prefetch the next chunk's structure
+          int64_t nx_col = 0;
+          T nx_val = T(0);
+          if (j0 + 32 + lane < rp_end) { nx_col = (int64_t)colind[j0 + 32 + lane]; nx_val = values[j0 + 32 + lane]; }
+          for (int t0 = 0; t0 < cnt; t0 += U) {
+            T xv[U][CPL];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int64_t c = __shfl_sync(0xffffffffu, my_col, (t0 + u) & 31);
+              if (t0 + u < cnt) {
+                ldx_row<T, CPL>(X + c * ldx + c0, xv[u]);
+              } else {
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) xv[u][q] = T(0);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const T v = __shfl_sync(0xffffffffu, my_val, (t0 + u) & 31);
+              if (t0 + u < cnt) {
+                const int64_t j = j0 + t0 + u;
+                while (j == nxt) {  // rows that end here (empty rows included)
+                  sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
+#pragma unroll
+                  for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
+                  ++cur;
+                  nxt = (cur + 1 < nr) ? __shfl_sync(0xffffffffu, rp_l, (cur + 1) & 31) : rp_end;
+                }
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v, xv[u][q]));
+              }
+            }
+          }
+          my_col = nx_col;
+          my_val = nx_val;
+        }
+        for (; cur < nr; ++cur) {  // the last rows (and trailing empty rows)
+          sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
+        }
+      } else {
+        // slow path: row by row, long rows skipped (kernels 2-3)
+        for (int r = 0; r < nr; ++r) {
+          const int64_t b = __shfl_sync(0xffffffffu, rp_l, r);
+          int64_t e = (r + 1 < nr) ? __shfl_sync(0xffffffffu, rp_l, (r + 1) & 31) : rp_end;
+          if (e < b) e = b;
+          if (e - b > SPLIT) continue;
+          T acc[CPL];
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
+          for (int64_t j = b; j < e; ++j) {
+            const T v = values[j];
+            T xv[CPL];
+            ldx_row<T, CPL>(X + (int64_t)colind[j] * ldx + c0, xv);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v, xv[q]));
+          }
+          sty_row<T, CPL>(Y + (r0 + r) * ldy + c0, acc);
+        }
+      }
+    }
+  }
+}
+
 // --------------------------------------------------------------- kernel 2
 template <class RP>
 __device__ __forceinline__ int64_t first_row_ending_after(int64_t nrows, const RP* rowptr,
@@ -221,6 +359,112 @@ spmm_seq_long_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
         for (int jj = 0; jj < n; ++jj) acc = Arith<T>::add(acc, stage[jj][threadIdx.x]);
     }
     if (threadIdx.x < kc) Y[r * ldy + c0 + threadIdx.x] = acc;
+  }
+}
+
+// Pipelined version (the one launched): warps 0-1 fold, one thread per dense
+// column, in ascending entry order; warps 2-7 stream the row's entries into a
+// PIPE_NS-stage shared-memory ring with cp.async (values + the X-row slices,
+// 8-byte copies), their colind loads running one stage further ahead, so the
+// fold never waits on a gather and the longest row costs ~its sequential add
+// chain instead of one gather latency per 32 entries.
+constexpr int PIPE_NS = 6, PIPE_SEQ = 128, PIPE_KC = 64, PIPE_LOADERS = 6;
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+template <class RP, class CI>
+__global__ void __launch_bounds__(256, 1)
+spmm_seq_long_pipe_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+                          const CI* __restrict__ colind, const float* __restrict__ values,
+                          const float* __restrict__ X, int64_t ldx, float* __restrict__ Y,
+                          int64_t ldy) {
+  constexpr int CPW = PIPE_SEQ / PIPE_LOADERS + 1;  // entries per loader warp per stage (22)
+  extern __shared__ __align__(16) unsigned char pipe_smem[];
+  float* xs = reinterpret_cast<float*>(pipe_smem);            // [NS][SEQ][KC]
+  float* vs = xs + PIPE_NS * PIPE_SEQ * PIPE_KC;               // [NS][SEQ]
+  const int64_t q = blockIdx.x;
+  const int64_t base = (int64_t)rowptr[0];
+  const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
+  const int64_t r = first_row_ending_after(nrows, rowptr, hi - 1);
+  if (r >= nrows) return;
+  const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
+  if (b < lo || b >= hi || e - b <= SPLIT) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool loader = warp >= 2;
+  const int lw = warp - 2;
+  const int64_t nst = (e - b + PIPE_SEQ - 1) / PIPE_SEQ;
+  for (int64_t c0 = 0; c0 < k; c0 += PIPE_KC) {
+    const int kc = (int)((k - c0) < PIPE_KC ? (k - c0) : PIPE_KC);
+    const bool pairs = (kc % 2 == 0) && (ldx % 2 == 0) && ((uintptr_t)X % 8 == 0);
+    int64_t cols[CPW];  // colind of the loader's entries of the NEXT stage to issue
+    auto load_cols = [&](int64_t s) {
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) {
+        const int jj = lw + PIPE_LOADERS * u;
+        const int64_t j = b + s * PIPE_SEQ + jj;
+        cols[u] = (s < nst && jj < PIPE_SEQ && j < e) ? (int64_t)colind[j] : 0;
+      }
+    };
+    auto issue = [&](int64_t s) {
+      if (s < nst) {
+        const int slot = (int)(s % PIPE_NS);
+        const int64_t j0 = b + s * PIPE_SEQ;
+        const int n = (int)((e - j0) < PIPE_SEQ ? (e - j0) : PIPE_SEQ);
+        const int lt = threadIdx.x - 64;
+        if (lt < n) cp_async4(&vs[slot * PIPE_SEQ + lt], values + j0 + lt);
+        if (lt + 192 < n) cp_async4(&vs[slot * PIPE_SEQ + lt + 192], values + j0 + lt + 192);
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+          const int jj = lw + PIPE_LOADERS * u;
+          if (jj < n) {
+            const float* src = X + cols[u] * ldx + c0;
+            float* dst = &xs[(slot * PIPE_SEQ + jj) * PIPE_KC];
+            if (pairs) {
+              if (2 * lane < kc) cp_async8(dst + 2 * lane, src + 2 * lane);
+            } else {
+              for (int cc = lane; cc < kc; cc += 32) cp_async4(dst + cc, src + cc);
+            }
+          }
+        }
+      }
+      cp_commit();  // one group per stage, possibly empty: uniform wait counts
+    };
+    if (loader) {
+      for (int s = 0; s < PIPE_NS - 1; ++s) {
+        load_cols(s);
+        issue(s);
+      }
+      load_cols(PIPE_NS - 1);
+    }
+    float acc = 0.0f;
+    for (int64_t s = 0; s < nst; ++s) {
+      if (loader) cp_wait<PIPE_NS - 2>();  // this thread's copies of stage s landed
+      __syncthreads();                      // everyone's copies of stage s visible; slot s-1 free
+      if (loader) {
+        issue(s + PIPE_NS - 1);             // into slot (s-1) % NS
+        load_cols(s + PIPE_NS);
+      } else if ((int)threadIdx.x < kc) {
+        const int slot = (int)(s % PIPE_NS);
+        const int64_t j0 = b + s * PIPE_SEQ;
+        const int n = (int)((e - j0) < PIPE_SEQ ? (e - j0) : PIPE_SEQ);
+        const float* xr = &xs[slot * PIPE_SEQ * PIPE_KC + threadIdx.x];
+        const float* vr = &vs[slot * PIPE_SEQ];
+        for (int jj = 0; jj < n; ++jj) acc = __fadd_rn(acc, __fmul_rn(vr[jj], xr[jj * PIPE_KC]));
+      }
+    }
+    if (loader) cp_wait<0>();
+    __syncthreads();  // the ring is reused by the next column block
+    if ((int)threadIdx.x < kc) Y[r * ldy + c0 + threadIdx.x] = acc;
   }
 }
 
@@ -288,6 +532,16 @@ __global__ void spmm_combine_kernel(int64_t k, const RP* __restrict__ rowptr,
 }
 
 // ================================================================ host side
+// LAPIS_B200_SPMM_ROW=1 selects the one-row-per-warp kernel (A/B measurements)
+inline bool spmm_force_row() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LAPIS_B200_SPMM_ROW");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <class T, class RP, class CI>
 struct SpmmOp {
   static int run(int64_t nrows, int64_t nnz, int64_t k, const void* rowptr, const void* colind,
@@ -298,7 +552,20 @@ struct SpmmOp {
     const bool grp = (k < 64) && (k % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
                      ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
     const bool vec = (ldx % 2 == 0) && ((uintptr_t)X % (2 * sizeof(T)) == 0);
-    if (grp) {
+    const int64_t cpl = (k % 128 == 0) ? 4 : (k % 64 == 0) ? 2 : (k % 32 == 0) ? 1 : 0;
+    const bool batch = cpl > 0 && (ldx % cpl == 0) && (ldy % cpl == 0) &&
+                       ((uintptr_t)X % (cpl * sizeof(T)) == 0) &&
+                       ((uintptr_t)Y % (cpl * sizeof(T)) == 0) && !spmm_force_row();
+    if (batch) {
+      int64_t gblocks = ((nrows + 31) / 32 + 7) / 8;
+      const int64_t cap = (int64_t)num_sms() * 8;
+      if (gblocks > cap) gblocks = cap;
+      if (gblocks < 1) gblocks = 1;
+#define LB_BAT(CC) spmm_batch_kernel<T, RP, CI, CC, 8><<<(unsigned)gblocks, 256, 0, st>>>( \
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy)
+      if (cpl == 4) LB_BAT(4); else if (cpl == 2) LB_BAT(2); else LB_BAT(1);
+#undef LB_BAT
+    } else if (grp) {
       const int64_t lanes_per_row = k >= 64 ? 16 : (k >= 32 ? 8 : (k >= 16 ? 4 : (k >= 8 ? 2 : 1)));
       int64_t gblocks = (nrows * lanes_per_row + 255) / 256;
       const int64_t cap = (int64_t)num_sms() * 8;
@@ -326,10 +593,15 @@ struct SpmmOp {
     if (nnz <= SPLIT) return LAPIS_B200_OK;  // no row can be long
     const int64_t nchunks = (nnz + SPLIT - 1) / SPLIT;
     if constexpr (std::is_same<T, float>::value) {
-      spmm_seq_long_kernel<T, RP, CI><<<(unsigned)nchunks, SPMM_WARPS * 32, 0, st>>>(
-          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
-          (T*)Y, ldy);
-      return check_launch("spmm_seq_long_kernel");
+      constexpr size_t pipe_smem =
+          (size_t)PIPE_NS * PIPE_SEQ * (PIPE_KC + 1) * sizeof(float);
+      LB_TRY(check_cuda(cudaFuncSetAttribute(spmm_seq_long_pipe_kernel<RP, CI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pipe_smem), "smem attr (seq pipe)"));
+      spmm_seq_long_pipe_kernel<RP, CI><<<(unsigned)nchunks, 256, pipe_smem, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const float*)values, (const float*)X,
+          ldx, (float*)Y, ldy);
+      return check_launch("spmm_seq_long_pipe_kernel");
     }
     T* part = nullptr;
     int64_t* slot_row = nullptr;
