@@ -5,20 +5,15 @@
 // with the per-(i, c) order of interp.py:798-812: j ascending, mul and add
 // each rounded.
 //
-// Kernel 1 (spmm_group_kernel; spmm_row_kernel for unaligned operands): G
-//   lanes per row, lanes across the dense columns (16-byte gathers of each X
-//   row slice), the j loop walked in ascending order with non-contracted
-//   mul/add -> bit-identical to the reference for every row of <= SPLIT
-//   entries.  Rows longer than SPLIT are left to kernels 2-3.
-// Kernel 2 (spmm_chunk_kernel): the nonzero stream is cut into fixed chunks of
-//   SPLIT entries; for each long row overlapping chunk q a CTA computes the
-//   partial row over the overlap (8 warps on contiguous sub-ranges, folded in
-//   warp order) into slot (q, 0 = row began earlier | 1 = row begins here).
-// Kernel 3 (spmm_combine_kernel): for each long row, sums its chunk partials
-//   in chunk order.  Deterministic (fixed association), parity by tolerance.
-//   fp32 long rows take spmm_seq_long_kernel instead (exact reference order).
-// This splits power-law hub rows (config 3: max 117,686 entries) over many
-// SMs without atomics.
+// Kernel 1 (spmm_batch_kernel when k is a multiple of 32; spmm_group_kernel /
+//   spmm_row_kernel otherwise): every row of <= SPLIT entries, each dense
+//   column summed in ascending entry order with non-contracted mul/add ->
+//   bit-identical to the reference.
+// Long rows (> SPLIT entries; power-law hubs, config 3: 117,686 entries) are
+//   listed by one pass over rowptr, then folded in exact order (fp32,
+//   spmm_seq_long_pipe_kernel) or cut into SPLIT-entry chunks whose partials a
+//   persistent CTA pool computes and a combine kernel adds in chunk order
+//   (other types; deterministic, no atomics on values).
 #include "common.cuh"
 
 #include <cstdlib>
@@ -228,25 +223,32 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
     // row lengths (monotone rowptr is validated by the executor)
     const int64_t dn = __shfl_down_sync(0xffffffffu, rp_l, 1);
     const int64_t nxt_l = (lane + 1 < nr) ? dn : rp_end;
-    const bool has_long = __any_sync(0xffffffffu, lane < nr && (nxt_l - rp_l) > SPLIT);
+    // rows longer than SPLIT are left to the long-row kernels: the batch is
+    // walked as maximal runs of short rows [ra, rb), each run one contiguous
+    // entry range
+    const unsigned long_mask = __ballot_sync(0xffffffffu, lane < nr && (nxt_l - rp_l) > SPLIT);
     for (int64_t c0 = (int64_t)lane * CPL; c0 - (int64_t)lane * CPL < k; c0 += 32 * CPL) {
-      if (!has_long) {
-        const int64_t jb = __shfl_sync(0xffffffffu, rp_l, 0);
-        int cur = 0;
-        int64_t nxt = __shfl_sync(0xffffffffu, rp_l, nr > 1 ? 1 : nr);
-        if (nr == 1) nxt = rp_end;
+      int ra = 0;
+      while (ra < nr) {
+        if ((long_mask >> ra) & 1u) { ++ra; continue; }
+        const unsigned above = long_mask & ~((2u << ra) - 1u);   // long rows after ra
+        const int rb = above ? (__ffs(above) - 1) : nr;
+        const int64_t jb = __shfl_sync(0xffffffffu, rp_l, ra);
+        const int64_t je = rb < nr ? __shfl_sync(0xffffffffu, rp_l, rb & 31) : rp_end;
+        int cur = ra;
+        int64_t nxt = (cur + 1 < nr) ? __shfl_sync(0xffffffffu, rp_l, (cur + 1) & 31) : rp_end;
         T acc[CPL];
 #pragma unroll
         for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
         int64_t my_col = 0;
         T my_val = T(0);
-        if (jb + lane < rp_end) { my_col = (int64_t)colind[jb + lane]; my_val = values[jb + lane]; }
-        for (int64_t j0 = jb; j0 < rp_end; j0 += 32) {
-          const int cnt = (int)((rp_end - j0) < 32 ? (rp_end - j0) : 32);
+        if (jb + lane < je) { my_col = (int64_t)colind[jb + lane]; my_val = values[jb + lane]; }
+        for (int64_t j0 = jb; j0 < je; j0 += 32) {
+          const int cnt = (int)((je - j0) < 32 ? (je - j0) : 32);
           // prefetch the next chunk's structure
           int64_t nx_col = 0;
           T nx_val = T(0);
-          if (j0 + 32 + lane < rp_end) { nx_col = (int64_t)colind[j0 + 32 + lane]; nx_val = values[j0 + 32 + lane]; }
+          if (j0 + 32 + lane < je) { nx_col = (int64_t)colind[j0 + 32 + lane]; nx_val = values[j0 + 32 + lane]; }
           for (int t0 = 0; t0 < cnt; t0 += U) {
             T xv[U][CPL];
 #pragma unroll
@@ -279,86 +281,78 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
           my_col = nx_col;
           my_val = nx_val;
         }
-        for (; cur < nr; ++cur) {  // the last rows (and trailing empty rows)
+        for (; cur < rb; ++cur) {  // the run's last rows (and trailing empty rows)
           sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
 #pragma unroll
           for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
         }
-      } else {
-        // slow path: row by row, long rows skipped (kernels 2-3)
-        for (int r = 0; r < nr; ++r) {
-          const int64_t b = __shfl_sync(0xffffffffu, rp_l, r);
-          int64_t e = (r + 1 < nr) ? __shfl_sync(0xffffffffu, rp_l, (r + 1) & 31) : rp_end;
-          if (e < b) e = b;
-          if (e - b > SPLIT) continue;
-          T acc[CPL];
-#pragma unroll
-          for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
-          for (int64_t j = b; j < e; ++j) {
-            const T v = values[j];
-            T xv[CPL];
-            ldx_row<T, CPL>(X + (int64_t)colind[j] * ldx + c0, xv);
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v, xv[q]));
-          }
-          sty_row<T, CPL>(Y + (r0 + r) * ldy + c0, acc);
-        }
+        ra = rb;
       }
     }
   }
 }
 
-// --------------------------------------------------------------- kernel 2
+// --------------------------------------------------------------- long rows
+// Rows longer than SPLIT entries (power-law hubs: config 3 has rows of
+// 117,686 entries) are listed once by a streaming pass over rowptr, then
+//  * fp32: each listed row is folded in the reference's exact order by the
+//    pipelined kernel below (a reassociated fp32 sum of thousands of terms can
+//    move by more than the 1e-5 contract);
+//  * other types: each row is cut into SPLIT-entry chunks (work items built on
+//    the device), a persistent CTA pool folds each chunk (8 warps on
+//    contiguous sub-ranges, combined in warp order) into a partial, and the
+//    partials of a row are added in chunk order.  Deterministic (fixed
+//    association); exact for integers, within tolerance for fp64.
+struct LongRows {
+  int64_t* count;      // [1] listed rows
+  int64_t* rows;       // [cap] row ids
+  int64_t* total;      // [1] work items
+  int64_t* work_row;   // [wcap] row of item
+  int64_t* work_beg;   // [wcap] first entry of item
+  int64_t* first;      // [cap] first item of listed row i
+};
+
 template <class RP>
-__device__ __forceinline__ int64_t first_row_ending_after(int64_t nrows, const RP* rowptr,
-                                                          int64_t value) {
-  // smallest r in [0, nrows) with rowptr[r+1] > value (nrows if none)
-  int64_t lo = 0, hi = nrows;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if ((int64_t)rowptr[mid + 1] > value) hi = mid; else lo = mid + 1;
+__global__ void long_rows_list_kernel(int64_t nrows, const RP* __restrict__ rowptr, LongRows lr) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = (int64_t)rowptr[r + 1] - (int64_t)rowptr[r];
+    if (len > SPLIT) lr.rows[atomicAdd(reinterpret_cast<unsigned long long*>(lr.count), 1ull)] = r;
   }
-  return lo;
 }
 
-// fp32 long rows instead follow the reference's exact sequential order (a
-// reassociated fp32 sum of thousands of terms can move by more than the 1e-5
-// contract): the CTA of the chunk where such a row BEGINS walks the whole row,
-// one thread per dense column, and writes Y directly.
-template <class T, class RP, class CI>
-__global__ void __launch_bounds__(SPMM_WARPS * 32)
-spmm_seq_long_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
-                     const CI* __restrict__ colind, const T* __restrict__ values,
-                     const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
-  // products of SEQ_CH entries x KC columns staged per round: every thread gathers
-  // (all loads of a round in flight at once), then one thread per column folds
-  // the round in ascending entry order
-  constexpr int SEQ_CH = 32, KC = 64;
-  __shared__ T stage[SEQ_CH][KC];
-  const int64_t q = blockIdx.x;
-  const int64_t base = (int64_t)rowptr[0];
-  const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
-  const int64_t r = first_row_ending_after(nrows, rowptr, hi - 1);
-  if (r >= nrows) return;
-  const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
-  if (b < lo || b >= hi || e - b <= SPLIT) return;
-  for (int64_t c0 = 0; c0 < k; c0 += KC) {
-    const int kc = (int)((k - c0) < KC ? (k - c0) : KC);
-    T acc = Arith<T>::zero();
-    for (int64_t j0 = b; j0 < e; j0 += SEQ_CH) {
-      const int n = (int)((e - j0) < SEQ_CH ? (e - j0) : SEQ_CH);
-      __syncthreads();
-      for (int t = threadIdx.x; t < SEQ_CH * KC; t += blockDim.x) {
-        const int jj = t / KC, cc = t % KC;
-        if (jj < n && cc < kc)
-          stage[jj][cc] = Arith<T>::mul(values[j0 + jj],
-                                        __ldg(X + (int64_t)colind[j0 + jj] * ldx + c0 + cc));
-      }
-      __syncthreads();
-      if (threadIdx.x < kc)
-        for (int jj = 0; jj < n; ++jj) acc = Arith<T>::add(acc, stage[jj][threadIdx.x]);
+// one CTA: each thread owns a contiguous slice of the listed rows; a block
+// scan of the slices' chunk counts gives every row its first work item
+template <class RP>
+__global__ void __launch_bounds__(1024) long_rows_work_kernel(const RP* __restrict__ rowptr,
+                                                              LongRows lr) {
+  __shared__ int64_t scan[1024];
+  const int64_t n = *lr.count;
+  const int t = threadIdx.x;
+  const int64_t i0 = n * t / 1024, i1 = n * (t + 1) / 1024;
+  int64_t mine = 0;
+  for (int64_t i = i0; i < i1; ++i) {
+    const int64_t r = lr.rows[i];
+    mine += ((int64_t)rowptr[r + 1] - (int64_t)rowptr[r] + SPLIT - 1) / SPLIT;
+  }
+  scan[t] = mine;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
+    const int64_t v = t >= off ? scan[t - off] : 0;
+    __syncthreads();
+    scan[t] += v;
+    __syncthreads();
+  }
+  int64_t w = scan[t] - mine;
+  if (t == 1023) *lr.total = scan[1023];
+  for (int64_t i = i0; i < i1; ++i) {
+    const int64_t r = lr.rows[i];
+    const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
+    lr.first[i] = w;
+    for (int64_t s = b; s < e; s += SPLIT, ++w) {
+      lr.work_row[w] = r;
+      lr.work_beg[w] = s;
     }
-    if (threadIdx.x < kc) Y[r * ldy + c0 + threadIdx.x] = acc;
   }
 }
 
@@ -384,36 +378,34 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 template <class RP, class CI>
 __global__ void __launch_bounds__(256, 1)
-spmm_seq_long_pipe_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
+spmm_seq_long_pipe_kernel(int64_t k, const RP* __restrict__ rowptr,
                           const CI* __restrict__ colind, const float* __restrict__ values,
                           const float* __restrict__ X, int64_t ldx, float* __restrict__ Y,
-                          int64_t ldy) {
+                          int64_t ldy, const LongRows lr) {
   constexpr int CPW = PIPE_SEQ / PIPE_LOADERS + 1;  // entries per loader warp per stage (22)
   extern __shared__ __align__(16) unsigned char pipe_smem[];
   float* xs = reinterpret_cast<float*>(pipe_smem);            // [NS][SEQ][KC]
   float* vs = xs + PIPE_NS * PIPE_SEQ * PIPE_KC;               // [NS][SEQ]
-  const int64_t q = blockIdx.x;
-  const int64_t base = (int64_t)rowptr[0];
-  const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
-  const int64_t r = first_row_ending_after(nrows, rowptr, hi - 1);
-  if (r >= nrows) return;
-  const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
-  if (b < lo || b >= hi || e - b <= SPLIT) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nlong = *lr.count;
+  for (int64_t li = blockIdx.x; li < nlong; li += gridDim.x) {
+  const int64_t r = lr.rows[li];
+  const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
   const bool loader = warp >= 2;
   const int lw = warp - 2;
   const int64_t nst = (e - b + PIPE_SEQ - 1) / PIPE_SEQ;
   for (int64_t c0 = 0; c0 < k; c0 += PIPE_KC) {
     const int kc = (int)((k - c0) < PIPE_KC ? (k - c0) : PIPE_KC);
     const bool pairs = (kc % 2 == 0) && (ldx % 2 == 0) && ((uintptr_t)X % 8 == 0);
-    int64_t cols[CPW];  // colind of the loader's entries of the NEXT stage to issue
+    // colind of the loader warp's entries of the NEXT stage to issue: lane u
+    // holds entry lw + 6u (one load per lane, issued a stage ahead), the
+    // issuing loop broadcasts it by shuffle
+    int64_t my_col = 0;
     auto load_cols = [&](int64_t s) {
-#pragma unroll
-      for (int u = 0; u < CPW; ++u) {
-        const int jj = lw + PIPE_LOADERS * u;
-        const int64_t j = b + s * PIPE_SEQ + jj;
-        cols[u] = (s < nst && jj < PIPE_SEQ && j < e) ? (int64_t)colind[j] : 0;
-      }
+      const int64_t jb = b + s * PIPE_SEQ;
+      const int64_t lim = (s < nst) ? e - jb : 0;
+      const int jj = lw + PIPE_LOADERS * lane;
+      my_col = (lane < CPW && jj < PIPE_SEQ && jj < lim) ? (int64_t)__ldg(colind + jb + jj) : 0;
     };
     auto issue = [&](int64_t s) {
       if (s < nst) {
@@ -426,8 +418,9 @@ spmm_seq_long_pipe_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowpt
 #pragma unroll
         for (int u = 0; u < CPW; ++u) {
           const int jj = lw + PIPE_LOADERS * u;
+          const int64_t cu = __shfl_sync(0xffffffffu, my_col, u);
           if (jj < n) {
-            const float* src = X + cols[u] * ldx + c0;
+            const float* src = X + cu * ldx + c0;
             float* dst = &xs[(slot * PIPE_SEQ + jj) * PIPE_KC];
             if (pairs) {
               if (2 * lane < kc) cp_async8(dst + 2 * lane, src + 2 * lane);
@@ -459,75 +452,82 @@ spmm_seq_long_pipe_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowpt
         const int n = (int)((e - j0) < PIPE_SEQ ? (e - j0) : PIPE_SEQ);
         const float* xr = &xs[slot * PIPE_SEQ * PIPE_KC + threadIdx.x];
         const float* vr = &vs[slot * PIPE_SEQ];
-        for (int jj = 0; jj < n; ++jj) acc = __fadd_rn(acc, __fmul_rn(vr[jj], xr[jj * PIPE_KC]));
+        int jj = 0;
+        for (; jj + 16 <= n; jj += 16) {  // all 32 shared loads in flight, then the add chain
+          float vv[16], xx[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) { vv[u] = vr[jj + u]; xx[u] = xr[(jj + u) * PIPE_KC]; }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, __fmul_rn(vv[u], xx[u]));
+        }
+        for (; jj < n; ++jj) acc = __fadd_rn(acc, __fmul_rn(vr[jj], xr[jj * PIPE_KC]));
       }
     }
     if (loader) cp_wait<0>();
     __syncthreads();  // the ring is reused by the next column block
     if ((int)threadIdx.x < kc) Y[r * ldy + c0 + threadIdx.x] = acc;
   }
+  }
 }
 
 template <class T, class RP, class CI>
 __global__ void __launch_bounds__(SPMM_WARPS * 32)
-spmm_chunk_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
-                  const CI* __restrict__ colind, const T* __restrict__ values,
-                  const T* __restrict__ X, int64_t ldx, T* __restrict__ part,
-                  int64_t* __restrict__ slot_row) {
+spmm_long_chunk_kernel(int64_t k, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
+                       const T* __restrict__ values, const T* __restrict__ X, int64_t ldx,
+                       T* __restrict__ part, const LongRows lr) {
   extern __shared__ unsigned char smem_raw[];
   T* wpart = reinterpret_cast<T*>(smem_raw);  // [SPMM_WARPS][k]
-  const int64_t q = blockIdx.x;
-  const int64_t base = (int64_t)rowptr[0];
-  const int64_t lo = base + q * SPLIT, hi = lo + SPLIT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // a long row (> SPLIT entries) cannot lie strictly inside one chunk, so only
-  // the first and the last row overlapping [lo, hi) can be long
-  const int64_t r_first = first_row_ending_after(nrows, rowptr, lo);
-  const int64_t r_last = first_row_ending_after(nrows, rowptr, hi - 1);
-  for (int cand = 0; cand < 2; ++cand) {
-    const int64_t r = cand == 0 ? r_first : r_last;
-    if (r >= nrows || (cand == 1 && r_last == r_first)) continue;
-    const int64_t b = (int64_t)rowptr[r];
-    if (b >= hi) continue;
+  const int64_t total = *lr.total;
+  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    const int64_t r = lr.work_row[w];
+    const int64_t s0 = lr.work_beg[w];
     const int64_t e = (int64_t)rowptr[r + 1];
-    if (e - b <= SPLIT) continue;  // short rows belong to kernel 1
-    const int64_t s0 = b > lo ? b : lo, s1 = e < hi ? e : hi;
-    const int slot = (b < lo) ? 0 : 1;
-    // warp w folds the contiguous sub-range [s0 + w*len/W, s0 + (w+1)*len/W)
+    const int64_t s1 = (s0 + SPLIT) < e ? (s0 + SPLIT) : e;
     const int64_t len = s1 - s0;
     const int64_t w0 = s0 + len * warp / SPMM_WARPS, w1 = s0 + len * (warp + 1) / SPMM_WARPS;
     for (int64_t col = lane; col < k; col += 32) {
       T acc = Arith<T>::zero();
-      for (int64_t j = w0; j < w1; ++j)
+      int64_t j = w0;
+      for (; j + 4 <= w1; j += 4) {  // 4 gathers in flight, folded in order
+        T v[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = values[j + u];
+          x[u] = __ldg(X + (int64_t)colind[j + u] * ldx + col);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = Arith<T>::add(acc, Arith<T>::mul(v[u], x[u]));
+      }
+      for (; j < w1; ++j)
         acc = Arith<T>::add(acc, Arith<T>::mul(values[j], __ldg(X + (int64_t)colind[j] * ldx + col)));
       wpart[warp * k + col] = acc;
     }
     __syncthreads();
-    T* dst = part + (q * 2 + slot) * k;
+    T* dst = part + w * k;
     for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
       T acc = Arith<T>::zero();
-      for (int w = 0; w < SPMM_WARPS; ++w) acc = Arith<T>::add(acc, wpart[w * k + col]);
+      for (int ww = 0; ww < SPMM_WARPS; ++ww) acc = Arith<T>::add(acc, wpart[ww * k + col]);
       dst[col] = acc;
     }
-    if (threadIdx.x == 0) slot_row[q * 2 + slot] = r;
     __syncthreads();
   }
 }
 
-// --------------------------------------------------------------- kernel 3
 template <class T, class RP>
-__global__ void spmm_combine_kernel(int64_t k, const RP* __restrict__ rowptr,
-                                    const T* __restrict__ part, const int64_t* __restrict__ slot_row,
-                                    T* __restrict__ Y, int64_t ldy) {
-  const int64_t q = blockIdx.x;
-  const int64_t r = slot_row[q * 2 + 1];
-  if (r < 0) return;
-  const int64_t base = (int64_t)rowptr[0];
-  const int64_t qend = ((int64_t)rowptr[r + 1] - base - 1) / SPLIT;
-  for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
-    T acc = part[(q * 2 + 1) * k + col];
-    for (int64_t qq = q + 1; qq <= qend; ++qq) acc = Arith<T>::add(acc, part[(qq * 2 + 0) * k + col]);
-    Y[r * ldy + col] = acc;
+__global__ void spmm_long_combine_kernel(int64_t k, const RP* __restrict__ rowptr,
+                                         const T* __restrict__ part, T* __restrict__ Y, int64_t ldy,
+                                         const LongRows lr) {
+  const int64_t n = *lr.count;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t r = lr.rows[i];
+    const int64_t w0 = lr.first[i];
+    const int64_t nch = ((int64_t)rowptr[r + 1] - (int64_t)rowptr[r] + SPLIT - 1) / SPLIT;
+    for (int64_t col = threadIdx.x; col < k; col += blockDim.x) {
+      T acc = part[w0 * k + col];
+      for (int64_t c = 1; c < nch; ++c) acc = Arith<T>::add(acc, part[(w0 + c) * k + col]);
+      Y[r * ldy + col] = acc;
+    }
   }
 }
 
@@ -591,46 +591,72 @@ struct SpmmOp {
           (T*)Y, ldy);
     LB_TRY(check_launch("spmm_row_kernel"));
     if (nnz <= SPLIT) return LAPIS_B200_OK;  // no row can be long
-    const int64_t nchunks = (nnz + SPLIT - 1) / SPLIT;
+    // ---- long rows: list them, then fold (fp32 exact) or chunk + combine
+    const int64_t cap = nnz / (SPLIT + 1) + 1;       // rows with > SPLIT entries
+    const int64_t wcap = nnz / SPLIT + cap + 1;       // chunks of those rows
+    int64_t* ws = nullptr;
+    const size_t ws_elems = 2 + 2 * (size_t)cap + 2 * (size_t)wcap;
+    LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, ws_elems * sizeof(int64_t), st), "alloc(long rows)"));
+    LongRows lr;
+    lr.count = ws;
+    lr.total = ws + 1;
+    lr.rows = ws + 2;
+    lr.first = lr.rows + cap;
+    lr.work_row = lr.first + cap;
+    lr.work_beg = lr.work_row + wcap;
+    int rc = check_cuda(cudaMemsetAsync(ws, 0, 2 * sizeof(int64_t), st), "memset(long rows)");
+    const int sms = num_sms();
+    if (rc == LAPIS_B200_OK) {
+      int64_t g = (nrows + 255) / 256;
+      if (g > (int64_t)sms * 8) g = (int64_t)sms * 8;
+      long_rows_list_kernel<RP><<<(unsigned)(g > 0 ? g : 1), 256, 0, st>>>(nrows, (const RP*)rowptr, lr);
+      rc = check_launch("long_rows_list_kernel");
+    }
     if constexpr (std::is_same<T, float>::value) {
-      constexpr size_t pipe_smem =
-          (size_t)PIPE_NS * PIPE_SEQ * (PIPE_KC + 1) * sizeof(float);
-      LB_TRY(check_cuda(cudaFuncSetAttribute(spmm_seq_long_pipe_kernel<RP, CI>,
+      constexpr size_t pipe_smem = (size_t)PIPE_NS * PIPE_SEQ * (PIPE_KC + 1) * sizeof(float);
+      if (rc == LAPIS_B200_OK)
+        rc = check_cuda(cudaFuncSetAttribute(spmm_seq_long_pipe_kernel<RP, CI>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)pipe_smem), "smem attr (seq pipe)"));
-      spmm_seq_long_pipe_kernel<RP, CI><<<(unsigned)nchunks, 256, pipe_smem, st>>>(
-          nrows, k, (const RP*)rowptr, (const CI*)colind, (const float*)values, (const float*)X,
-          ldx, (float*)Y, ldy);
-      return check_launch("spmm_seq_long_pipe_kernel");
+                                             (int)pipe_smem), "smem attr (seq pipe)");
+      if (rc == LAPIS_B200_OK) {
+        const int64_t g = cap < sms ? cap : sms;
+        spmm_seq_long_pipe_kernel<RP, CI><<<(unsigned)g, 256, pipe_smem, st>>>(
+            k, (const RP*)rowptr, (const CI*)colind, (const float*)values, (const float*)X, ldx,
+            (float*)Y, ldy, lr);
+        rc = check_launch("spmm_seq_long_pipe_kernel");
+      }
+      cudaFreeAsync(ws, st);
+      return rc;
+    }
+    if (rc == LAPIS_B200_OK) {
+      long_rows_work_kernel<RP><<<1, 1024, 0, st>>>((const RP*)rowptr, lr);
+      rc = check_launch("long_rows_work_kernel");
     }
     T* part = nullptr;
-    int64_t* slot_row = nullptr;
-    LB_TRY(check_cuda(cudaMallocAsync((void**)&part, nchunks * 2 * k * sizeof(T), st), "alloc(part)"));
-    int rc = check_cuda(cudaMallocAsync((void**)&slot_row, nchunks * 2 * sizeof(int64_t), st),
-                        "alloc(slot_row)");
     if (rc == LAPIS_B200_OK)
-      rc = check_cuda(cudaMemsetAsync(slot_row, 0xff, nchunks * 2 * sizeof(int64_t), st), "memset");
+      rc = check_cuda(cudaMallocAsync((void**)&part, (size_t)wcap * k * sizeof(T), st), "alloc(part)");
     const size_t smem = (size_t)SPMM_WARPS * k * sizeof(T);
     if (rc == LAPIS_B200_OK && smem > 48 * 1024) {
-      rc = check_cuda(cudaFuncSetAttribute(spmm_chunk_kernel<T, RP, CI>,
+      rc = check_cuda(cudaFuncSetAttribute(spmm_long_chunk_kernel<T, RP, CI>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "smem attr");
       if (rc == LAPIS_B200_OK && smem > 200 * 1024)
         rc = fail(LAPIS_B200_ERR_UNSUPPORTED, "spmm: k too large for long-row staging");
     }
     if (rc == LAPIS_B200_OK) {
-      spmm_chunk_kernel<T, RP, CI><<<(unsigned)nchunks, SPMM_WARPS * 32, smem, st>>>(
-          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
-          part, slot_row);
-      rc = check_launch("spmm_chunk_kernel");
+      const int64_t g = wcap < (int64_t)sms * 8 ? wcap : (int64_t)sms * 8;
+      spmm_long_chunk_kernel<T, RP, CI><<<(unsigned)g, SPMM_WARPS * 32, smem, st>>>(
+          k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, part, lr);
+      rc = check_launch("spmm_long_chunk_kernel");
     }
     if (rc == LAPIS_B200_OK) {
-      spmm_combine_kernel<T, RP><<<(unsigned)nchunks, 64, 0, st>>>(k, (const RP*)rowptr, part,
-                                                                  slot_row, (T*)Y, ldy);
-      rc = check_launch("spmm_combine_kernel");
+      const int64_t g = cap < (int64_t)sms * 4 ? cap : (int64_t)sms * 4;
+      spmm_long_combine_kernel<T, RP><<<(unsigned)g, 64, 0, st>>>(k, (const RP*)rowptr, part,
+                                                                 (T*)Y, ldy, lr);
+      rc = check_launch("spmm_long_combine_kernel");
     }
     if (part) cudaFreeAsync(part, st);
-    if (slot_row) cudaFreeAsync(slot_row, st);
+    cudaFreeAsync(ws, st);
     return rc;
   }
 };
