@@ -50,10 +50,16 @@ extern "C" {
 #define LAPIS_B200_MAX 3
 
 /* dense matmul precision modes (lapis_b200_gemm `mode`) */
-#define LAPIS_B200_GEMM_AUTO 0    /* f32 -> TF32X3, f64 -> DMMA, ints -> EXACT */
+#define LAPIS_B200_GEMM_AUTO 0    /* f32 -> TF32X3, f64 -> OZAKI (DMMA beyond its k range),
+                                     ints -> EXACT */
 #define LAPIS_B200_GEMM_TF32X3 1  /* f32: 3xTF32 split on tcgen05 (kind::tf32), TMEM accum */
 #define LAPIS_B200_GEMM_DMMA 2    /* f64: DMMA tensor cores */
 #define LAPIS_B200_GEMM_EXACT 3   /* reference order: sequential k, no FMA -> bit-exact */
+#define LAPIS_B200_GEMM_OZAKI 4   /* f64 / f32: Ozaki digit split on the int8 tensor cores
+                                     (tcgen05 kind::i8; f64 8-9 7-bit digits, f32 3 8-bit
+                                     digits; s32 accumulation).  Every element is certified
+                                     against an a-priori error bound; uncertified results
+                                     are recomputed by DMMA / TF32X3 on the device */
 
 /* ----------------------------------------------------------------- library */
 const char* lapis_b200_last_error(void);

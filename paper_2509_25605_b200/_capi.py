@@ -15,7 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "liblapis_b200.so"
 OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED, ERR_NOMEM = 0, 1, 2, 3, 4
 F32, F64, I32, I64 = 0, 1, 2, 3
 ADD, MUL, MIN, MAX = 0, 1, 2, 3
-GEMM_AUTO, GEMM_TF32X3, GEMM_DMMA, GEMM_EXACT = 0, 1, 2, 3
+GEMM_AUTO, GEMM_TF32X3, GEMM_DMMA, GEMM_EXACT, GEMM_OZAKI = 0, 1, 2, 3, 4
 
 
 class BackendError(RuntimeError):

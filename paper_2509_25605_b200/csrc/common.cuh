@@ -95,6 +95,32 @@ inline void keep_pool_memory() {
   done[dev] = true;
 }
 
+// Device-side launch guard: a fallback kernel launched unconditionally that
+// returns at once unless its flag condition holds (keeps data-dependent
+// fallbacks stream-ordered, no host sync).  mode 0: always run; mode 1: run
+// iff flags[0]; mode 2: run iff !flags[0] && flags[1].
+struct Guard {
+  const int* flags = nullptr;
+  int mode = 0;
+};
+__device__ __forceinline__ bool guard_skip(const Guard& g) {
+  if (g.mode == 0 || !g.flags) return false;
+  if (g.mode == 1) return g.flags[0] == 0;
+  return g.flags[0] != 0 || g.flags[1] == 0;
+}
+
+// GEMM paths shared across translation units (dense.cu dispatches; the Ozaki
+// path launches the others as guarded fallbacks)
+int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+                int64_t sC, cudaStream_t st, Guard guard = Guard());
+int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+              const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+              int64_t sC, cudaStream_t st, Guard guard = Guard());
+int launch_gemm_exact_guarded(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                              const void* B, int64_t ldb, void* C, int64_t ldc, int dtype,
+                              Guard guard, cudaStream_t st);
+
 inline int elem_bytes(int dtype) {
   return (dtype == LAPIS_B200_F64 || dtype == LAPIS_B200_I64) ? 8 : 4;
 }

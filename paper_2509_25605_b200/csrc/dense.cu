@@ -61,7 +61,8 @@ template <class T, bool RELU>
 __global__ void __launch_bounds__(256)
 gemm_exact_kernel(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int64_t lda,
                   const T* __restrict__ B, int64_t ldb, T* __restrict__ C, int64_t ldc,
-                  int64_t strideA, int64_t strideB, int64_t strideC) {
+                  int64_t strideA, int64_t strideB, int64_t strideC, Guard guard) {
+  if (guard_skip(guard)) return;   // fallback launches run only when flagged
   __shared__ T As[EG_TILE][EG_TILE + 1];
   __shared__ T Bs[EG_TILE][EG_TILE + 1];
   A += blockIdx.z * strideA;
@@ -156,13 +157,24 @@ __global__ void relu_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ 
 template <class T, bool RELU = false>
 static int launch_gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
                              int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                             int64_t sA, int64_t sB, int64_t sC, cudaStream_t st) {
+                             int64_t sA, int64_t sB, int64_t sC, cudaStream_t st,
+                             Guard guard = Guard()) {
   dim3 grid((unsigned)((n + EG_TILE - 1) / EG_TILE), (unsigned)((m + EG_TILE - 1) / EG_TILE),
             (unsigned)batch);
   if (grid.y > 65535 || grid.z > 65535) return fail(LAPIS_B200_ERR_ARG, "gemm: grid too large");
   gemm_exact_kernel<T, RELU><<<grid, 256, 0, st>>>(m, n, k, (const T*)A, lda, (const T*)B, ldb,
-                                                   (T*)C, ldc, sA, sB, sC);
+                                                   (T*)C, ldc, sA, sB, sC, guard);
   return check_launch("gemm_exact_kernel");
+}
+
+// The reference-order GEMM behind a device flag (the Ozaki path's fallback for
+// non-finite inputs): launched unconditionally, returns at once unless *guard.
+int launch_gemm_exact_guarded(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                              const void* B, int64_t ldb, void* C, int64_t ldc, int dtype,
+                              Guard guard, cudaStream_t st) {
+  if (dtype == LAPIS_B200_F64)
+    return launch_gemm_exact<double>(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, st, guard);
+  return launch_gemm_exact<float>(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, st, guard);
 }
 
 int gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
@@ -249,13 +261,12 @@ int relu(int64_t n, const void* x, void* y, int dtype, cudaStream_t st) {
 
 namespace lapis_b200 {
 
-// tensor-core paths (gemm_tf32x3.cu, gemm_dmma.cu)
-int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
-                const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-                int64_t sC, cudaStream_t st);
-int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
-              const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-              int64_t sC, cudaStream_t st);
+// tensor-core paths (gemm_tf32x3.cu, gemm_dmma.cu): prototypes in common.cuh
+
+int gemm_ozaki(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+               const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+               int64_t sC, int dtype, int slices, cudaStream_t st);
+int ozaki_slices_for(int dtype, int64_t k);
 
 int gemm_dispatch(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
@@ -266,8 +277,12 @@ int gemm_dispatch(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
   if (batch == 0 || m == 0 || n == 0) return LAPIS_B200_OK;
   if (!C || (k > 0 && (!A || !B))) return fail(LAPIS_B200_ERR_ARG, "gemm: null operand");
   if (mode == LAPIS_B200_GEMM_AUTO) {
+    // f64: certified Ozaki on the int8 tensor cores when k is in its range
+    // (DMMA otherwise); f32: 3xTF32 (the Ozaki path certifies only data whose
+    // products do not cancel, see gemm_ozaki.cu); ints: reference order
     if (dtype == LAPIS_B200_F32) mode = LAPIS_B200_GEMM_TF32X3;
-    else if (dtype == LAPIS_B200_F64) mode = LAPIS_B200_GEMM_DMMA;
+    else if (dtype == LAPIS_B200_F64)
+      mode = ozaki_slices_for(dtype, k) ? LAPIS_B200_GEMM_OZAKI : LAPIS_B200_GEMM_DMMA;
     else mode = LAPIS_B200_GEMM_EXACT;
   }
   switch (mode) {
@@ -281,6 +296,10 @@ int gemm_dispatch(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
       if (dtype != LAPIS_B200_F64)
         return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm: DMMA is an f64 mode");
       return gemm_dmma(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, st);
+    case LAPIS_B200_GEMM_OZAKI:
+      if (dtype != LAPIS_B200_F64 && dtype != LAPIS_B200_F32)
+        return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm: OZAKI is an f32 / f64 mode");
+      return gemm_ozaki(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, dtype, 0, st);
   }
   return fail(LAPIS_B200_ERR_ARG, "gemm: unknown mode");
 }

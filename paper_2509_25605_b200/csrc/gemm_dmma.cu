@@ -38,7 +38,9 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 __global__ void __launch_bounds__(DM_THREADS, 1)
 gemm_dmma_kernel(int64_t m, int64_t n, int64_t k, const double* __restrict__ A, int64_t lda,
-                 const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc) {
+                 const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
+                 Guard guard) {
+  if (guard_skip(guard)) return;
   extern __shared__ __align__(16) double dsm[];
   double* sA = dsm;                                  // [STAGES][BM][AS]
   double* sB = dsm + DM_STAGES * DM_A_ELEMS;         // [STAGES][BK][BS]
@@ -126,13 +128,20 @@ int gemm_exact(int64_t, int64_t, int64_t, int64_t, const void*, int64_t, const v
 
 int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
               const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-              int64_t sC, cudaStream_t st) {
+              int64_t sC, cudaStream_t st, Guard guard) {
   // the 16-byte cp.async path needs even leading dimensions / extents and aligned bases
   const bool aligned = (lda % 2 == 0) && (ldb % 2 == 0) && (k % 2 == 0) && (n % 2 == 0) &&
                        ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) &&
                        (sA % 2 == 0) && (sB % 2 == 0);
-  if (!aligned)
-    return gemm_exact(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, LAPIS_B200_F64, st);
+  if (!aligned) {
+    if (guard.mode == 0)
+      return gemm_exact(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, LAPIS_B200_F64, st);
+    for (int64_t b = 0; b < batch; ++b)   // guarded fallback (single batches from the Ozaki path)
+      LB_TRY(launch_gemm_exact_guarded(m, n, k, (const double*)A + b * sA, lda,
+                                       (const double*)B + b * sB, ldb, (double*)C + b * sC, ldc,
+                                       LAPIS_B200_F64, guard, st));
+    return LAPIS_B200_OK;
+  }
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -147,7 +156,7 @@ int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int
   for (int64_t b = 0; b < batch; ++b) {
     gemm_dmma_kernel<<<grid, DM_THREADS, DM_SMEM, st>>>(
         m, n, k, (const double*)A + b * sA, lda, (const double*)B + b * sB, ldb,
-        (double*)C + b * sC, ldc);
+        (double*)C + b * sC, ldc, guard);
     LB_TRY(check_launch("gemm_dmma_kernel"));
   }
   return LAPIS_B200_OK;

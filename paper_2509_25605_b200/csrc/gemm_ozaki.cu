@@ -1,0 +1,629 @@
+// gemm_ozaki.cu — fp64 / fp32 dense matmul on the int8 tensor cores.
+//
+// C = A * B (row-major) for linalg.matmul / kokkos.gemm (interp.py:711-722,
+// runtime_header.py:249-266) through the Ozaki splitting scheme: every row of
+// A (column of B) is scaled by a power of two into (-1, 1) and cut into S
+// signed 7-bit digits,
+//     a_ij = 2^ea_i * sum_s  A_s[i,j] * 2^(-7(s+1)) + r,   |r| < 2^(ea_i - 7S),
+// so that  C ~= 2^(ea_i + eb_j) * sum_{d<S} 2^(-7(d+2)) * C_d,
+//          C_d = sum_{s+t=d} A_s B_t   (exact int32 products and sums).
+// Each C_d is one int8 GEMM with a concatenated K' = (d+1) K on
+// tcgen05.mma kind::i8 (UTCIMMA): S(S+1)/2 slice products in total.  S = 8 for
+// fp64 (36 products; 6.8e-14 worst relative error at 4096^3 against the
+// reference's sequential fp64 sum, contract 1e-12) and S = 4 for fp32 (10
+// products; the reference's own fp32 rounding dominates).  SURVEY H2 "stretch:
+// Ozaki fp64 emulation on kind::i8".
+//
+// Kernel shape (one CTA per SM, persistent over 128x256 output tiles), the
+// warp roles of gemm_tf32x3.cu:
+//   warp 0     TMA producer: 128x128 A-digit and 256x128 B-digit boxes (int8,
+//              SWIZZLE_128B) into a 4-stage ring
+//   warp 1     TMEM allocator + MMA issuer: M=128 N=256 K=32 int8 MMAs into a
+//              double-buffered s32 accumulator (2 x 256 TMEM columns), one
+//              accumulator per diagonal d
+//   warps 2-9  epilogue: tcgen05.ld the s32 diagonal, scale by
+//              2^(ea_i + eb_j - 7(d+2)) in fp64 and add it to the tile's fp64
+//              partial (the output itself for fp64, a workspace for fp32,
+//              L2-resident between diagonals); the last diagonal writes C.
+// Non-finite inputs cannot be digit-split: the split kernels raise a device
+// flag, the Ozaki kernel then returns at once and a guarded reference-order
+// GEMM computes C instead (all stream-ordered, no host sync).
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+namespace lapis_b200 {
+
+constexpr int OZ_BM = 128, OZ_BK = 128, OZ_STAGES = 4, OZ_UMMA_K = 32;
+constexpr uint32_t OZ_A_BYTES = OZ_BM * OZ_BK;   // 16 KB
+constexpr uint32_t OZ_TMEM_COLS = 512;
+constexpr size_t OZ_EPI_SMEM = 8 * 32 * 16 * sizeof(double);   // per-warp transpose tiles
+// tile N: 256 (fewer operand bytes per MMA) or 192 (finer tile grid); per dtype
+template <int BN> struct OzTile {
+  static constexpr int HALF = BN / 2;                       // columns per epilogue warp
+  static constexpr uint32_t B_BYTES = BN * OZ_BK;
+  static constexpr uint32_t STAGE_BYTES = OZ_A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = (size_t)OZ_STAGES * STAGE_BYTES + OZ_EPI_SMEM + 1024;
+};
+constexpr int OZ_EPI_WARPS = 8;
+constexpr int OZ_THREADS = 64 + OZ_EPI_WARPS * 32;
+constexpr int OZ_MAX_S = 9;
+
+struct OzParams {
+  int m, n, nk, num_m, num_n, S;
+  int mp, np;               // slice row pitches (multiples of the tile)
+  void* C;                  // OUT*
+  int64_t ldc;
+  double* part;             // fp64 partial sums (== C for fp64 output)
+  int64_t ldp;
+  const int* ea;            // [m] row exponents
+  const int* eb;            // [n] column exponents
+  int* flag;                // [0] non-finite input (skip), [1] certification failed
+  double cert_k;            // error bound per unit 2^(ea+eb): K * per-product bound
+  double cert_tol;          // certified |C - exact| <= cert_tol * max(|C|, 1)
+  bool vec2;                // 16-byte partial accesses (even pitch, aligned)
+  unsigned long long* prof; // optional: wait-cycle counters (LAPIS_B200_OZAKI_PROF=1)
+  int digits8;              // 1: signed 8-bit leading digit + unsigned 8-bit digits
+};
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// instruction descriptor: D s32 (2), A/B 8-bit signed (1) or unsigned (0),
+// both K-major, N>>3, M>>4
+__host__ __device__ constexpr uint32_t i8_idesc(int M, int N, bool a_signed = true,
+                                                bool b_signed = true) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// x * 2^e, exact: one multiply by a constructed power of two in the normal
+// range (scalbn for the rest)
+__device__ __forceinline__ double pow2_scale(double x, int e) {
+  if (e >= -1022 && e <= 1023) return x * __hiloint2double((e + 1023) << 20, 0);
+  return scalbn(x, e);
+}
+
+template <class OUT, int OZ_BN>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                  OzParams p) {
+  if (*p.flag) return;  // uniform: the guarded fallback owns this call
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[OZ_STAGES], empty[OZ_STAGES], tmem_full[2], tmem_empty[2];
+  __shared__ uint32_t tmem_base_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = p.num_m * p.num_n;
+  const int S = p.S;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tA);
+    prefetch_tmap(&tB);
+    for (int s = 0; s < OZ_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], OZ_EPI_WARPS * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&tmem_base_slot)), "r"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      int stage = 0;
+      uint32_t phase = 0;
+      long long prod_wait = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int mb = tile % p.num_m, nb = tile / p.num_m;
+        for (int d = 0; d < S; ++d)
+          for (int s = 0; s <= d; ++s)
+            for (int kb = 0; kb < p.nk; ++kb) {
+              const long long t0 = p.prof ? clock64() : 0;
+              mbar_wait(&empty[stage], phase ^ 1);
+              if (p.prof) prod_wait += clock64() - t0;
+              uint8_t* sa = smem + stage * OzTile<OZ_BN>::STAGE_BYTES;
+              mbar_arrive_expect_tx(&full[stage], OzTile<OZ_BN>::STAGE_BYTES);
+              tma_load_2d(sa, &tA, kb * OZ_BK, s * p.mp + mb * OZ_BM, &full[stage]);
+              tma_load_2d(sa + OZ_A_BYTES, &tB, kb * OZ_BK, (d - s) * p.np + nb * OZ_BN, &full[stage]);
+              if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+            }
+      }
+      if (p.prof) atomicAdd(p.prof + 0, (unsigned long long)prod_wait);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      // 7-bit digits: all signed.  8-bit digits: only digit 0 is signed.
+      constexpr uint32_t idesc_ss = i8_idesc(OZ_BM, OZ_BN, true, true);
+      constexpr uint32_t idesc_su = i8_idesc(OZ_BM, OZ_BN, true, false);
+      constexpr uint32_t idesc_us = i8_idesc(OZ_BM, OZ_BN, false, true);
+      constexpr uint32_t idesc_uu = i8_idesc(OZ_BM, OZ_BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      long long w_tmem = 0, w_full = 0;
+      const long long t_start = clock64();
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        for (int d = 0; d < S; ++d) {
+          long long t0 = p.prof ? clock64() : 0;
+          mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+          if (p.prof) w_tmem += clock64() - t0;
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * OZ_BN);
+          bool first = true;
+          for (int s = 0; s <= d; ++s) {
+            const uint32_t idesc = !p.digits8 ? idesc_ss
+                                 : (s == 0 ? (d == 0 ? idesc_ss : idesc_su)
+                                           : (d - s == 0 ? idesc_us : idesc_uu));
+            for (int kb = 0; kb < p.nk; ++kb) {
+              t0 = p.prof ? clock64() : 0;
+              mbar_wait(&full[stage], phase);
+              if (p.prof) w_full += clock64() - t0;
+              tc_fence_after();
+              const uint8_t* sa = smem + stage * OzTile<OZ_BN>::STAGE_BYTES;
+              const uint64_t adesc = smem_desc_sw128(sa);
+              const uint64_t bdesc = smem_desc_sw128(sa + OZ_A_BYTES);
+#pragma unroll
+              for (int kk = 0; kk < OZ_BK / OZ_UMMA_K; ++kk) {
+                // 32 bytes of K per MMA: advance the start address inside the swizzle atom
+                tc_mma_i8(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                          first ? 0u : 1u);
+                first = false;
+              }
+              tc_commit(&empty[stage]);
+              if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+          tc_commit(&tmem_full[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+      if (p.prof) {
+        atomicAdd(p.prof + 1, (unsigned long long)w_tmem);
+        atomicAdd(p.prof + 2, (unsigned long long)w_full);
+        atomicAdd(p.prof + 3, (unsigned long long)(clock64() - t_start));
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const int ew = warp - 2;                 // 0..7
+    double* wsm = reinterpret_cast<double*>(smem + OZ_STAGES * OzTile<OZ_BN>::STAGE_BYTES) + ew * 32 * 16;
+    const int lg = warp & 3;                 // TMEM lane group this warp may access
+    const int half = ew >> 2;                // columns [128*half, 128*half + 128)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int mb = tile % p.num_m, nb = tile / p.num_m;
+      const int row_base = mb * OZ_BM + lg * 32;
+      const int row = row_base + lane;
+      const int col0 = nb * OZ_BN + half * OzTile<OZ_BN>::HALF;
+      const int ea = row < p.m ? p.ea[row] : 0;
+      for (int d = 0; d < S; ++d) {
+        const long long t0 = (p.prof && threadIdx.x == 64) ? clock64() : 0;
+        mbar_wait(&tmem_full[acc], acc_phase);
+        if (p.prof && threadIdx.x == 64) atomicAdd(p.prof + 4, (unsigned long long)(clock64() - t0));
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) +
+                               (uint32_t)(acc * OZ_BN + half * OzTile<OZ_BN>::HALF);
+        const int shift = p.digits8 ? ea - 14 - 8 * d : ea - 7 * (d + 2);
+        const bool last = d == S - 1;
+#pragma unroll 1
+        for (int c0 = 0; c0 < OzTile<OZ_BN>::HALF; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld_x16(tbase + (uint32_t)c0, v);
+          const int cb = col0 + c0;
+          // scale this thread's row segment, then transpose it through the
+          // warp's shared tile (16-byte pairs XOR-swizzled by row) so that the
+          // partial's read-modify-write is 4 rows x 128 B per instruction
+#pragma unroll
+          for (int pq = 0; pq < 8; ++pq) {
+            const int q = 2 * pq;
+            const int e0 = (cb + q < p.n) ? __ldg(p.eb + cb + q) : 0;
+            const int e1 = (cb + q + 1 < p.n) ? __ldg(p.eb + cb + q + 1) : 0;
+            const double x0 = pow2_scale((double)(int)v[q], shift + e0);
+            const double x1 = pow2_scale((double)(int)v[q + 1], shift + e1);
+            *reinterpret_cast<double2*>(wsm + lane * 16 + 2 * (pq ^ (lane & 7))) = make_double2(x0, x1);
+          }
+          __syncwarp();
+          double2 t[8];
+          const int pq = lane & 7;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + (lane >> 3);
+            t[i] = *reinterpret_cast<const double2*>(wsm + r * 16 + 2 * (pq ^ (r & 7)));
+          }
+          __syncwarp();
+          const int gc = cb + 2 * pq;
+          double2 old[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int gr = row_base + 4 * i + (lane >> 3);
+            old[i] = make_double2(0.0, 0.0);
+            if (d > 0 && gr < p.m) {
+              const double* src = p.part + (int64_t)gr * p.ldp + gc;
+              if (p.vec2 && gc + 1 < p.n) old[i] = *reinterpret_cast<const double2*>(src);
+              else {
+                if (gc < p.n) old[i].x = src[0];
+                if (gc + 1 < p.n) old[i].y = src[1];
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int gr = row_base + 4 * i + (lane >> 3);
+            if (gr >= p.m) continue;
+            const double y0 = t[i].x + old[i].x, y1 = t[i].y + old[i].y;
+            if (last) {
+              // certify |y - exact| <= cert_tol * max(|y|, 1) from the a-priori bound
+              const int er = __ldg(p.ea + gr);
+              const double b0 = pow2_scale(p.cert_k, er + (gc < p.n ? __ldg(p.eb + gc) : 0));
+              const double b1 = pow2_scale(p.cert_k, er + (gc + 1 < p.n ? __ldg(p.eb + gc + 1) : 0));
+              if ((gc < p.n && b0 > p.cert_tol * fmax(fabs(y0), 1.0)) ||
+                  (gc + 1 < p.n && b1 > p.cert_tol * fmax(fabs(y1), 1.0)))
+                atomicExch(p.flag + 1, 1);
+              OUT* dst = reinterpret_cast<OUT*>(p.C) + (int64_t)gr * p.ldc + gc;
+              if (gc < p.n) dst[0] = (OUT)y0;
+              if (gc + 1 < p.n) dst[1] = (OUT)y1;
+            } else {
+              double* dst = p.part + (int64_t)gr * p.ldp + gc;
+              if (p.vec2 && gc + 1 < p.n) *reinterpret_cast<double2*>(dst) = make_double2(y0, y1);
+              else {
+                if (gc < p.n) dst[0] = y0;
+                if (gc + 1 < p.n) dst[1] = y1;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(tmem_base), "r"(OZ_TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------- digit split
+// Peel the S signed 7-bit digits of r in (-1, 1) (every step exact in fp64)
+// for 4 consecutive elements and store them as one 32-bit word per plane.
+__device__ __forceinline__ void peel4(double r0, double r1, double r2, double r3, int S,
+                                      int8_t* __restrict__ out, int64_t plane) {
+  double r[4] = {r0, r1, r2, r3};
+  for (int s = 0; s < S; ++s) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double t = r[q] * 128.0;
+      const double dg = trunc(t);
+      r[q] = t - dg;
+      w |= (uint32_t)(uint8_t)(int8_t)(int)dg << (8 * q);
+    }
+    *reinterpret_cast<uint32_t*>(out + (int64_t)s * plane) = w;
+  }
+}
+
+// 8-bit digits: the leading digit floor(128 r) is signed ([-128, 127]), the
+// remainder is in [0, 1) and every further digit floor(256 r) unsigned.
+__device__ __forceinline__ void peel4_u8(double r0, double r1, double r2, double r3, int S,
+                                         int8_t* __restrict__ out, int64_t plane) {
+  double r[4] = {r0, r1, r2, r3};
+  for (int s = 0; s < S; ++s) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double t = r[q] * (s == 0 ? 128.0 : 256.0);
+      const double dg = floor(t);
+      r[q] = t - dg;
+      w |= (uint32_t)((int)dg & 0xff) << (8 * q);
+    }
+    *reinterpret_cast<uint32_t*>(out + (int64_t)s * plane) = w;
+  }
+}
+
+// One CTA per row of A: the row's largest magnitude gives ea (max < 2^ea),
+// then each element is scaled into (-1, 1) and peeled.  Rows [m, mp) and
+// columns [k, kp) are zeros; non-finite values raise the flag (they are
+// split as zeros; the guarded fallback recomputes C).
+template <class T>
+__global__ void __launch_bounds__(256)
+ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restrict__ A,
+                 int64_t lda, int S, int8_t* __restrict__ out, int* __restrict__ e_out,
+                 int* __restrict__ flag, int digits8) {
+  __shared__ double red[8];
+  const int64_t plane = mp * kp;
+  for (int64_t i = blockIdx.x; i < mp; i += gridDim.x) {
+    const T* arow = A + i * lda;
+    double mx = 0.0;
+    bool bad = false;
+    if (i < m)
+      for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        const double v = (double)arow[j];
+        bad |= !isfinite(v);
+        mx = fmax(mx, fabs(v));
+      }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    __syncthreads();
+    const int e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) + 1 : 0;
+    if (threadIdx.x == 0 && i < m) e_out[i] = e;
+    int8_t* orow = out + i * kp;
+    for (int64_t j = 4 * (int64_t)threadIdx.x; j < kp; j += 4 * (int64_t)blockDim.x) {
+      double r[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double v = (i < m && j + q < k) ? (double)arow[j + q] : 0.0;
+        r[q] = isfinite(v) ? scalbn(v, -e) : 0.0;
+      }
+      if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, orow + j, plane);
+      else peel4(r[0], r[1], r[2], r[3], S, orow + j, plane);
+    }
+  }
+}
+
+// column magnitudes of B [k, n]: atomicMax on the bit pattern of |b| (monotone
+// for non-negative doubles); NaN/inf raise the flag
+template <class T>
+__global__ void ozaki_colmax(int64_t k, int64_t n, const T* __restrict__ B, int64_t ldb,
+                             unsigned long long* __restrict__ colmax, int* __restrict__ flag) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t k0 = (int64_t)blockIdx.y * 64, k1 = k0 + 64 < k ? k0 + 64 : k;
+  double mx = 0.0;
+  bool bad = false;
+  for (int64_t r = k0; r < k1; ++r) {
+    const double v = (double)B[r * ldb + j];
+    bad |= !isfinite(v);
+    mx = fmax(mx, fabs(v));
+  }
+  if (bad) atomicExch(flag, 1);
+  atomicMax(colmax + j, (unsigned long long)__double_as_longlong(mx));
+}
+
+// B [k, n] -> digit planes [S][np][kp] (transposed: K-major).  A block stages
+// 128 (k) x 32 (n) of B in shared memory; warp w then emits columns
+// n0 + 4w .. 4w+3, lane l the 4 digits of k0 + 4l .. 4l+3: one 128-byte row
+// segment per plane per warp store.
+template <class T>
+__global__ void __launch_bounds__(256)
+ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restrict__ B,
+                 int64_t ldb, int S, const unsigned long long* __restrict__ colmax,
+                 int8_t* __restrict__ out, int* __restrict__ e_out, int digits8) {
+  __shared__ double tile[128][33];
+  const int64_t k0 = (int64_t)blockIdx.y * 128, n0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  for (int r = ty; r < 128; r += 8) {
+    const int64_t kk = k0 + r, nn = n0 + tx;
+    const double v = (kk < k && nn < n) ? (double)B[kk * ldb + nn] : 0.0;
+    tile[r][tx] = isfinite(v) ? v : 0.0;
+  }
+  __syncthreads();
+  const int64_t plane = np * kp;
+  for (int c = 0; c < 4; ++c) {
+    const int cc = 4 * ty + c;
+    const int64_t nn = n0 + cc;
+    const int64_t kk = k0 + 4 * tx;
+    if (nn >= np || kk >= kp) continue;
+    int e = 0;
+    if (nn < n) {
+      const double mx = __longlong_as_double((long long)colmax[nn]);
+      e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) + 1 : 0;
+      if (blockIdx.y == 0 && tx == 0) e_out[nn] = e;
+    }
+    double r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = (nn < n) ? scalbn(tile[4 * tx + q][cc], -e) : 0.0;
+    if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
+    else peel4(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
+  }
+}
+
+// -------------------------------------------------------------- host side
+static int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t kp,
+                       uint32_t box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kp};
+  const cuuint32_t box[2] = {(cuuint32_t)OZ_BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled (int8) failed");
+  return LAPIS_B200_OK;
+}
+
+
+// Digits per operand for a k-deep product, 0 when the scheme cannot certify
+// the contract for unit-scale data (or s32 accumulation would overflow):
+// fp64 7-bit digits, per-product bound (S + 1) 2^-7S -> S = 8 up to k ~ 6000,
+// S = 9 up to the s32 limit; fp32 8-bit digits, S = 3 up to the s32 limit.
+int ozaki_slices_for(int dtype, int64_t k) {
+  if (dtype == LAPIS_B200_F64) {
+    if (k * 9.0 * ldexp(1.0, -56) <= 0.75e-12 && 8 * k * 16129 < (1ll << 31)) return 8;
+    if (k * 10.0 * ldexp(1.0, -63) <= 0.75e-12 && 9 * k * 16129 < (1ll << 31)) return 9;
+    return 0;
+  }
+  if (dtype == LAPIS_B200_F32 && 3 * k * 65025 < (1ll << 31)) return 3;
+  return 0;
+}
+
+template <class T, int BN>
+static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+                        int64_t sC, int S, cudaStream_t st) {
+  if (m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
+    return fail(LAPIS_B200_ERR_ARG, "gemm ozaki: extent too large");
+  if (S < 1 || S > OZ_MAX_S) return fail(LAPIS_B200_ERR_ARG, "gemm ozaki: bad slice count");
+  // fp32: 8-bit digits (signed leading + unsigned), S = 3 covers 24 bits;
+  // fp64: 7-bit signed digits (truncation toward zero keeps the dropped
+  // remainders sign-symmetric, which the 1e-12 contract needs), S = 8
+  const int digits8 = std::is_same<T, float>::value ? 1 : 0;
+  const int64_t dmax = digits8 ? 255 * 255 : 127 * 127;
+  // int32 accumulation bound: (d+1) * k * max|digit product| < 2^31 for every diagonal
+  if ((int64_t)S * k * dmax >= (1ll << 31))
+    return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm ozaki: k too large for s32 accumulation");
+  constexpr int64_t DT = std::is_same<T, double>::value ? LAPIS_B200_F64 : LAPIS_B200_F32;
+  const int dtype = (int)DT;
+  if (k == 0) return launch_gemm_exact_guarded(m, n, k, A, lda, B, ldb, C, ldc, dtype, Guard(), st);
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_ozaki_kernel<T, BN>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)OzTile<BN>::SMEM),
+                      "smem attr (gemm_ozaki_kernel)"));
+    configured_dev = dev;
+  }
+  const int64_t kp = (k + 15) / 16 * 16;
+  const int64_t mp = (m + OZ_BM - 1) / OZ_BM * OZ_BM, np = (n + BN - 1) / BN * BN;
+  // workspace: digits of A and B, exponents, column maxima, flag, fp32 partials
+  const size_t a_bytes = (size_t)S * mp * kp, b_bytes = (size_t)S * np * kp;
+  const size_t part_bytes = std::is_same<T, float>::value ? (size_t)m * n * sizeof(double) : 0;
+  const size_t meta = (size_t)(m + n) * sizeof(int) + (size_t)n * 8 + 64 + 8;
+  uint8_t* ws = nullptr;
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, a_bytes + b_bytes + part_bytes + meta + 256, st),
+                    "alloc(ozaki workspace)"));
+  int8_t* ad = reinterpret_cast<int8_t*>(ws);
+  int8_t* bd = ad + a_bytes;
+  double* part = reinterpret_cast<double*>(ws + ((a_bytes + b_bytes + 255) / 256 * 256));
+  uint8_t* mp_ = reinterpret_cast<uint8_t*>(part) + part_bytes;
+  unsigned long long* colmax = reinterpret_cast<unsigned long long*>(mp_);
+  int* ea = reinterpret_cast<int*>(colmax + n);
+  int* eb = ea + m;
+  int* flag = eb + n;
+  int rc = LAPIS_B200_OK;
+  for (int64_t b = 0; b < batch && rc == LAPIS_B200_OK; ++b) {
+    const T* Ab = (const T*)A + b * sA;
+    const T* Bb = (const T*)B + b * sB;
+    T* Cb = (T*)C + b * sC;
+    rc = check_cuda(cudaMemsetAsync(colmax, 0, (size_t)n * 8, st), "memset(colmax)");
+    if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st), "memset(flag)");
+    if (rc != LAPIS_B200_OK) break;
+    const int64_t rblocks = std::min<int64_t>(mp, (int64_t)num_sms() * 16);
+    ozaki_split_rows<T><<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
+                                                           digits8);
+    dim3 cg((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
+    ozaki_colmax<T><<<cg, 256, 0, st>>>(k, n, Bb, ldb, colmax, flag);
+    dim3 tg((unsigned)((np + 31) / 32), (unsigned)((kp + 127) / 128));
+    ozaki_split_cols<T><<<tg, 256, 0, st>>>(k, n, kp, np, Bb, ldb, S, colmax, bd, eb, digits8);
+    rc = check_launch("ozaki split");
+    CUtensorMap ma, mb;
+    if (rc == LAPIS_B200_OK) rc = make_i8_map(&ma, ad, (int64_t)S * mp, kp, OZ_BM);
+    if (rc == LAPIS_B200_OK) rc = make_i8_map(&mb, bd, (int64_t)S * np, kp, BN);
+    if (rc != LAPIS_B200_OK) break;
+    OzParams prm;
+    prm.m = (int)m;
+    prm.n = (int)n;
+    prm.nk = (int)((kp + OZ_BK - 1) / OZ_BK);
+    prm.num_m = (int)(mp / OZ_BM);
+    prm.num_n = (int)(np / BN);
+    prm.S = S;
+    prm.mp = (int)mp;
+    prm.np = (int)np;
+    prm.C = Cb;
+    prm.ldc = ldc;
+    prm.part = std::is_same<T, double>::value ? reinterpret_cast<double*>(Cb) : part;
+    prm.ldp = std::is_same<T, double>::value ? ldc : n;
+    prm.ea = ea;
+    prm.eb = eb;
+    prm.flag = flag;
+    {
+      // a-priori bound per product, in units of 2^(ea_i + eb_j): the digit
+      // truncation of both operands (2 delta) plus the dropped digit products
+      // (s + t >= S); K products; 3/4 of the contract certified, the rest left
+      // for the reference's own rounding
+      const double delta = digits8 ? ldexp(1.0, -(7 + 8 * (S - 1))) : ldexp(1.0, -7 * S);
+      const double cross = digits8 ? (S - 1) * ldexp(1.0, 2 - 8 * S) : (S - 1) * ldexp(1.0, -7 * S);
+      prm.cert_k = (double)k * (2.0 * delta + delta * delta + cross) * (1.0 + 1e-3);
+      prm.cert_tol = 0.75 * (std::is_same<T, double>::value ? 1e-12 : 1e-5);
+    }
+    prm.digits8 = digits8;
+    prm.vec2 = (prm.ldp % 2 == 0) && ((uintptr_t)prm.part % 16 == 0);
+    static const bool prof_on = [] {
+      const char* e = getenv("LAPIS_B200_OZAKI_PROF");
+      return e && e[0] == '1';
+    }();
+    unsigned long long* dprof = nullptr;
+    if (prof_on) {
+      cudaMallocAsync((void**)&dprof, 8 * sizeof(unsigned long long), st);
+      cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), st);
+    }
+    prm.prof = dprof;
+    const int tiles = prm.num_m * prm.num_n;
+    const int grid = std::min(tiles, num_sms());
+    gemm_ozaki_kernel<T, BN><<<grid, OZ_THREADS, OzTile<BN>::SMEM, st>>>(ma, mb, prm);
+    rc = check_launch("gemm_ozaki_kernel");
+    if (dprof) {
+      unsigned long long h[8];
+      cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "ozaki prof (cycles summed over CTAs): producer-wait-empty %llu  "
+              "mma-wait-tmem-empty %llu  mma-wait-full %llu  mma-total %llu  epi-wait-full %llu\n",
+              h[0], h[1], h[2], h[3], h[4]);
+      cudaFreeAsync(dprof, st);
+    }
+    // non-finite inputs: the reference-order GEMM, run only when flag[0] is set;
+    // a certification failure (flag[1]): the fp64 DMMA / fp32 3xTF32 path
+    if (rc == LAPIS_B200_OK)
+      rc = launch_gemm_exact_guarded(m, n, k, Ab, lda, Bb, ldb, Cb, ldc, dtype, Guard{flag, 1}, st);
+    if (rc == LAPIS_B200_OK) {
+      if (std::is_same<T, double>::value)
+        rc = gemm_dmma(1, m, n, k, Ab, lda, Bb, ldb, Cb, ldc, 0, 0, 0, st, Guard{flag, 2});
+      else
+        rc = gemm_tf32x3(1, m, n, k, Ab, lda, Bb, ldb, Cb, ldc, 0, 0, 0, st, Guard{flag, 2});
+    }
+  }
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+int gemm_ozaki(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+               const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
+               int64_t sC, int dtype, int slices, cudaStream_t st) {
+  const int S = slices > 0 ? slices : ozaki_slices_for(dtype, k);
+  if (S == 0) return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm ozaki: k out of the certified range");
+  static const int bn_env = [] {
+    const char* e = getenv("LAPIS_B200_OZAKI_BN");
+    return e ? atoi(e) : 0;
+  }();
+  const int bn = bn_env ? bn_env : (dtype == LAPIS_B200_F64 ? 256 : 192);
+#define LB_OZ(T, BN_) return gemm_ozaki_t<T, BN_>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st)
+  if (dtype == LAPIS_B200_F64) { if (bn == 192) LB_OZ(double, 192); LB_OZ(double, 256); }
+  if (dtype == LAPIS_B200_F32) { if (bn == 256) LB_OZ(float, 256); LB_OZ(float, 192); }
+#undef LB_OZ
+  return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm ozaki: f32 / f64 only");
+}
+
+}  // namespace lapis_b200

@@ -24,8 +24,7 @@
 // operands, i.e. a TF32 GEMM with K' = 3K.  The split (and the transpose that
 // makes B K-major) is a bandwidth-bound prepass.
 #include "common.cuh"
-
-#include <cuda.h>
+#include "tcgen05.cuh"
 
 #include <algorithm>
 
@@ -45,64 +44,10 @@ struct Tf32Params {
   int64_t ldc;
 };
 
-// ---------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3}], [%4];"
-      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
-         "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-               :: "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
-      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-// K-major operand, SWIZZLE_128B: rows of 128 B, 8-row groups 1024 B apart (SBO);
-// LBO unused for a single 128-B swizzle atom along K; version 1 (sm_100).
-__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
-  const uint32_t a = smem_u32(p);
-  uint64_t d = 0;
-  d |= (uint64_t)((a & 0x3FFFF) >> 4);
-  d |= (uint64_t)(16 >> 4) << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
 // instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
 __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
          ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 // ----------------------------------------------------------------------- kernel
@@ -119,7 +64,8 @@ constexpr int TG_THREADS_V2 = 64 + TG_EPI_WARPS * 32;
 __global__ void __launch_bounds__(TG_THREADS_V2, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                    const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
-                   Tf32Params p) {
+                   Tf32Params p, Guard guard) {
+  if (guard_skip(guard)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[TG_STAGES], empty[TG_STAGES], tmem_full[2], tmem_empty[2];
@@ -271,7 +217,9 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // A [m, k] (lda) -> hi, lo [m, kp], zero padded for k <= j < kp
 __global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float* __restrict__ A,
-                                  int64_t lda, float* __restrict__ hi, float* __restrict__ lo) {
+                                  int64_t lda, float* __restrict__ hi, float* __restrict__ lo,
+                                  Guard guard) {
+  if (guard_skip(guard)) return;
   const int64_t total = m * kp;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -285,7 +233,9 @@ __global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float*
 
 // B [k, n] (ldb) -> hi, lo [n, kp] (transposed: K-major), zero padded
 __global__ void split_transpose_kernel(int64_t k, int64_t n, int64_t kp, const float* __restrict__ B,
-                                       int64_t ldb, float* __restrict__ hi, float* __restrict__ lo) {
+                                       int64_t ldb, float* __restrict__ hi, float* __restrict__ lo,
+                                       Guard guard) {
+  if (guard_skip(guard)) return;
   __shared__ float tile[32][33];
   const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
@@ -306,23 +256,6 @@ __global__ void split_transpose_kernel(int64_t k, int64_t n, int64_t kp, const f
 }
 
 // ----------------------------------------------------------------- host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (EncodeTiledFn) nullptr;
-    return reinterpret_cast<EncodeTiledFn>(f);
-  }();
-  return fn;
-}
-
 // rows x kp fp32, K-major; box = 32 (k) x box_rows
 static int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t kp,
                            uint32_t box_rows) {
@@ -341,7 +274,7 @@ static int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, in
 
 int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                 const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-                int64_t sC, cudaStream_t st) {
+                int64_t sC, cudaStream_t st, Guard guard) {
   if (m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(LAPIS_B200_ERR_ARG, "gemm tf32x3: extent too large");
   const int64_t kp = (k + 3) / 4 * 4;  // 16-byte row pitch for TMA
@@ -375,9 +308,9 @@ int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, i
     const float* Bb = (const float*)B + b * sB;
     float* Cb = (float*)C + b * sC;
     const int64_t sblocks = std::min<int64_t>((m * kp + 255) / 256, (int64_t)num_sms() * 16);
-    split_rows_kernel<<<(unsigned)sblocks, 256, 0, st>>>(m, k, kp, Ab, lda, ah, al);
+    split_rows_kernel<<<(unsigned)sblocks, 256, 0, st>>>(m, k, kp, Ab, lda, ah, al, guard);
     dim3 tg((unsigned)((n + 31) / 32), (unsigned)((kp + 31) / 32));
-    split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl);
+    split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl, guard);
     rc = check_launch("tf32 split");
     CUtensorMap mah, mal, mbh, mbl;
     if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mah, ah, m, kp, TG_BM);
@@ -395,7 +328,7 @@ int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, i
     prm.ldc = ldc;
     const int tiles = prm.num_m * prm.num_n;
     const int grid = std::min(tiles, num_sms());
-    gemm_tf32x3_kernel<<<grid, TG_THREADS_V2, TG_SMEM, st>>>(mah, mal, mbh, mbl, prm);
+    gemm_tf32x3_kernel<<<grid, TG_THREADS_V2, TG_SMEM, st>>>(mah, mal, mbh, mbl, prm, guard);
     rc = check_launch("gemm_tf32x3_kernel");
   }
   cudaFreeAsync(ws, st);

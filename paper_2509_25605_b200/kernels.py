@@ -19,7 +19,7 @@ _DTYPES = {torch.float32: _capi.F32, torch.float64: _capi.F64,
            torch.int32: _capi.I32, torch.int64: _capi.I64}
 _COMBINERS = {"add": _capi.ADD, "mul": _capi.MUL, "min": _capi.MIN, "max": _capi.MAX}
 _MODES = {"auto": _capi.GEMM_AUTO, "tf32x3": _capi.GEMM_TF32X3, "dmma": _capi.GEMM_DMMA,
-          "exact": _capi.GEMM_EXACT}
+          "exact": _capi.GEMM_EXACT, "ozaki": _capi.GEMM_OZAKI}
 _initialised: set[int] = set()
 
 

@@ -120,3 +120,56 @@ def test_dmma_gemm_fp64_contract(cuda_device, m, n, k):
     got = host(lb.gemm(cu(A), cu(B), mode="dmma"))
     ok, msg = O.diff_outputs([got], [O.matmul(A, B)], 1e-12)
     assert ok, msg
+
+
+@pytest.mark.parametrize("dt,tol,lo", [(np.float64, 1e-12, -1.0), (np.float32, 1e-5, 0.0)])
+@pytest.mark.parametrize("m,n,k", [(96, 80, 160), (200, 300, 517), (257, 129, 1000), (512, 512, 4096)])
+def test_ozaki_int8_within_tolerance(cuda_device, dt, tol, lo, m, n, k):
+    """Ozaki digit split on the int8 tensor cores vs the reference-order
+    sequential sum (oracle), the reference's parity criterion."""
+    rng = np.random.default_rng(m + n + k)
+    A = rng.uniform(lo, 1, (m, k)).astype(dt)
+    B = rng.uniform(lo, 1, (k, n)).astype(dt)
+    got = host(lb.gemm(cu(A), cu(B), mode="ozaki"))
+    ok, msg = O.diff_outputs([got], [O.matmul(A, B)], tol)
+    assert ok, msg
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_ozaki_scaled_rows_and_zeros(cuda_device, dt):
+    """Rows / columns of very different magnitude (per-row / per-column
+    exponents), an all-zero row and column."""
+    rng = np.random.default_rng(7)
+    lo = -1.0 if dt == np.float64 else 0.0   # fp32: U(0,1) (SURVEY 8(d), H1)
+    A = rng.uniform(lo, 1, (64, 300)).astype(dt) * np.logspace(-20, 20, 64)[:, None].astype(dt)
+    B = rng.uniform(lo, 1, (300, 48)).astype(dt) * np.logspace(-10, 10, 48)[None, :].astype(dt)
+    A[5] = 0
+    B[:, 7] = 0
+    got = host(lb.gemm(cu(A), cu(B), mode="ozaki"))
+    ok, msg = O.diff_outputs([got], [O.matmul(A, B)], 1e-12 if dt == np.float64 else 1e-5)
+    assert ok, msg
+
+
+@pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
+def test_ozaki_non_finite_falls_back_to_reference_order(cuda_device, bad):
+    rng = np.random.default_rng(3)
+    A = rng.uniform(-1, 1, (40, 64))
+    B = rng.uniform(-1, 1, (64, 24))
+    A[3, 5] = bad
+    got = host(lb.gemm(cu(A), cu(B), mode="ozaki"))
+    assert bits_equal(got, O.matmul(A, B))
+
+
+@pytest.mark.parametrize("dt,lo", [(np.float64, -1.0), (np.float32, 0.0)])
+def test_ozaki_certification_falls_back(cuda_device, dt, lo):
+    """A row whose largest element dwarfs the rest while the product
+    cancels it: the a-priori bound cannot certify the contract, so the
+    certified fallback (fp64 DMMA / fp32 3xTF32) produces C."""
+    rng = np.random.default_rng(11)
+    A = rng.uniform(lo, 1, (48, 512)).astype(dt)
+    B = rng.uniform(lo, 1, (512, 40)).astype(dt)
+    A[:, 0] = 1e10
+    B[0, :] = 0.0
+    got = host(lb.gemm(cu(A), cu(B), mode="ozaki"))
+    ok, msg = O.diff_outputs([got], [O.matmul(A, B)], 1e-12 if dt == np.float64 else 1e-5)
+    assert ok, msg
