@@ -114,11 +114,43 @@ def build_reference(force: bool = False) -> Path | None:
     return REF_SO
 
 
+EMITTED = OUT / "emitted"
+RUN_GOLDEN = HERE.parent / "tests" / "golden" / "run"
+
+
+def emit_run_cases(force: bool = False) -> list:
+    """The reference emitter's Kokkos C++ for every lowered drop-in case
+    (tests/golden/run/*.lowered.mlir) -> oracle/_ref/emitted/<name>.hpp, plus
+    the runtime header.  Compiled on the GPU box against
+    include/kokkos_b200/Kokkos_Core.hpp by tests/test_kokkos_b200_gpu.py.
+    Cases the reference emitter rejects are skipped (listed in index.txt)."""
+    if not reference_available():
+        return []
+    EMITTED.mkdir(parents=True, exist_ok=True)
+    index = EMITTED / "index.txt"
+    srcs = sorted(RUN_GOLDEN.glob("*.lowered.mlir"))
+    if not force and index.exists() and not _stale(index, [*srcs, __file__]):
+        return index.read_text().split()
+    ok = []
+    for src in srcs:
+        name = src.name[: -len(".lowered.mlir")]
+        try:
+            _lapis_cli(["translate", "--header-name", name, "--emit-runtime-header",
+                        str(EMITTED / "lapis_dualview_runtime.hpp"), "-o",
+                        str(EMITTED / f"{name}.hpp"), str(src)])
+            ok.append(name)
+        except RuntimeError:
+            continue
+    index.write_text("\n".join(ok) + "\n")
+    return ok
+
+
 def main() -> None:
     force = "--force" in sys.argv
     print("oracle:", build_oracle(force))
     ref = build_reference(force)
     print("reference CPU path:", ref if ref else "unavailable (no /root/reference and no prebuilt)")
+    print("emitted C++ cases:", len(emit_run_cases(force)))
 
 
 if __name__ == "__main__":
