@@ -629,6 +629,11 @@ def cpu_baseline(wl, args, threads):
         return {"unavailable": "oracle/_ref not built"}, None
     want, got, times, work, desc, tol = wl.cpu_reference(args.cpu_rows, threads, args.cpu_reps)
     t = float(np.median(times))
+    # about 10 s of CPU work in total (bounded sample, repeated)
+    reps = int(min(2000, max(args.cpu_reps, np.ceil(args.cpu_seconds / max(t, 1e-6)))))
+    if reps > args.cpu_reps:
+        want, got, times, work, desc, tol = wl.cpu_reference(args.cpu_rows, threads, reps)
+        t = float(np.median(times))
     scale = 1e9 if wl.unit == "GB/s" else 1e12
     base = {"value": round(work / t / scale, 4), "unit": wl.unit, "cores": threads,
             "kind": "reference", "sample": desc + f", median of {len(times)} reps",
@@ -676,6 +681,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="problem size override")
     ap.add_argument("--cpu-rows", type=int, default=4_000_000)
     ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU time of the cpu_baseline sample (reps are added to reach it)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--vl", type=int, default=0,
