@@ -14,6 +14,8 @@
 // gemm_tf32x3.cu and gemm_dmma.cu.
 #include "common.cuh"
 
+#include <type_traits>
+
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -100,6 +102,103 @@ gemm_exact_kernel(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int6
   }
 }
 
+// -------------------------------------------- exact GEMM, narrow B (N, K <= 64)
+// The GCN's (A_hat X) W: M = 1e6 rows against a 64 x 64 W.  The whole B sits in
+// shared memory; a CTA stages 256 rows of A (coalesced, padded) per pass and
+// each thread owns 4 rows x 16 columns (64 independent accumulator chains),
+// walking k in the reference order with separately rounded mul / add — the
+// same result as gemm_exact_kernel bit for bit, at ~1 shared load per 16
+// floating-point operations (B read as broadcast 16-byte vectors).
+constexpr int EN_MAX = 64, EN_ROWS = 256, EN_COLS = 16, EN_RPT = 4;
+constexpr size_t EN_SMEM = (size_t)(EN_MAX * EN_MAX + EN_ROWS * (EN_MAX + 1)) * sizeof(float);
+
+template <bool RELU>
+__global__ void __launch_bounds__(256)
+gemm_exact_narrow_kernel(int64_t m, int n, int k, const float* __restrict__ A, int64_t lda,
+                         const float* __restrict__ B, int64_t ldb, float* __restrict__ C,
+                         int64_t ldc) {
+  extern __shared__ __align__(16) float en_smem[];
+  float* Bs = en_smem;                          // [EN_MAX][EN_MAX]
+  float* As = en_smem + EN_MAX * EN_MAX;        // [EN_ROWS][EN_MAX + 1]
+  for (int t = threadIdx.x; t < EN_MAX * EN_MAX; t += blockDim.x) {
+    const int r = t / EN_MAX, c = t % EN_MAX;
+    Bs[t] = (r < k && c < n) ? B[(int64_t)r * ldb + c] : 0.0f;
+  }
+  const int cg = threadIdx.x & 3;          // columns [16 cg, 16 cg + 16)
+  const int rg = threadIdx.x >> 2;         // rows 4 rg .. 4 rg + 3 of the pass
+  const bool vec4 = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0) && (k % 4 == 0);
+  for (int64_t r0 = (int64_t)blockIdx.x * EN_ROWS; r0 < m; r0 += (int64_t)gridDim.x * EN_ROWS) {
+    __syncthreads();
+    // stage the pass's rows: all loads of a thread issued before any store
+    // (a store right after each load would serialise one DRAM latency per
+    // element); 16-byte loads when the pitch allows
+    if (vec4) {
+      float4 v[EN_ROWS * EN_MAX / 4 / 256];
+#pragma unroll
+      for (int u = 0; u < EN_ROWS * EN_MAX / 4 / 256; ++u) {
+        const int t = threadIdx.x + 256 * u;
+        const int r = t / (EN_MAX / 4), c4 = (t % (EN_MAX / 4)) * 4;
+        v[u] = (r0 + r < m && c4 < k) ? *reinterpret_cast<const float4*>(A + (r0 + r) * lda + c4)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < EN_ROWS * EN_MAX / 4 / 256; ++u) {
+        const int t = threadIdx.x + 256 * u;
+        const int r = t / (EN_MAX / 4), c4 = (t % (EN_MAX / 4)) * 4;
+        float* d = As + r * (EN_MAX + 1) + c4;
+        d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+      }
+    } else {
+      for (int t0 = 0; t0 < EN_ROWS * EN_MAX; t0 += 256 * 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + threadIdx.x + 256 * u;
+          const int r = t / EN_MAX, c = t % EN_MAX;
+          v[u] = (r0 + r < m && c < k) ? A[(r0 + r) * lda + c] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + threadIdx.x + 256 * u;
+          As[(t / EN_MAX) * (EN_MAX + 1) + t % EN_MAX] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    float acc[EN_RPT][EN_COLS];
+#pragma unroll
+    for (int i = 0; i < EN_RPT; ++i)
+#pragma unroll
+      for (int q = 0; q < EN_COLS; ++q) acc[i][q] = 0.0f;
+    for (int kk = 0; kk < k; ++kk) {
+      float a[EN_RPT];
+#pragma unroll
+      for (int i = 0; i < EN_RPT; ++i) a[i] = As[(rg * EN_RPT + i) * (EN_MAX + 1) + kk];
+      float bv[EN_COLS];
+      const float4* brow = reinterpret_cast<const float4*>(Bs + kk * EN_MAX + cg * EN_COLS);
+#pragma unroll
+      for (int q = 0; q < EN_COLS / 4; ++q) {
+        const float4 w = brow[q];
+        bv[4 * q] = w.x; bv[4 * q + 1] = w.y; bv[4 * q + 2] = w.z; bv[4 * q + 3] = w.w;
+      }
+#pragma unroll
+      for (int i = 0; i < EN_RPT; ++i)
+#pragma unroll
+        for (int q = 0; q < EN_COLS; ++q) acc[i][q] = __fadd_rn(acc[i][q], __fmul_rn(a[i], bv[q]));
+    }
+#pragma unroll
+    for (int i = 0; i < EN_RPT; ++i) {
+      const int64_t row = r0 + rg * EN_RPT + i;
+      if (row >= m) continue;
+#pragma unroll
+      for (int q = 0; q < EN_COLS; ++q) {
+        const int c = cg * EN_COLS + q;
+        if (c < n) C[row * ldc + c] = RELU ? ((acc[i][q] > 0.0f) ? acc[i][q] : 0.0f) : acc[i][q];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------- row-sequential row folds
 // One thread per row; A staged through shared memory in 32-column slabs.
 constexpr int RF_ROWS = 128;
@@ -159,6 +258,23 @@ static int launch_gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, con
                              int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                              int64_t sA, int64_t sB, int64_t sC, cudaStream_t st,
                              Guard guard = Guard()) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (batch == 1 && guard.mode == 0 && n <= EN_MAX && k <= EN_MAX) {
+      LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_exact_narrow_kernel<RELU>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)EN_SMEM), "smem attr (narrow gemm)"));
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_exact_narrow_kernel<RELU>, 256,
+                                                    EN_SMEM);
+      int64_t blocks = (m + EN_ROWS - 1) / EN_ROWS;
+      const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+      if (blocks > cap) blocks = cap;
+      if (blocks < 1) blocks = 1;
+      gemm_exact_narrow_kernel<RELU><<<(unsigned)blocks, 256, EN_SMEM, st>>>(
+          m, (int)n, (int)k, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc);
+      return check_launch("gemm_exact_narrow_kernel");
+    }
+  }
   dim3 grid((unsigned)((n + EG_TILE - 1) / EG_TILE), (unsigned)((m + EG_TILE - 1) / EG_TILE),
             (unsigned)batch);
   if (grid.y > 65535 || grid.z > 65535) return fail(LAPIS_B200_ERR_ARG, "gemm: grid too large");

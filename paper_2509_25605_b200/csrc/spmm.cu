@@ -400,12 +400,14 @@ spmm_seq_long_pipe_kernel(int64_t k, const RP* __restrict__ rowptr,
     // colind of the loader warp's entries of the NEXT stage to issue: lane u
     // holds entry lw + 6u (one load per lane, issued a stage ahead), the
     // issuing loop broadcasts it by shuffle
-    int64_t my_col = 0;
+    // kept in the index type: widening right after the load would make the
+    // loader wait for it here instead of at its use one stage later
+    CI my_col = CI(0);
     auto load_cols = [&](int64_t s) {
       const int64_t jb = b + s * PIPE_SEQ;
       const int64_t lim = (s < nst) ? e - jb : 0;
       const int jj = lw + PIPE_LOADERS * lane;
-      my_col = (lane < CPW && jj < PIPE_SEQ && jj < lim) ? (int64_t)__ldg(colind + jb + jj) : 0;
+      my_col = (lane < CPW && jj < PIPE_SEQ && jj < lim) ? __ldg(colind + jb + jj) : CI(0);
     };
     auto issue = [&](int64_t s) {
       if (s < nst) {
@@ -418,7 +420,7 @@ spmm_seq_long_pipe_kernel(int64_t k, const RP* __restrict__ rowptr,
 #pragma unroll
         for (int u = 0; u < CPW; ++u) {
           const int jj = lw + PIPE_LOADERS * u;
-          const int64_t cu = __shfl_sync(0xffffffffu, my_col, u);
+          const int64_t cu = (int64_t)__shfl_sync(0xffffffffu, my_col, u);
           if (jj < n) {
             const float* src = X + cu * ldx + c0;
             float* dst = &xs[(slot * PIPE_SEQ + jj) * PIPE_KC];
