@@ -37,12 +37,15 @@ def nvcc() -> str | None:
     return None
 
 
-def driver_source(name: str, program, entry: str, inputs: list) -> str:
-    """C++ driver for `entry` of the (lowered) program with these inputs."""
+def driver_source(name: str, program, entry: str, inputs: list, b200_seam: bool = False) -> str:
+    """C++ driver for `entry` of the (lowered) program with these inputs.
+    ``b200_seam``: include include/lapis_b200_runtime.hpp first, so the emitted
+    LAPIS::gemm / gemv calls resolve to the B200 kernels."""
     from lapis.ir import MemRefType, func_result_types
     func = program.find_func(entry)
     params = func.region(0).args
-    lines = [f'#include "{name}.hpp"', "#include <algorithm>", "#include <cstdio>",
+    lines = (['#include "lapis_b200_runtime.hpp"'] if b200_seam else []) + [
+             f'#include "{name}.hpp"', "#include <algorithm>", "#include <cstdio>",
              "#include <fstream>", "#include <string>", "#include <vector>",
              "template <class T> static std::vector<T> slurp(const std::string& p, size_t n) {",
              "  std::vector<T> v(n ? n : 1); std::ifstream f(p, std::ios::binary);",
@@ -99,10 +102,17 @@ def driver_source(name: str, program, entry: str, inputs: list) -> str:
     return "\n".join(lines) + "\n"
 
 
-def compile_driver(src: Path, out: Path, compile_only: bool = False) -> subprocess.CompletedProcess:
+LIBDIR = ROOT / "paper_2509_25605_b200" / "lib"
+
+
+def compile_driver(src: Path, out: Path, compile_only: bool = False,
+                   b200_seam: bool = False) -> subprocess.CompletedProcess:
     cmd = [nvcc(), "-std=c++17", "-O2", "-gencode", "arch=compute_100a,code=sm_100a",
-           "--extended-lambda", "-w", f"-I{KOKKOS_B200}", f"-I{EMITTED}", "-x", "cu"]
+           "--extended-lambda", "-w", f"-I{KOKKOS_B200}", f"-I{EMITTED}", f"-I{ROOT / 'include'}",
+           "-x", "cu"]
     cmd += (["-c", str(src), "-o", str(out)] if compile_only else [str(src), "-o", str(out)])
+    if b200_seam and not compile_only:
+        cmd += [f"-L{LIBDIR}", "-llapis_b200", f"-Xlinker=-rpath,{LIBDIR}"]
     return subprocess.run(cmd, capture_output=True, text=True)
 
 

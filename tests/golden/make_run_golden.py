@@ -76,9 +76,14 @@ def main() -> None:
     OUT.mkdir(exist_ok=True)
     sources = [(p.stem, p) for p in sorted((REF / "tests" / "fixtures").glob("*.mlir"))]
     sources += [("ir_" + p.stem, p) for p in sorted(IR.glob("*.mlir"))]
-    for name, path in sources:
+    # the kernel-library route (kokkos.gemm / gemv -> LAPIS::gemm / gemv) of the dense programs
+    kl = [("kl_" + n, p) for n, p in sources if n in ("matmul_f64", "matmul_i32", "matvec_f64",
+                                                      "ir_matmul_f32", "ir_matmul_f64",
+                                                      "ir_matvec_f64")]
+    for name, path in sources + kl:
         program = parse_file(str(path))
-        lowered = run_pipeline(program, PassPipeline.preset(), TargetConfig()).program
+        cfg = TargetConfig(kernel_library_calls=True) if name.startswith("kl_") else TargetConfig()
+        lowered = run_pipeline(program, PassPipeline.preset(), cfg).program
         entry = program.funcs()[0].attrs["sym_name"]
         (OUT / f"{name}.lowered.mlir").write_text(print_program(lowered))
         (OUT / f"{name}.orig.mlir").write_text(print_program(program))

@@ -27,21 +27,27 @@ needs_build = pytest.mark.skipif(not CASES or D.nvcc() is None,
                                  reason="emitted C++ not built (oracle/_ref/emitted) or no nvcc")
 
 
+def _seam(name: str) -> bool:
+    # kernel-library route: LAPIS::gemm / gemv through include/lapis_b200_runtime.hpp
+    return name.startswith("kl_")
+
+
 def _prepare(name: str, d: Path):
     case = load_run_case(f"{name}.b")
     program = lapis_parser.parse(case["lowered"])
     src = d / f"{name}.cu"
     inputs = D.coerce_inputs(program, case["entry"], case["inputs"])
-    src.write_text(D.driver_source(name, program, case["entry"], inputs))
+    src.write_text(D.driver_source(name, program, case["entry"], inputs, b200_seam=_seam(name)))
     D.write_inputs(d, inputs)
     return case, src
 
 
 @needs_build
-@pytest.mark.parametrize("name", [n for n in ("spmv", "team_single_barrier", "globals") if n in CASES])
+@pytest.mark.parametrize("name", [n for n in ("spmv", "team_single_barrier", "globals",
+                                              "kl_matmul_f64") if n in CASES])
 def test_emitted_cpp_compiles_for_sm100a(name, tmp_path):
     _, src = _prepare(name, tmp_path)
-    r = D.compile_driver(src, tmp_path / f"{name}.o", compile_only=True)
+    r = D.compile_driver(src, tmp_path / f"{name}.o", compile_only=True, b200_seam=_seam(name))
     assert r.returncode == 0, r.stderr[-3000:]
 
 
@@ -56,7 +62,7 @@ def built():
         d.mkdir()
         case, src = _prepare(name, d)
         exe = d / "drv"
-        r = D.compile_driver(src, exe)
+        r = D.compile_driver(src, exe, b200_seam=_seam(name))
         return name, (case, d, exe, r)
 
     with cf.ThreadPoolExecutor(8) as ex:
@@ -72,6 +78,12 @@ def test_emitted_cpp_runs_on_b200(name, built, cuda_device):
     from lapis.interp import diff_outputs
     case, d, exe, r = built[name]
     assert r.returncode == 0, r.stderr[-3000:]
+    if _seam(name):
+        # the emitted LAPIS::gemm / gemv bound to the B200 kernels, not the
+        # runtime header's generic templates
+        syms = subprocess.run(["nm", "-D", "--undefined-only", str(exe)], capture_output=True,
+                              text=True).stdout
+        assert "lapis_b200_gemm" in syms or "lapis_b200_gemv" in syms, syms[-500:]
     run = subprocess.run([str(exe), str(d)], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stderr[-2000:]
     want = np.asarray(case["outputs"][0])
