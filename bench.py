@@ -316,6 +316,81 @@ class StencilSpmv(Workload):
         return yref, got, times, work, desc, 1e-12
 
 
+class MtxSpmv(Workload):
+    """CSR SpMV fp64 on a Matrix Market file (--mtx; the paper's SuiteSparse
+    runs): read natively (paper_2509_25605_b200/mmio.py),
+    planned once, x U(-1,1) seed 7.  N > 1: independent replicas."""
+
+    scaling = "weak"
+
+    data = "matrix market file (--mtx), x seeded"
+
+    def __init__(self, args, rank, world):
+        import paper_2509_25605_b200 as lb
+        from paper_2509_25605_b200 import mmio
+        if not args.mtx:
+            raise SystemExit("--workload mtx needs --mtx <file.mtx>")
+        self.lb, self.args, self.world, self.path = lb, args, world, args.mtx
+        rp, ci, v, (self.N, self.ncols) = mmio.read_matrix_market(args.mtx)
+        self.rowptr, self.colind, self.values = mmio.to_device(rp, ci, v)
+        self.nnz = int(rp[-1])
+        self.stream = torch.cuda.current_stream()
+        self.x_host = np.random.default_rng(7).uniform(-1.0, 1.0, self.ncols)
+        self.x = torch.from_numpy(self.x_host).cuda()
+        self.y = torch.empty(self.N, dtype=torch.float64, device="cuda")
+        self.plan = lb.CsrPlan(self.rowptr, nnz=self.nnz)
+        if self.work_local() < (512 << 20):
+            self.flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+
+    @property
+    def name(self):
+        return f"matrix market SpMV fp64: {Path(self.path).name}"
+
+    def config(self):
+        return {"workload": self.name, "rows": self.N, "cols": self.ncols, "nnz": self.nnz,
+                "index_layout": "rowptr int64, colind int32", "parallelism": "replica",
+                "l2": "L2 flushed between steps" if self.flush is not None else "inputs > L2"}
+
+    def work_local(self):
+        return self.nnz * 12 + (self.N + 1) * 8 + self.ncols * 8 + self.N * 8
+
+    def work_global(self):
+        return self.work_local() * self.world
+
+    def kernel_name(self):
+        return self.plan.info()["kernel"] + " <double,int64,int32>"
+
+    def step(self):
+        self.plan.spmv(self.colind, self.values, self.x, self.y, stream=self.stream)
+
+    def e2e(self, steps, warmup):
+        from paper_2509_25605_b200.dualview import DualView
+        from paper_2509_25605_b200.streamed import StreamedSpmv
+        xs = DualView.from_host(self.x_host, "x", device_buffer=self.x)
+        ys = DualView.allocate((self.N,), torch.float64, "y")
+        op = StreamedSpmv(self.rowptr, self.colind, self.values, self.ncols)
+
+        def one():
+            xs.modify_host()
+            op.multiply(xs, ys, stream=self.stream)
+
+        return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
+
+    def cpu_reference(self, rows_sample, threads, reps):
+        from oracle import ref as R
+        rp = self.rowptr.cpu().numpy()
+        b = min(self.N, rows_sample)
+        e0, e1 = int(rp[0]), int(rp[b])
+        ci = self.colind[e0:e1].cpu().numpy().astype(np.int64)
+        v = self.values[e0:e1].cpu().numpy()
+        yref, times = R.spmv_csr(rp[:b + 1] - e0, ci, v, self.x_host, reps=reps, threads=threads)
+        work = (e1 - e0) * 12 + (b + 1) * 8 + b * 8 * 2
+        desc = (f"rows [0, {b}) ({e1 - e0} nnz): reference emitted Kokkos C++ on its serial "
+                f"stub, {threads} row blocks")
+        return yref, self.y[:b].cpu().numpy(), times, work, desc, 1e-12
+
+
 class PowerLawSpmm(Workload):
     """Config 3: CSR x dense SpMM fp64, K = 64, Chung-Lu power-law matrix."""
 
@@ -618,6 +693,7 @@ WORKLOADS = {
     "c2f32": lambda args, r, w: DenseMatmul(args, r, w, torch.float32, args.n or 4096),
     "c2f64": lambda args, r, w: DenseMatmul(args, r, w, torch.float64, args.n or 4096),
     "c4": lambda args, r, w: GcnLayer(args, r, w, args.n or 1_000_000),
+    "mtx": lambda args, r, w: MtxSpmv(args, r, w),
 }
 
 
@@ -687,6 +763,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--vl", type=int, default=0,
                     help="SpMV: time the emitted-mapping vector kernel with this vector length")
+    ap.add_argument("--mtx", default="", help="Matrix Market file for --workload mtx")
     ap.add_argument("--gemm-mode", default="auto", choices=["auto", "tf32x3", "dmma", "exact", "ozaki"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -755,7 +832,7 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": wl.unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
         "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype,
-        "data": "synthetic (device-generated inputs, seeded)",
+        "data": getattr(wl, "data", "synthetic (device-generated inputs, seeded)"),
         "config": wl.config(),
         "roofline": ({**override, "traffic": traffic, "kernel": wl.kernel_name(),
                       "algorithmic_work_per_launch": wl.work_local()} if override else

@@ -183,6 +183,19 @@ int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz,
 int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,
                              int64_t* rowptr, int32_t* colind, double* values, void* stream);
 
+/* ------------------------------------------------------- on-disk inputs
+ * Matrix Market coordinate files (the paper's SuiteSparse matrices,
+ * PAPER.md:349-376) read straight into host CSR, in
+ * parallel.  Host-only (no device needed).  mm_info: out4 = {nrows, ncols,
+ * nnz after symmetric expansion, flags (bit 0 pattern, bit 1 integer,
+ * bits 2-3: 0 general, 1 symmetric, 2 skew-symmetric, 3 hermitian)}.
+ * mm_read_csr fills rowptr [nrows + 1] (int64), colind [nnz] (4- or 8-byte),
+ * values [nnz] (f64, may be NULL): rows sorted by column, symmetric storage
+ * mirrored (skew: negated). */
+int lapis_b200_mm_info(const char* path, int64_t* out4);
+int lapis_b200_mm_read_csr(const char* path, int64_t* rowptr, void* colind, int colind_bytes,
+                           double* values);
+
 /* ------------------------------------------------------- generated kernels
  * The reference turns every kokkos.{range,thread,team}_parallel nest into a
  * Kokkos parallel_for / parallel_reduce lambda (emitter.py:596-780) compiled

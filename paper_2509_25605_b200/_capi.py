@@ -58,6 +58,9 @@ _SIGNATURES = {
     "lapis_b200_synth_stencil": ([_INT, _I64, _I64, _I64, _VP, _VP, _VP, _VP], _INT),
     "lapis_b200_csr_check": ([_I64, _VP, _INT, _VP, _INT, _I64, _I64, C.POINTER(_I64), _VP],
                              _INT),
+    "lapis_b200_mm_info": ([C.c_char_p, C.POINTER(_I64)], _INT),
+    "lapis_b200_mm_read_csr": ([C.c_char_p, C.POINTER(_I64), _VP, _INT, C.POINTER(C.c_double)],
+                               _INT),
     "lapis_b200_jit_available": ([], _INT),
     "lapis_b200_jit_compile": ([C.c_char_p, C.c_char_p, C.POINTER(_VP)], _INT),
     "lapis_b200_jit_launch": ([_VP, _I64, _INT, _INT, _VP, _I64, _VP], _INT),
