@@ -67,7 +67,40 @@ struct OzParams {
   bool vec2;                // 16-byte partial accesses (even pitch, aligned)
   unsigned long long* prof; // optional: wait-cycle counters (LAPIS_B200_OZAKI_PROF=1)
   int digits8;              // 1: signed 8-bit leading digit + unsigned 8-bit digits
+  // last-wave split (tiles >= split_base): the owner CTA runs the diagonals in
+  // owner_mask (always the last one), a helper CTA the rest into its own fp64
+  // tile in `split_ws` and raises one flag per epilogue warp; the owner adds
+  // that tile before its last diagonal
+  int split_base, nsplit;
+  uint32_t owner_mask, helper_mask;
+  double* split_ws;         // [nsplit][OZ_BM][BN]
+  int* split_flag;          // [nsplit][OZ_EPI_WARPS], zeroed per call
 };
+
+// Work item k of this CTA: whole tiles blockIdx.x + k * gridDim.x below
+// split_base (a multiple of gridDim.x), then at most one half of a split tile.
+struct OzItem {
+  int tile, role, slot;     // role 0 whole, 1 owner, 2 helper
+  uint32_t mask;            // diagonals this item runs
+};
+__device__ __forceinline__ bool oz_item(const OzParams& p, int k, OzItem& it) {
+  const int t = blockIdx.x + k * gridDim.x;
+  if (t < p.split_base) {
+    it.tile = t; it.role = 0; it.slot = 0; it.mask = (1u << p.S) - 1u;
+    return true;
+  }
+  if (k * (int)gridDim.x != p.split_base || (int)blockIdx.x >= 2 * p.nsplit) return false;
+  it.slot = blockIdx.x >> 1;
+  it.tile = p.split_base + it.slot;
+  it.role = 1 + (blockIdx.x & 1);
+  it.mask = it.role == 1 ? p.owner_mask : p.helper_mask;
+  return true;
+}
+__device__ __forceinline__ int ld_acquire(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                           uint32_t idesc, uint32_t accumulate) {
@@ -85,11 +118,93 @@ __host__ __device__ constexpr uint32_t i8_idesc(int M, int N, bool a_signed = tr
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// x * 2^e, exact: one multiply by a constructed power of two in the normal
-// range (scalbn for the rest)
+// x * 2^e for an integer-valued x (|x| < 2^31), correctly rounded like scalbn,
+// branch-free: two multiplies by constructed powers of two, the first clamped
+// to the normal range (exact for such x), the second carrying the rest (1.0
+// for every in-range e).  Branch-free keeps the unrolled epilogues small enough
+// for the instruction cache (an inlined scalbn per element does not fit).
 __device__ __forceinline__ double pow2_scale(double x, int e) {
-  if (e >= -1022 && e <= 1023) return x * __hiloint2double((e + 1023) << 20, 0);
-  return scalbn(x, e);
+  const int e1 = min(max(e, -1022), 1023);
+  const int e2 = min(max(e - e1, -1022), 1023);
+  return x * __hiloint2double((e1 + 1023) << 20, 0) * __hiloint2double((e2 + 1023) << 20, 0);
+}
+
+// Drain one s32 diagonal of this warp's 32 x HALF accumulator slice: scale by
+// 2^(shift + eb_j), add to the fp64 partial at pbase (the output / fp32
+// workspace with pitch ldp, or a helper's tile with pitch OZ_BN) and, for the
+// last diagonal, certify and write C.
+template <class OUT, int OZ_BN, bool HELPER>
+__device__ __forceinline__ void oz_drain(const OzParams& p, double* wsm, uint32_t tbase, int row_base,
+                                         int col0, int shift, bool read_old, bool last,
+                                         double* pbase) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int c0 = 0; c0 < OzTile<OZ_BN>::HALF; c0 += 16) {
+    uint32_t v[16];
+    tmem_ld_x16(tbase + (uint32_t)c0, v);
+    const int cb = col0 + c0;
+    // scale this thread's row segment, then transpose it through the
+    // warp's shared tile (16-byte pairs XOR-swizzled by row) so that the
+    // partial's read-modify-write is 4 rows x 128 B per instruction
+#pragma unroll
+    for (int pq = 0; pq < 8; ++pq) {
+      const int q = 2 * pq;
+      const int e0 = (cb + q < p.n) ? __ldg(p.eb + cb + q) : 0;
+      const int e1 = (cb + q + 1 < p.n) ? __ldg(p.eb + cb + q + 1) : 0;
+      const double x0 = pow2_scale((double)(int)v[q], shift + e0);
+      const double x1 = pow2_scale((double)(int)v[q + 1], shift + e1);
+      *reinterpret_cast<double2*>(wsm + lane * 16 + 2 * (pq ^ (lane & 7))) = make_double2(x0, x1);
+    }
+    __syncwarp();
+    double2 t[8];
+    const int pq = lane & 7;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 4 * i + (lane >> 3);
+      t[i] = *reinterpret_cast<const double2*>(wsm + r * 16 + 2 * (pq ^ (r & 7)));
+    }
+    __syncwarp();
+    const int gc = cb + 2 * pq;
+    double2 old[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gr = row_base + 4 * i + (lane >> 3);
+      old[i] = make_double2(0.0, 0.0);
+      if (read_old && gr < p.m) {
+        const double* src = pbase + (int64_t)gr * (HELPER ? OZ_BN : p.ldp) + gc;
+        if (p.vec2 && gc + 1 < p.n) old[i] = *reinterpret_cast<const double2*>(src);
+        else {
+          if (gc < p.n) old[i].x = src[0];
+          if (gc + 1 < p.n) old[i].y = src[1];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gr = row_base + 4 * i + (lane >> 3);
+      if (gr >= p.m) continue;
+      const double y0 = t[i].x + old[i].x, y1 = t[i].y + old[i].y;
+      if (!HELPER && last) {
+        // certify |y - exact| <= cert_tol * max(|y|, 1) from the a-priori bound
+        const int er = __ldg(p.ea + gr);
+        const double b0 = pow2_scale(p.cert_k, er + (gc < p.n ? __ldg(p.eb + gc) : 0));
+        const double b1 = pow2_scale(p.cert_k, er + (gc + 1 < p.n ? __ldg(p.eb + gc + 1) : 0));
+        if ((gc < p.n && b0 > p.cert_tol * fmax(fabs(y0), 1.0)) ||
+            (gc + 1 < p.n && b1 > p.cert_tol * fmax(fabs(y1), 1.0)))
+          atomicExch(p.flag + 1, 1);
+        OUT* dst = reinterpret_cast<OUT*>(p.C) + (int64_t)gr * p.ldc + gc;
+        if (gc < p.n) dst[0] = (OUT)y0;
+        if (gc + 1 < p.n) dst[1] = (OUT)y1;
+      } else {
+        double* dst = pbase + (int64_t)gr * (HELPER ? OZ_BN : p.ldp) + gc;
+        if (p.vec2 && gc + 1 < p.n) *reinterpret_cast<double2*>(dst) = make_double2(y0, y1);
+        else {
+          if (gc < p.n) dst[0] = y0;
+          if (gc + 1 < p.n) dst[1] = y1;
+        }
+      }
+    }
+  }
 }
 
 template <class OUT, int OZ_BN>
@@ -102,7 +217,6 @@ gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant_
   __shared__ uint64_t full[OZ_STAGES], empty[OZ_STAGES], tmem_full[2], tmem_empty[2];
   __shared__ uint32_t tmem_base_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = p.num_m * p.num_n;
   const int S = p.S;
 
   if (warp == 0 && lane == 0) {
@@ -131,9 +245,11 @@ gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant_
       int stage = 0;
       uint32_t phase = 0;
       long long prod_wait = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int mb = tile % p.num_m, nb = tile / p.num_m;
+      OzItem it;
+      for (int k = 0; oz_item(p, k, it); ++k) {
+        const int mb = it.tile % p.num_m, nb = it.tile / p.num_m;
         for (int d = 0; d < S; ++d)
+          if ((it.mask >> d) & 1u)
           for (int s = 0; s <= d; ++s)
             for (int kb = 0; kb < p.nk; ++kb) {
               const long long t0 = p.prof ? clock64() : 0;
@@ -162,8 +278,10 @@ gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant_
       uint32_t acc_phase = 0;
       long long w_tmem = 0, w_full = 0;
       const long long t_start = clock64();
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      OzItem it;
+      for (int k = 0; oz_item(p, k, it); ++k) {
         for (int d = 0; d < S; ++d) {
+          if (!((it.mask >> d) & 1u)) continue;
           long long t0 = p.prof ? clock64() : 0;
           mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
           if (p.prof) w_tmem += clock64() - t0;
@@ -211,13 +329,20 @@ gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant_
     const int half = ew >> 2;                // columns [128*half, 128*half + 128)
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int mb = tile % p.num_m, nb = tile / p.num_m;
+    OzItem it;
+    for (int k = 0; oz_item(p, k, it); ++k) {
+      const int mb = it.tile % p.num_m, nb = it.tile / p.num_m;
       const int row_base = mb * OZ_BM + lg * 32;
+      // a helper accumulates into its own tile (pitch OZ_BN), indexed by the
+      // output's row / column
+      double* const hbase = p.split_ws + (int64_t)it.slot * OZ_BM * OZ_BN -
+                            (int64_t)mb * OZ_BM * OZ_BN - nb * OZ_BN;
+      const int d_first = __ffs(it.mask) - 1, d_last = 31 - __clz(it.mask);
       const int row = row_base + lane;
       const int col0 = nb * OZ_BN + half * OzTile<OZ_BN>::HALF;
       const int ea = row < p.m ? p.ea[row] : 0;
       for (int d = 0; d < S; ++d) {
+        if (!((it.mask >> d) & 1u)) continue;
         const long long t0 = (p.prof && threadIdx.x == 64) ? clock64() : 0;
         mbar_wait(&tmem_full[acc], acc_phase);
         if (p.prof && threadIdx.x == 64) atomicAdd(p.prof + 4, (unsigned long long)(clock64() - t0));
@@ -225,77 +350,280 @@ gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant_
         const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) +
                                (uint32_t)(acc * OZ_BN + half * OzTile<OZ_BN>::HALF);
         const int shift = p.digits8 ? ea - 14 - 8 * d : ea - 7 * (d + 2);
-        const bool last = d == S - 1;
-#pragma unroll 1
-        for (int c0 = 0; c0 < OzTile<OZ_BN>::HALF; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld_x16(tbase + (uint32_t)c0, v);
-          const int cb = col0 + c0;
-          // scale this thread's row segment, then transpose it through the
-          // warp's shared tile (16-byte pairs XOR-swizzled by row) so that the
-          // partial's read-modify-write is 4 rows x 128 B per instruction
-#pragma unroll
-          for (int pq = 0; pq < 8; ++pq) {
-            const int q = 2 * pq;
-            const int e0 = (cb + q < p.n) ? __ldg(p.eb + cb + q) : 0;
-            const int e1 = (cb + q + 1 < p.n) ? __ldg(p.eb + cb + q + 1) : 0;
-            const double x0 = pow2_scale((double)(int)v[q], shift + e0);
-            const double x1 = pow2_scale((double)(int)v[q + 1], shift + e1);
-            *reinterpret_cast<double2*>(wsm + lane * 16 + 2 * (pq ^ (lane & 7))) = make_double2(x0, x1);
-          }
-          __syncwarp();
-          double2 t[8];
-          const int pq = lane & 7;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = 4 * i + (lane >> 3);
-            t[i] = *reinterpret_cast<const double2*>(wsm + r * 16 + 2 * (pq ^ (r & 7)));
-          }
-          __syncwarp();
-          const int gc = cb + 2 * pq;
-          double2 old[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int gr = row_base + 4 * i + (lane >> 3);
-            old[i] = make_double2(0.0, 0.0);
-            if (d > 0 && gr < p.m) {
-              const double* src = p.part + (int64_t)gr * p.ldp + gc;
-              if (p.vec2 && gc + 1 < p.n) old[i] = *reinterpret_cast<const double2*>(src);
-              else {
-                if (gc < p.n) old[i].x = src[0];
-                if (gc + 1 < p.n) old[i].y = src[1];
+        const bool last = d == d_last && it.role != 2;
+        if (last && it.role == 1) {
+          // owner: add the helper's tile into the partial first (a plain pass;
+          // it is the only partial when the owner runs a single diagonal)
+          const int* f = p.split_flag + it.slot * OZ_EPI_WARPS + ew;
+          while (ld_acquire(f) == 0) __nanosleep(128);   // every lane acquires
+          const double* hws = p.split_ws + (int64_t)it.slot * OZ_BM * OZ_BN + (lg * 32) * OZ_BN +
+                              half * OzTile<OZ_BN>::HALF;
+          for (int r = 0; r < 32; ++r) {
+            const int gr = row_base + r;
+            if (gr >= p.m) break;
+            for (int c = lane; c < OzTile<OZ_BN>::HALF; c += 32) {
+              const int gc = col0 + c;
+              if (gc < p.n) {
+                double* dst = p.part + (int64_t)gr * p.ldp + gc;
+                *dst = (d == d_first ? 0.0 : *dst) + hws[r * OZ_BN + c];
               }
             }
           }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int gr = row_base + 4 * i + (lane >> 3);
-            if (gr >= p.m) continue;
-            const double y0 = t[i].x + old[i].x, y1 = t[i].y + old[i].y;
-            if (last) {
-              // certify |y - exact| <= cert_tol * max(|y|, 1) from the a-priori bound
-              const int er = __ldg(p.ea + gr);
-              const double b0 = pow2_scale(p.cert_k, er + (gc < p.n ? __ldg(p.eb + gc) : 0));
-              const double b1 = pow2_scale(p.cert_k, er + (gc + 1 < p.n ? __ldg(p.eb + gc + 1) : 0));
-              if ((gc < p.n && b0 > p.cert_tol * fmax(fabs(y0), 1.0)) ||
-                  (gc + 1 < p.n && b1 > p.cert_tol * fmax(fabs(y1), 1.0)))
-                atomicExch(p.flag + 1, 1);
-              OUT* dst = reinterpret_cast<OUT*>(p.C) + (int64_t)gr * p.ldc + gc;
-              if (gc < p.n) dst[0] = (OUT)y0;
-              if (gc + 1 < p.n) dst[1] = (OUT)y1;
-            } else {
-              double* dst = p.part + (int64_t)gr * p.ldp + gc;
-              if (p.vec2 && gc + 1 < p.n) *reinterpret_cast<double2*>(dst) = make_double2(y0, y1);
-              else {
-                if (gc < p.n) dst[0] = y0;
-                if (gc + 1 < p.n) dst[1] = y1;
-              }
-            }
-          }
+          __syncwarp();
+        }
+        const bool read_old = d != d_first || (last && it.role == 1);
+        const long long t1 = (p.prof && threadIdx.x == 64) ? clock64() : 0;
+        if (it.role == 2)
+          oz_drain<OUT, OZ_BN, true>(p, wsm, tbase, row_base, col0, shift, read_old, false, hbase);
+        else
+          oz_drain<OUT, OZ_BN, false>(p, wsm, tbase, row_base, col0, shift, read_old, last, p.part);
+        if (p.prof && threadIdx.x == 64) {
+          atomicAdd(p.prof + 5, (unsigned long long)(clock64() - t1));
+          atomicAdd(p.prof + 6, 1ull);
         }
         tc_fence_before();
         mbar_arrive(&tmem_empty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (it.role == 2 && d == d_last) {
+          // publish this warp's rows of the helper tile to the owner
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(p.split_flag + it.slot * OZ_EPI_WARPS + ew, 1);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(tmem_base), "r"(OZ_TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------- two-pass kernel
+// fp64, S = 8: the diagonals' s32 accumulators live in TMEM four at a time
+// (4 x 128 columns), so each K block's digit tiles are loaded ONCE and feed
+// every slice product of a pass:
+//   pass A  diagonals 0-3: digits 0-3 of A and B, 10 products per K block
+//   pass B  diagonals 4-7: digits 0-7,            26 products per K block
+// against S(S+1)/2 = 36 re-streamed tile pairs per K block in the
+// per-diagonal kernel above, whose operand stream is L2->SM bound.  A stage
+// is 64 KB: two K blocks of 4+4 digit tiles (pass A) or one K block of 8+8
+// (pass B), each digit tile 128 x 32 int8 (SWIZZLE_32B, one 3-D TMA box per
+// 4 digits).  The epilogue folds pass A's diagonals into an fp64 partial kept
+// in a per-CTA L2-resident slot, then adds pass B's in ascending d — the
+// per-diagonal kernel's summation order, so both kernels give identical bits.
+constexpr int OZ2_BN = 128, OZ2_BK = 32, OZ2_STAGES = 3;
+constexpr uint32_t OZ2_DIGIT = 128 * OZ2_BK;                 // 4 KB
+constexpr uint32_t OZ2_STAGE = 16 * OZ2_DIGIT;               // 64 KB
+constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + OZ_EPI_SMEM + 1024;
+constexpr int OZ2_SLOT = 8 * 4 * 16 * 32;                    // doubles per CTA partial (128 KB)
+
+template <class OUT>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                     OzParams p) {
+  if (*p.flag) return;  // uniform: the guarded fallback owns this call
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[OZ2_STAGES], empty[OZ2_STAGES], acc_full, acc_empty;
+  __shared__ uint32_t tmem_base_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = p.num_m * p.num_n;
+  const int nk = p.nk, nk2 = (p.nk + 1) / 2;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tA);
+    prefetch_tmap(&tB);
+    for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, OZ_EPI_WARPS * 32);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&tmem_base_slot)), "r"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int ma = (tile % p.num_m) * OZ_BM, nbn = (tile / p.num_m) * OZ2_BN;
+        for (int j = 0; j < nk2; ++j) {            // pass A: K blocks 2j, 2j+1 (zero-filled past K)
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * OZ2_STAGE;
+          mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
+          for (int h = 0; h < 2; ++h) {
+            tma_load_3d(sa + h * 8 * OZ2_DIGIT, &tA, (2 * j + h) * OZ2_BK, ma, 0, &full[stage]);
+            tma_load_3d(sa + h * 8 * OZ2_DIGIT + 4 * OZ2_DIGIT, &tB, (2 * j + h) * OZ2_BK, nbn, 0, &full[stage]);
+          }
+          if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        for (int kb = 0; kb < nk; ++kb) {          // pass B: one K block, all 8 digits
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * OZ2_STAGE;
+          mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
+          tma_load_3d(sa, &tA, kb * OZ2_BK, ma, 0, &full[stage]);
+          tma_load_3d(sa + 4 * OZ2_DIGIT, &tA, kb * OZ2_BK, ma, 4, &full[stage]);
+          tma_load_3d(sa + 8 * OZ2_DIGIT, &tB, kb * OZ2_BK, nbn, 0, &full[stage]);
+          tma_load_3d(sa + 12 * OZ2_DIGIT, &tB, kb * OZ2_BK, nbn, 4, &full[stage]);
+          if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // (the whole warp runs the loop, one elected lane issues)
+    constexpr uint32_t idesc = i8_idesc(OZ_BM, OZ2_BN, true, true);
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    long long w_tmem = 0, w_full = 0;
+    const long long t_start = clock64();
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      for (int pass = 0; pass < 2; ++pass) {
+        long long t0 = p.prof ? clock64() : 0;
+        mbar_wait(&acc_empty, acc_phase ^ 1);
+        if (p.prof) w_tmem += clock64() - t0;
+        acc_phase ^= 1;
+        tc_fence_after();
+        const int nstage = pass == 0 ? nk2 : nk;
+        for (int j = 0; j < nstage; ++j) {
+          t0 = p.prof ? clock64() : 0;
+          mbar_wait(&full[stage], phase);
+          if (p.prof) w_full += clock64() - t0;
+          tc_fence_after();
+          const uint64_t desc0 = smem_desc_sw32(smem + stage * OZ2_STAGE);
+          if (elect_one()) {
+            if (pass == 0) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int d = 0; d < 4; ++d)
+#pragma unroll
+                  for (int s = 0; s <= d; ++s)
+                    tc_mma_i8(tmem_base + (uint32_t)(d * OZ2_BN),
+                              desc0 + (uint64_t)(((h * 8 + s) * OZ2_DIGIT) >> 4),
+                              desc0 + (uint64_t)(((h * 8 + 4 + d - s) * OZ2_DIGIT) >> 4), idesc,
+                              (j > 0 || h > 0 || s > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int d = 4; d < 8; ++d)
+#pragma unroll
+                for (int s = 0; s <= d; ++s)
+                  tc_mma_i8(tmem_base + (uint32_t)((d - 4) * OZ2_BN),
+                            desc0 + (uint64_t)((s * OZ2_DIGIT) >> 4),
+                            desc0 + (uint64_t)(((8 + d - s) * OZ2_DIGIT) >> 4), idesc,
+                            (j > 0 || s > 0) ? 1u : 0u);
+            }
+            tc_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) tc_commit(&acc_full);
+        __syncwarp();
+      }
+    }
+    if (p.prof && lane == 0) {
+      atomicAdd(p.prof + 1, (unsigned long long)w_tmem);
+      atomicAdd(p.prof + 2, (unsigned long long)w_full);
+      atomicAdd(p.prof + 3, (unsigned long long)(clock64() - t_start));
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const int ew = warp - 2;                 // 0..7
+    const int lg = warp & 3;                 // TMEM lane group this warp may access
+    const int half = ew >> 2;                // columns [64*half, 64*half + 64)
+    double* wsm = reinterpret_cast<double*>(smem + OZ2_STAGES * OZ2_STAGE) + ew * 32 * 16;
+    // this warp's partial in the CTA's slot: [chunk][j][lane], coalesced per j
+    double* slot = p.split_ws + (int64_t)blockIdx.x * OZ2_SLOT + ew * (4 * 16 * 32) + lane;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int mb = tile % p.num_m, nb = tile / p.num_m;
+      const int row_base = mb * OZ_BM + lg * 32;
+      const int row = row_base + lane;
+      const int ea = row < p.m ? __ldg(p.ea + row) : 0;
+      const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(half * 64);
+      for (int pass = 0; pass < 2; ++pass) {
+        mbar_wait(&acc_full, acc_phase);
+        acc_phase ^= 1;
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          const int cb = nb * OZ2_BN + half * 64 + c * 16;
+          int e[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) e[j] = (cb + j < p.n) ? __ldg(p.eb + cb + j) : 0;
+          double y[16];
+          if (pass == 1) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) y[j] = slot[(c * 16 + j) * 32];
+          }
+#pragma unroll 1
+          for (int q = 0; q < 4; ++q) {
+            const int d = pass * 4 + q;
+            uint32_t v[16];
+            tmem_ld_x16(tbase + (uint32_t)(q * OZ2_BN + c * 16), v);
+            const int shift = ea - 7 * (d + 2);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const double x = pow2_scale((double)(int)v[j], shift + e[j]);
+              y[j] = d == 0 ? x : x + y[j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) slot[(c * 16 + j) * 32] = y[j];
+        }
+        // every accumulator read: the next pass's MMAs may start
+        tc_fence_before();
+        mbar_arrive(&acc_empty);
+      }
+      // final: certify and write C through the shared transpose (4 rows x 16
+      // columns per store instruction)
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        const int cb = nb * OZ2_BN + half * 64 + c * 16;
+        bool bad = false;
+#pragma unroll
+        for (int pq = 0; pq < 8; ++pq) {
+          const double y0 = slot[(c * 16 + 2 * pq) * 32], y1 = slot[(c * 16 + 2 * pq + 1) * 32];
+          const int c0 = cb + 2 * pq;
+          if (row < p.m) {
+            bad |= c0 < p.n && pow2_scale(p.cert_k, ea + __ldg(p.eb + c0)) > p.cert_tol * fmax(fabs(y0), 1.0);
+            bad |= c0 + 1 < p.n &&
+                   pow2_scale(p.cert_k, ea + __ldg(p.eb + c0 + 1)) > p.cert_tol * fmax(fabs(y1), 1.0);
+          }
+          *reinterpret_cast<double2*>(wsm + lane * 16 + 2 * (pq ^ (lane & 7))) = make_double2(y0, y1);
+        }
+        if (bad) atomicExch(p.flag + 1, 1);
+        __syncwarp();
+        const int pq = lane & 7;
+        const int gc = cb + 2 * pq;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = 4 * i + (lane >> 3);
+          const double2 t = *reinterpret_cast<const double2*>(wsm + r * 16 + 2 * (pq ^ (r & 7)));
+          const int gr = row_base + r;
+          if (gr >= p.m) continue;
+          OUT* dst = reinterpret_cast<OUT*>(p.C) + (int64_t)gr * p.ldc + gc;
+          if (p.vec2 && gc + 1 < p.n) {
+            *reinterpret_cast<double2*>(dst) = t;
+          } else {
+            if (gc < p.n) dst[0] = (OUT)t.x;
+            if (gc + 1 < p.n) dst[1] = (OUT)t.y;
+          }
+        }
+        __syncwarp();
       }
     }
   }
@@ -463,6 +791,21 @@ static int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64
   return LAPIS_B200_OK;
 }
 
+// S digit planes [S][rows][kp] as one 3-D map: box {32, box_rows, box_digits}, SWIZZLE_32B
+static int make_i8_map3(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t kp, int S,
+                        uint32_t box_rows, uint32_t box_digits) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)S};
+  const cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(rows * kp)};
+  const cuuint32_t box[3] = {32u, box_rows, box_digits};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled (int8, 3-D) failed");
+  return LAPIS_B200_OK;
+}
 
 // Digits per operand for a k-deep product, 0 when the scheme cannot certify
 // the contract for unit-scale data (or s32 accumulation would overflow):
@@ -478,7 +821,23 @@ int ozaki_slices_for(int dtype, int64_t k) {
   return 0;
 }
 
-template <class T, int BN>
+static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& prm,
+                           int grid, cudaStream_t st) {
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_ozaki_2p_kernel<double>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ2_SMEM),
+                      "smem attr (gemm_ozaki_2p_kernel)"));
+    configured_dev = dev;
+  }
+  gemm_ozaki_2p_kernel<double><<<grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, prm);
+  return check_launch("gemm_ozaki_2p_kernel");
+}
+
+// TWO_PASS: the two-pass kernel (fp64, S = 8, BN = 128)
+template <class T, int BN, bool TWO_PASS = false>
 static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
                         int64_t sC, int S, cudaStream_t st) {
@@ -499,37 +858,71 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured_dev != dev) {
-    LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_ozaki_kernel<T, BN>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)OzTile<BN>::SMEM),
-                      "smem attr (gemm_ozaki_kernel)"));
-    configured_dev = dev;
+  if constexpr (!TWO_PASS) {
+    if (configured_dev != dev) {
+      LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_ozaki_kernel<T, BN>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)OzTile<BN>::SMEM),
+                        "smem attr (gemm_ozaki_kernel)"));
+      configured_dev = dev;
+    }
   }
   const int64_t kp = (k + 15) / 16 * 16;
   const int64_t mp = (m + OZ_BM - 1) / OZ_BM * OZ_BM, np = (n + BN - 1) / BN * BN;
   // workspace: digits of A and B, exponents, column maxima, flag, fp32 partials
   const size_t a_bytes = (size_t)S * mp * kp, b_bytes = (size_t)S * np * kp;
-  const size_t part_bytes = std::is_same<T, float>::value ? (size_t)m * n * sizeof(double) : 0;
+  const size_t part_bytes = (std::is_same<T, float>::value && !TWO_PASS) ? (size_t)m * n * sizeof(double) : 0;
   const size_t meta = (size_t)(m + n) * sizeof(int) + (size_t)n * 8 + 64 + 8;
+  // last-wave split: with R tiles left after the full waves and 2R <= #SMs,
+  // each of them is cut in two halves of about equal int8 work
+  const int num_m_t = (int)(mp / OZ_BM), num_n_t = (int)(np / BN);
+  const int tiles = num_m_t * num_n_t, sms = num_sms();
+  static const bool split_on = [] {
+    const char* e = getenv("LAPIS_B200_OZAKI_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  const int rem = tiles % sms;
+  const int nsplit = (!TWO_PASS && split_on && S > 1 && rem > 0 && 2 * rem <= sms) ? rem : 0;
+  const int grid = nsplit ? (tiles >= sms ? sms : 2 * rem) : std::min(tiles, sms);
+  uint32_t helper_mask = 0;
+  if (nsplit) {
+    // helper: the subset of diagonals 0..S-2 (diagonal d = d+1 slice products)
+    // minimising the larger half
+    const int all = S * (S + 1) / 2;
+    int best = all;
+    for (uint32_t msk = 1; msk < (1u << (S - 1)); ++msk) {
+      int h = 0;
+      for (int d = 0; d < S - 1; ++d) h += ((msk >> d) & 1u) ? d + 1 : 0;
+      const int mx = std::max(h, all - h);
+      if (mx < best) { best = mx; helper_mask = msk; }
+    }
+  }
+  const size_t split_bytes = TWO_PASS ? (size_t)std::min(tiles, sms) * OZ2_SLOT * sizeof(double)
+                          : nsplit ? (size_t)nsplit * OZ_BM * BN * sizeof(double) : 0;
+  const size_t flag_bytes = (size_t)nsplit * OZ_EPI_WARPS * sizeof(int);
   uint8_t* ws = nullptr;
-  LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, a_bytes + b_bytes + part_bytes + meta + 256, st),
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, a_bytes + b_bytes + part_bytes + split_bytes +
+                                                     meta + flag_bytes + 512, st),
                     "alloc(ozaki workspace)"));
   int8_t* ad = reinterpret_cast<int8_t*>(ws);
   int8_t* bd = ad + a_bytes;
   double* part = reinterpret_cast<double*>(ws + ((a_bytes + b_bytes + 255) / 256 * 256));
-  uint8_t* mp_ = reinterpret_cast<uint8_t*>(part) + part_bytes;
+  double* split_ws = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(part) + part_bytes + 255) / 256 * 256);
+  uint8_t* mp_ = reinterpret_cast<uint8_t*>(split_ws) + split_bytes;
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(mp_);
   int* ea = reinterpret_cast<int*>(colmax + n);
   int* eb = ea + m;
   int* flag = eb + n;
+  int* split_flag = flag + 2;
   int rc = LAPIS_B200_OK;
   for (int64_t b = 0; b < batch && rc == LAPIS_B200_OK; ++b) {
     const T* Ab = (const T*)A + b * sA;
     const T* Bb = (const T*)B + b * sB;
     T* Cb = (T*)C + b * sC;
     rc = check_cuda(cudaMemsetAsync(colmax, 0, (size_t)n * 8, st), "memset(colmax)");
-    if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st), "memset(flag)");
+    if (rc == LAPIS_B200_OK)
+      rc = check_cuda(cudaMemsetAsync(flag, 0, 2 * sizeof(int) + flag_bytes, st), "memset(flag)");
     if (rc != LAPIS_B200_OK) break;
     const int64_t rblocks = std::min<int64_t>(mp, (int64_t)num_sms() * 16);
     ozaki_split_rows<T><<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
@@ -540,15 +933,26 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
     ozaki_split_cols<T><<<tg, 256, 0, st>>>(k, n, kp, np, Bb, ldb, S, colmax, bd, eb, digits8);
     rc = check_launch("ozaki split");
     CUtensorMap ma, mb;
-    if (rc == LAPIS_B200_OK) rc = make_i8_map(&ma, ad, (int64_t)S * mp, kp, OZ_BM);
-    if (rc == LAPIS_B200_OK) rc = make_i8_map(&mb, bd, (int64_t)S * np, kp, BN);
+    if (TWO_PASS) {
+      if (rc == LAPIS_B200_OK) rc = make_i8_map3(&ma, ad, mp, kp, S, OZ_BM, 4);
+      if (rc == LAPIS_B200_OK) rc = make_i8_map3(&mb, bd, np, kp, S, BN, 4);
+    } else {
+      if (rc == LAPIS_B200_OK) rc = make_i8_map(&ma, ad, (int64_t)S * mp, kp, OZ_BM);
+      if (rc == LAPIS_B200_OK) rc = make_i8_map(&mb, bd, (int64_t)S * np, kp, BN);
+    }
     if (rc != LAPIS_B200_OK) break;
     OzParams prm;
     prm.m = (int)m;
     prm.n = (int)n;
     prm.nk = (int)((kp + OZ_BK - 1) / OZ_BK);
-    prm.num_m = (int)(mp / OZ_BM);
-    prm.num_n = (int)(np / BN);
+    prm.num_m = num_m_t;
+    prm.num_n = num_n_t;
+    prm.split_base = nsplit ? (tiles / sms) * grid : tiles;
+    prm.nsplit = nsplit;
+    prm.helper_mask = helper_mask;
+    prm.owner_mask = ((1u << S) - 1u) & ~helper_mask;
+    prm.split_ws = split_ws;
+    prm.split_flag = split_flag;
     prm.S = S;
     prm.mp = (int)mp;
     prm.np = (int)np;
@@ -581,17 +985,22 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
       cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), st);
     }
     prm.prof = dprof;
-    const int tiles = prm.num_m * prm.num_n;
-    const int grid = std::min(tiles, num_sms());
-    gemm_ozaki_kernel<T, BN><<<grid, OZ_THREADS, OzTile<BN>::SMEM, st>>>(ma, mb, prm);
-    rc = check_launch("gemm_ozaki_kernel");
+    if constexpr (TWO_PASS) {
+      prm.nk = (int)((kp + OZ2_BK - 1) / OZ2_BK);
+      prm.vec2 = ((uintptr_t)Cb % 16 == 0) && (ldc % 2 == 0);
+      rc = launch_ozaki_2p(ma, mb, prm, std::min(tiles, sms), st);
+    } else {
+      gemm_ozaki_kernel<T, BN><<<grid, OZ_THREADS, OzTile<BN>::SMEM, st>>>(ma, mb, prm);
+      rc = check_launch("gemm_ozaki_kernel");
+    }
     if (dprof) {
       unsigned long long h[8];
       cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       fprintf(stderr, "ozaki prof (cycles summed over CTAs): producer-wait-empty %llu  "
-              "mma-wait-tmem-empty %llu  mma-wait-full %llu  mma-total %llu  epi-wait-full %llu\n",
-              h[0], h[1], h[2], h[3], h[4]);
+              "mma-wait-tmem-empty %llu  mma-wait-full %llu  mma-total %llu  epi-wait-full %llu  "
+              "drain %llu over %llu drains (%.0f cycles each)\n",
+              h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[6] ? (double)h[5] / h[6] : 0.0);
       cudaFreeAsync(dprof, st);
     }
     // non-finite inputs: the reference-order GEMM, run only when flag[0] is set;
@@ -619,6 +1028,14 @@ int gemm_ozaki(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, in
     return e ? atoi(e) : 0;
   }();
   const int bn = bn_env ? bn_env : (dtype == LAPIS_B200_F64 ? 256 : 192);
+  // fp64 S = 8: the two-pass kernel (LAPIS_B200_OZAKI_2P=0 selects the
+  // per-diagonal kernel)
+  static const bool two_pass = [] {
+    const char* e = getenv("LAPIS_B200_OZAKI_2P");
+    return !(e && e[0] == '0');
+  }();
+  if (two_pass && dtype == LAPIS_B200_F64 && S == 8)
+    return gemm_ozaki_t<double, OZ2_BN, true>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st);
 #define LB_OZ(T, BN_) return gemm_ozaki_t<T, BN_>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st)
   if (dtype == LAPIS_B200_F64) { if (bn == 192) LB_OZ(double, 192); LB_OZ(double, 256); }
   if (dtype == LAPIS_B200_F32) { if (bn == 256) LB_OZ(float, 256); LB_OZ(float, 192); }
