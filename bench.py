@@ -429,7 +429,8 @@ class PowerLawSpmm(Workload):
         return 4 if self.max_len > 2048 else 1
 
     def kernel_name(self):
-        return "spmm_row_kernel<double,int64,int32,2> (+ hub-row chunk/combine)"
+        return ("spmm_batch_kernel<double> (32 rows per warp) + long rows: "
+                "long_rows_list/work, spmm_long_chunk/combine")
 
     def step(self):
         self.lb.spmm_csr(self.rowptr, self.colind, self.values, self.X, self.Y, nnz=self.nnz)
@@ -518,7 +519,9 @@ class DenseMatmul(Workload):
         names = {"tf32x3": "gemm_tf32x3_kernel (tcgen05 kind::tf32, 3xTF32)",
                  "dmma": "gemm_dmma_kernel (DMMA m8n8k4)",
                  "exact": "gemm_exact_kernel (reference order)",
-                 "ozaki": "gemm_ozaki_kernel (tcgen05 kind::i8, Ozaki digits, certified)"}
+                 "ozaki": ("gemm_ozaki_2p_kernel (tcgen05 kind::i8, two-pass Ozaki, certified)"
+                           if self.dt == torch.float64 and self.n * 9.0 * 2.0 ** -56 <= 0.75e-12
+                           else "gemm_ozaki_kernel (tcgen05 kind::i8, Ozaki digits, certified)")}
         return f"gemm<{self.dtype}> mode={self.mode} -> {names[m]}"
 
     def roofline_override(self, kern_avg):
@@ -614,7 +617,8 @@ class GcnLayer(Workload):
         return 4 if self.max_len > 2048 else 2
 
     def kernel_name(self):
-        return "spmm_row_kernel<float> + gemm_exact_kernel<float, relu> (reference order)"
+        return ("spmm_batch_kernel<float> + spmm_seq_long_pipe_kernel (exact-order hub rows) + "
+                "gemm_exact_narrow_kernel<relu> (reference order)")
 
     def step(self):
         self.lb.gcn_layer(self.rowptr, self.colind, self.values, self.X, self.W, self.H,
@@ -747,6 +751,38 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(out))
 
 
+def launch_census(wl):
+    """Kernels one step launches, counted by the CUDA activity tracer (CUPTI via
+    torch.profiler) on an untimed step after the timed region: how many of
+    OUR kernels (namespace lapis_b200 / NVRTC-generated lapis_*) run per step
+    and each one's share of the step's device time.  None when the tracer is
+    unavailable."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            wl.step()
+            torch.cuda.synchronize()
+        per = {}
+        for e in prof.events():
+            if getattr(e, "device_type", None) is None or "cuda" not in str(e.device_type).lower():
+                continue
+            name = e.name
+            if "lapis" not in name:
+                continue
+            short = name.split("(")[0].replace("void ", "").replace("lapis_b200::", "")
+            c, t = per.get(short, (0, 0.0))
+            per[short] = (c + 1, t + float(getattr(e, "device_time", 0.0) or
+                                          getattr(e, "cuda_time", 0.0) or 0.0))
+        if not per:
+            return None
+        total = sum(t for _, t in per.values()) or 1.0
+        return {k: {"launches_per_step": c, "share": round(t / total, 4)}
+                for k, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1])}
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -824,6 +860,7 @@ def main():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
     exact_variant = (wl.exact_variant(max(3, args.steps // 2))
                      if hasattr(wl, "exact_variant") and not args.vl else None)
+    census = launch_census(wl)
     wl.step()   # the parity sample below checks the headline kernel's output
     torch.cuda.synchronize()
     e2e_dt, hb, db = wl.e2e(args.e2e_steps, 2)
@@ -846,7 +883,11 @@ def main():
                 "path": getattr(wl, "e2e_path", "DualView lazy sync (inputs host-modified each "
                                 "step) + C-ABI kernels + result read on the host"),
                 **({"matches_device_result": wl.e2e_parity} if hasattr(wl, "e2e_parity") else {})},
-        "gpu_launches": args.steps * wl.launches_per_step(),
+        "gpu_launches": args.steps * (sum(v["launches_per_step"] for v in census.values())
+                                      if census else wl.launches_per_step()),
+        "gpu_launches_source": ("CUDA activity trace of one untimed step x steps" if census
+                                else "static count per step x steps"),
+        **({"kernels": census} if census else {}),
         **({"exact_mode": exact_variant} if exact_variant else {}),
         "clocks": clk.summary(),
     }

@@ -637,40 +637,59 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
 }
 
 // ------------------------------------------------------------- digit split
-// Peel the S signed 7-bit digits of r in (-1, 1) (every step exact in fp64)
-// for 4 consecutive elements and store them as one 32-bit word per plane.
+// Peel the S signed 7-bit digits of r in (-1, 1) for 4 consecutive elements
+// and store them as one 32-bit word per plane.  Sequential peeling
+// (t = 128 r, digit = trunc(t), r = t - digit, all exact in fp64) yields the
+// base-128 digits of trunc(|r| 2^(7S)) with r's sign, so one conversion per
+// element replaces S of them.
 __device__ __forceinline__ void peel4(double r0, double r1, double r2, double r3, int S,
                                       int8_t* __restrict__ out, int64_t plane) {
-  double r[4] = {r0, r1, r2, r3};
+  const double r[4] = {r0, r1, r2, r3};
+  const double scale = __hiloint2double((7 * S + 1023) << 20, 0);
+  unsigned long long q[4];
+  uint32_t neg = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    q[c] = (unsigned long long)(fabs(r[c]) * scale);   // exact scaling, truncating conversion
+    neg |= (r[c] < 0.0 ? 1u : 0u) << c;
+  }
   for (int s = 0; s < S; ++s) {
+    const int sh = 7 * (S - 1 - s);
     uint32_t w = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double t = r[q] * 128.0;
-      const double dg = trunc(t);
-      r[q] = t - dg;
-      w |= (uint32_t)(uint8_t)(int8_t)(int)dg << (8 * q);
+    for (int c = 0; c < 4; ++c) {
+      const int d = (int)((q[c] >> sh) & 127u);
+      w |= (uint32_t)(uint8_t)((neg >> c) & 1u ? -d : d) << (8 * c);
     }
     *reinterpret_cast<uint32_t*>(out + (int64_t)s * plane) = w;
   }
 }
 
 // 8-bit digits: the leading digit floor(128 r) is signed ([-128, 127]), the
-// remainder is in [0, 1) and every further digit floor(256 r) unsigned.
+// remainder is in [0, 1) and every further digit floor(256 r) unsigned — the
+// two's-complement bytes of floor(r 2^(7 + 8(S-1))).
 __device__ __forceinline__ void peel4_u8(double r0, double r1, double r2, double r3, int S,
                                          int8_t* __restrict__ out, int64_t plane) {
-  double r[4] = {r0, r1, r2, r3};
+  const double r[4] = {r0, r1, r2, r3};
+  const double scale = __hiloint2double((7 + 8 * (S - 1) + 1023) << 20, 0);
+  long long q[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) q[c] = (long long)floor(r[c] * scale);
   for (int s = 0; s < S; ++s) {
+    const int sh = 8 * (S - 1 - s);
     uint32_t w = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double t = r[q] * (s == 0 ? 128.0 : 256.0);
-      const double dg = floor(t);
-      r[q] = t - dg;
-      w |= (uint32_t)((int)dg & 0xff) << (8 * q);
-    }
+    for (int c = 0; c < 4; ++c) w |= (uint32_t)((q[c] >> sh) & 0xff) << (8 * c);
     *reinterpret_cast<uint32_t*>(out + (int64_t)s * plane) = w;
   }
+}
+
+// v * 2^-e for the split (any finite v with |v| < 2^e): two exact multiplies
+// by powers of two in the normal range
+__device__ __forceinline__ double scale_down(double v, int e) {
+  const int e1 = min(max(-e, -1022), 1023);
+  const int e2 = min(max(-e - e1, -1022), 1023);
+  return v * __hiloint2double((e1 + 1023) << 20, 0) * __hiloint2double((e2 + 1023) << 20, 0);
 }
 
 // One CTA per row of A: the row's largest magnitude gives ea (max < 2^ea),
@@ -710,7 +729,7 @@ ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restri
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const double v = (i < m && j + q < k) ? (double)arow[j + q] : 0.0;
-        r[q] = isfinite(v) ? scalbn(v, -e) : 0.0;
+        r[q] = isfinite(v) ? scale_down(v, e) : 0.0;
       }
       if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, orow + j, plane);
       else peel4(r[0], r[1], r[2], r[3], S, orow + j, plane);
@@ -746,13 +765,16 @@ __global__ void __launch_bounds__(256)
 ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restrict__ B,
                  int64_t ldb, int S, const unsigned long long* __restrict__ colmax,
                  int8_t* __restrict__ out, int* __restrict__ e_out, int digits8) {
-  __shared__ double tile[128][33];
+  // column c of row r lives at tile[r][c ^ (r / 4 % 32)]: the row-wise fill and
+  // the 4-rows-per-lane column reads below are both free of bank conflicts
+  __shared__ double tile[128][32];
   const int64_t k0 = (int64_t)blockIdx.y * 128, n0 = (int64_t)blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+#pragma unroll
   for (int r = ty; r < 128; r += 8) {
     const int64_t kk = k0 + r, nn = n0 + tx;
     const double v = (kk < k && nn < n) ? (double)B[kk * ldb + nn] : 0.0;
-    tile[r][tx] = isfinite(v) ? v : 0.0;
+    tile[r][tx ^ ((r >> 2) & 31)] = isfinite(v) ? v : 0.0;
   }
   __syncthreads();
   const int64_t plane = np * kp;
@@ -769,7 +791,7 @@ ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restri
     }
     double r[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) r[q] = (nn < n) ? scalbn(tile[4 * tx + q][cc], -e) : 0.0;
+    for (int q = 0; q < 4; ++q) r[q] = (nn < n) ? scale_down(tile[4 * tx + q][cc ^ tx], e) : 0.0;
     if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
     else peel4(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
   }
