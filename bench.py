@@ -848,7 +848,9 @@ def main():
     else:
         # tensor-bound: nominal B200 dense peaks (MEASURED_PEAKS has bf16 only)
         if wl.dtype == "f32":
-            peak, psrc = 1100.0 / 3.0, "nominal TF32 dense 1.1 PF / 3 (3xTF32)"
+            # dense TF32 runs at half the bf16 rate on B200; 3xTF32 issues 3
+            peak = pk["bf16_tflops"] / 2.0 / 3.0
+            psrc = f"{pk['source']} bf16_tflops / 2 (dense TF32 = bf16 / 2) / 3 (3xTF32 products)"
         else:
             peak, psrc = 40.0, "nominal FP64 tensor 40 TF"
         punit = "TFLOP/s"
