@@ -421,6 +421,21 @@ constexpr uint32_t OZ2_STAGE = 16 * OZ2_DIGIT;               // 64 KB
 constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + OZ_EPI_SMEM + 1024;
 constexpr int OZ2_SLOT = 8 * 4 * 16 * 32;                    // doubles per CTA partial (128 KB)
 
+// Grouped raster: bands of OZ2_GM row blocks, column-major inside a band, so
+// the ~148 tiles in flight share ~12 A and ~12 B digit blocks (instead of all
+// 32 A blocks) and the concurrent CTAs hit the same lines in L2
+#ifndef OZ2_GM
+#define OZ2_GM 12
+#endif
+__device__ __forceinline__ void oz2_tile(int tile, int num_m, int num_n, int& mb, int& nb) {
+  const int band = OZ2_GM * num_n;
+  const int first = (tile / band) * OZ2_GM;
+  const int rows = min(num_m - first, OZ2_GM);
+  const int t = tile % band;
+  mb = first + t % rows;
+  nb = t / rows;
+}
+
 template <class OUT>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
@@ -458,7 +473,9 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int ma = (tile % p.num_m) * OZ_BM, nbn = (tile / p.num_m) * OZ2_BN;
+        int mb, nb;
+        oz2_tile(tile, p.num_m, p.num_n, mb, nb);
+        const int ma = mb * OZ_BM, nbn = nb * OZ2_BN;
         for (int j = 0; j < nk2; ++j) {            // pass A: K blocks 2j, 2j+1 (zero-filled past K)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * OZ2_STAGE;
@@ -549,7 +566,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
     double* slot = p.split_ws + (int64_t)blockIdx.x * OZ2_SLOT + ew * (4 * 16 * 32) + lane;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int mb = tile % p.num_m, nb = tile / p.num_m;
+      int mb, nb;
+      oz2_tile(tile, p.num_m, p.num_n, mb, nb);
       const int row_base = mb * OZ_BM + lg * 32;
       const int row = row_base + lane;
       const int ea = row < p.m ? __ldg(p.ea + row) : 0;
