@@ -998,7 +998,7 @@ class LibGen(NestGen):
             self.ind -= 1
             self.emit("}")
             self.store(y, idx, acc)
-        elif name == "sparse.spmv_csr":
+        elif name in ("sparse.spmv_csr", "kokkos.spmv_csr"):
             rp, ci, vals, x, y = op.operands
             kind = y.type.element.kind
             rpd = self.memref(rp)[1]
@@ -1069,7 +1069,8 @@ def identity_literal(comb: str, kind: str) -> str:
 
 
 LIBRARY_OPS = ("linalg.fill", "linalg.elementwise", "linalg.reduce", "linalg.matmul", "kokkos.gemm",
-               "linalg.batch_matmul", "linalg.matvec", "kokkos.gemv", "sparse.spmv_csr")
+               "linalg.batch_matmul", "linalg.matvec", "kokkos.gemv", "sparse.spmv_csr",
+               "kokkos.spmv_csr")
 
 
 def generate_library(op, name: str) -> Kernel:

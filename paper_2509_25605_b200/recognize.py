@@ -701,7 +701,7 @@ _LIBRARY = {
     "kokkos.gemm": _lib_matmul, "linalg.matmul": _lib_matmul,
     "kokkos.gemv": _lib_matvec, "linalg.matvec": _lib_matvec,
     "linalg.batch_matmul": _lib_batch_matmul,
-    "sparse.spmv_csr": _lib_spmv,
+    "sparse.spmv_csr": _lib_spmv, "kokkos.spmv_csr": _lib_spmv,
     "linalg.reduce": _lib_reduce,
 }
 

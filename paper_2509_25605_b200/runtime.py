@@ -778,7 +778,7 @@ def _library_checks(m: _Machine, op, env) -> None:
         nb, mm, kk = a.shape
         if b.shape[1] != kk or c.shape[1:] != (mm, b.shape[2]):
             m.fail(op, f"batch_matmul shape mismatch {a.shape} x {b.shape} -> {c.shape}")
-    elif name == "sparse.spmv_csr":
+    elif name in ("sparse.spmv_csr", "kokkos.spmv_csr"):
         rowptr, y = env[op.operands[0]], env[op.operands[4]]
         nrows = rowptr.shape[0] - 1
         if y.shape[0] != nrows:
@@ -794,7 +794,7 @@ def _library_total(op, env) -> int:
         return int(np.prod([e for d, e in enumerate(src.shape) if d not in axes], dtype=np.int64))
     if name in ("linalg.matvec", "kokkos.gemv"):
         return env[op.operands[2]].shape[0]
-    if name == "sparse.spmv_csr":
+    if name in ("sparse.spmv_csr", "kokkos.spmv_csr"):
         return max(env[op.operands[0]].shape[0] - 1, 0)
     out = env[op.operands[1] if name == "linalg.fill" else
               op.operands[-1] if name == "linalg.elementwise" else op.operands[2]]
@@ -845,6 +845,7 @@ _LIBRARY_OPERANDS = {
     "linalg.elementwise": lambda op: (op.operands[:-1], op.operands[-1:]),
     "linalg.reduce": lambda op: (op.operands[:1], op.operands[1:2]),
     "sparse.spmv_csr": lambda op: (op.operands[:4], op.operands[4:5]),
+    "kokkos.spmv_csr": lambda op: (op.operands[:4], op.operands[4:5]),
 }
 
 
@@ -1024,7 +1025,8 @@ def _h_scf_parallel(m: _Machine, op, env):
 def _device_mappable(op) -> bool:
     return not any(o.name in ("memref.alloc", "memref.dealloc", "func.call", "memref.copy",
                               "memref.subview", "memref.cast", "memref.get_global",
-                              "linalg.matmul", "linalg.matvec", "sparse.spmv_csr")
+                              "linalg.matmul", "linalg.matvec", "sparse.spmv_csr",
+                              "kokkos.spmv_csr")
                    for o in walk(op)) and all(
         getattr(v.type, "kind", "f64") != "f16" for o in walk(op) for v in o.results)
 
@@ -1066,7 +1068,7 @@ def _h_call(m, op, env):
 
 def _h_library(m: _Machine, op, env):
     # linalg.* / sparse.spmv_csr run in the current context (interp.py:704-812);
-    # kokkos.gemm / gemv always on the device (interp.py:949-976)
+    # kokkos.gemm / gemv / spmv_csr always on the device (interp.py:949-976)
     space = "device" if op.name.startswith("kokkos.") else m.ctx
     m.launch(op, env, space)
 
@@ -1175,6 +1177,7 @@ _HOST = {
     "linalg.elementwise": _h_library,
     "linalg.reduce": _h_library,
     "sparse.spmv_csr": _h_library,
+    "kokkos.spmv_csr": _h_library,   # sparse_route.py: the kernel-library route
     "kokkos.range_parallel": _h_kernel,
     "kokkos.team_parallel": _h_kernel,
     "kokkos.thread_parallel": _h_kernel,

@@ -106,10 +106,12 @@ LIBDIR = ROOT / "paper_2509_25605_b200" / "lib"
 
 
 def compile_driver(src: Path, out: Path, compile_only: bool = False,
-                   b200_seam: bool = False) -> subprocess.CompletedProcess:
+                   b200_seam: bool = False, extra_include: Path | None = None
+                   ) -> subprocess.CompletedProcess:
+    inc = [f"-I{extra_include}"] if extra_include else []
     cmd = [nvcc(), "-std=c++17", "-O2", "-gencode", "arch=compute_100a,code=sm_100a",
-           "--extended-lambda", "-w", f"-I{KOKKOS_B200}", f"-I{EMITTED}", f"-I{ROOT / 'include'}",
-           "-x", "cu"]
+           "--extended-lambda", "-w", f"-I{KOKKOS_B200}", *inc, f"-I{EMITTED}",
+           f"-I{ROOT / 'include'}", "-x", "cu"]
     cmd += (["-c", str(src), "-o", str(out)] if compile_only else [str(src), "-o", str(out)])
     if b200_seam and not compile_only:
         cmd += [f"-L{LIBDIR}", "-llapis_b200", f"-Xlinker=-rpath,{LIBDIR}"]
