@@ -11,7 +11,7 @@ int64 rowptr / int32 colind, row-block sharded over the ranks with the halo
 exchange of x (paper_2509_25605_b200/sharded.py).  A step is one SpMV over the
 whole matrix.  Inputs (69 GB) exceed L2 (126 MB) many times, so no flush is
 needed between steps.  Other workloads (--workload) are config 1 (SpMV, 5-point
-Laplacian, L2 flushed between steps), config 3 (SpMM, K = 64, power-law
+Laplacian, 84 MB < L2: steps rotate over input copies), config 3 (SpMM, K = 64, power-law
 matrix) and config 2 (dense matmul 4096^3, f32 or f64).
 
 `value` is device-resident throughput (algorithmic bytes or flops / step time,
@@ -44,6 +44,9 @@ METRIC = "SpMV/SpMM HBM GB/s (% of peak), matmul TFLOP/s, at 1/2/4/8 B200 vs CPU
 
 
 # --------------------------------------------------------------------- utilities
+L2_BYTES = 126 << 20   # B200 L2
+
+
 def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -192,9 +195,21 @@ class StencilSpmv(Workload):
         self.op = sharded.RowBlockSpmv(self.rowptr, self.colind, self.values, self.r0, self.r1,
                                        self.N, self.ranges, rank, world)
         self.halo_bytes = 8 * self.op.plan.recv_elems
-        # config 1 (80 MB) fits in L2: flush it between timed steps
-        if self.work_local() < (512 << 20):
-            self.flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        # config 1 (84 MB) fits in L2 (126 MB): the timed steps rotate over R
+        # device copies of the whole input (matrix, x, y; R * work >= 3 x L2), so
+        # every step reads its operands cold from HBM without a flush kernel
+        # between steps (a 256 MB write flush leaves L2 full of dirty lines whose
+        # write-back would be timed inside the next SpMV)
+        self.rot = [(self.rowptr, self.colind, self.values, self.x, self.y, self.op)]
+        self.rot_i = 0
+        self.last_y = self.y
+        if self.work_local() < (512 << 20) and not args.vl:
+            ncopy = -(-(3 * L2_BYTES) // int(self.work_local()))
+            for _ in range(1, ncopy):
+                rp, ci, v = self.rowptr.clone(), self.colind.clone(), self.values.clone()
+                self.rot.append((rp, ci, v, self.x.clone(), torch.empty_like(self.y),
+                                 sharded.RowBlockSpmv(rp, ci, v, self.r0, self.r1, self.N,
+                                                      self.ranges, rank, world)))
         torch.cuda.synchronize()
 
     @property
@@ -210,8 +225,11 @@ class StencilSpmv(Workload):
         return {"workload": self.name, "rows": self.N, "nnz": self.nnz_global(),
                 "index_layout": "rowptr int64, colind int32", "x": f"U(-1,1) seed {self.x_seed}",
                 "sharding": f"row blocks x{self.world}, halo exchange of x (NCCL P2P)",
-                "l2": "inputs >> L2 (126 MB), no flush needed" if self.flush is None else
-                      "L2 flushed between steps (256 MB write, outside the step events)",
+                **({"launch": self.graph_note} if self.graphs else {}),
+                "l2": ("inputs >> L2 (126 MB), no flush needed" if len(self.rot) == 1 else
+                       f"inputs < L2: steps rotate over {len(self.rot)} device copies of the "
+                       f"whole input ({len(self.rot) * self.work_local() / 1e6:.0f} MB > 3 x L2), "
+                       "no flush"),
                 "parallelism": f"rowblock{self.world}"}
 
     def work_global(self) -> float:
@@ -236,29 +254,59 @@ class StencilSpmv(Workload):
             # emitted TeamPolicy mapping with an explicit vector length (no plan)
             self.lb.spmv_csr(self.rowptr, self.colind, self.values, self.x, self.y,
                              vector_length=self.args.vl, nnz=self.nnz_local)
+            self.last_y = self.y
             return
-        self.op.multiply(self.x, self.y, stream=self.stream)
+        rp, ci, v, x, y, op = self.rot[self.rot_i]
+        g = self.graphs[self.rot_i] if self.graphs else None
+        self.rot_i = (self.rot_i + 1) % len(self.rot)
+        if g is not None:
+            g.replay()
+        else:
+            op.multiply(x, y, stream=self.stream)
+        self.last_y = y
+
+    graphs = None
+
+    def capture_graphs(self):
+        """Config 1's SpMV (~15-20 us) is shorter than the host cost of one
+        Python-level multiply, so on one GPU each rotation copy's multiply is
+        captured once in a CUDA graph and a step replays it (same kernel, same
+        arguments; the graph only removes the host launch overhead)."""
+        if self.world > 1 or len(self.rot) == 1 or self.args.vl:
+            return
+        graphs = []
+        side = torch.cuda.Stream()
+        side.wait_stream(self.stream)
+        for rp, ci, v, x, y, op in self.rot:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                op.multiply(x, y, stream=side)
+            graphs.append(g)
+        self.stream.wait_stream(side)
+        torch.cuda.synchronize()
+        self.graphs = graphs
+        self.graph_note = f"each step replays a captured CUDA graph of the multiply ({len(graphs)} graphs, one per input copy)"
 
     def exact_variant(self, steps):
         """The same multiply with every row folded in the reference order (plan
         exact mode, bit-identical); device-resident throughput."""
         from paper_2509_25605_b200 import sharded
-        op = sharded.RowBlockSpmv(self.rowptr, self.colind, self.values, self.r0, self.r1,
-                                  self.N, self.ranges, self.rank, self.world, exact=True)
-        for _ in range(3):
-            op.multiply(self.x, self.y, stream=self.stream)
-        evs = []
-        for _ in range(steps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if self.flush is not None:
-                self.flush.fill_(1)
-            a.record(self.stream)
-            op.multiply(self.x, self.y, stream=self.stream)
-            b.record(self.stream)
-            evs.append((a, b))
+        ops = [(sharded.RowBlockSpmv(rp, ci, v, self.r0, self.r1, self.N, self.ranges, self.rank,
+                                     self.world, exact=True), x, y)
+               for rp, ci, v, x, y, _ in self.rot]
+        for i in range(3):
+            op, x, y = ops[i % len(ops)]
+            op.multiply(x, y, stream=self.stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        t = max_over_ranks(float(np.mean([a.elapsed_time(b) / 1e3 for a, b in evs])), self.world)
-        names = sorted({p.info()["kernel"] for p in op.plans.values()})
+        a.record(self.stream)
+        for i in range(steps):
+            op, x, y = ops[i % len(ops)]
+            op.multiply(x, y, stream=self.stream)
+        b.record(self.stream)
+        torch.cuda.synchronize()
+        t = max_over_ranks(a.elapsed_time(b) / 1e3 / steps, self.world)
+        names = sorted({p.info()["kernel"] for p in ops[0][0].plans.values()})
         return {"value": round(self.work_global() / t / 1e9, 3), "unit": "GB/s",
                 "frac": round(self.work_local() / t / 1e9 / peaks()["hbm_gbs"], 4),
                 "kernel": "; ".join(names), "note": "bit-identical to the reference"}
@@ -312,7 +360,7 @@ class StencilSpmv(Workload):
         desc = (f"rows [{a}, {b}) of the same matrix ({nnz} nnz): reference emitted Kokkos C++ "
                 f"(tests/fixtures/spmv.mlir, index colind) on its serial stub, {threads} row "
                 f"blocks on std::threads")
-        got = self.y[a - self.r0:b - self.r0].cpu().numpy()
+        got = self.last_y[a - self.r0:b - self.r0].cpu().numpy()
         return yref, got, times, work, desc, 1e-12
 
 
@@ -392,38 +440,70 @@ class MtxSpmv(Workload):
 
 
 class PowerLawSpmm(Workload):
-    """Config 3: CSR x dense SpMM fp64, K = 64, Chung-Lu power-law matrix."""
+    """Config 3: CSR x dense SpMM fp64, K = 64, Chung-Lu power-law matrix.
+
+    N > 1: the SAME global matrix, row-block sharded
+    (sharded.RowBlockSpmm: rank r owns rows [r*c, r*c + c), c = ceil(N / world),
+    and the matching rows of X and Y); a step is the NCCL all-gather of X
+    followed by the local SpMM (strong scaling, total work fixed).  The
+    "x_replicated" variant times the local SpMM alone (features resident on
+    every GPU, the GCN case)."""
 
     name = "config3: CSR x dense SpMM fp64, K=64, power-law (Chung-Lu, Pareto 2.5) 10M rows"
-    scaling = "weak"
+    scaling = "strong"
+    variant_key = "variants"
 
     def __init__(self, args, rank, world, n=10_000_000, k=64, mean=10.0, seed=1):
         import paper_2509_25605_b200 as lb
-        self.lb, self.args, self.world = lb, args, world
+        from paper_2509_25605_b200 import sharded
+        self.lb, self.args, self.world, self.rank = lb, args, world, rank
         self.N, self.k, self.seed = n, k, seed
         self.stream = torch.cuda.current_stream()
-        self.rowptr, self.colind, self.values = powerlaw_csr_device(n, mean, 2.5, seed)
-        self.nnz = int(self.rowptr[-1].item())
+        rowptr, colind, values = powerlaw_csr_device(n, mean, 2.5, seed)
+        self.nnz_global_ = int(rowptr[-1].item())
         g = torch.Generator(device="cuda").manual_seed(seed + 100)
-        self.X = torch.rand((n, k), generator=g, dtype=torch.float64, device="cuda") * 2 - 1
-        self.Y = torch.empty((n, k), dtype=torch.float64, device="cuda")
-        lens = (self.rowptr[1:] - self.rowptr[:-1])
+        X = torch.rand((n, k), generator=g, dtype=torch.float64, device="cuda") * 2 - 1
+        lens = (rowptr[1:] - rowptr[:-1])
         self.max_len = int(lens.max().item())
         self.median_len = float(lens.double().median().item())
+        self.r0, self.r1 = sharded.equal_row_ranges(n, world)[rank]
+        if world > 1:
+            a, b = int(rowptr[self.r0].item()), int(rowptr[self.r1].item())
+            self.rowptr = (rowptr[self.r0:self.r1 + 1] - a).contiguous()
+            self.colind, self.values = colind[a:b].contiguous(), values[a:b].contiguous()
+            del rowptr, colind, values
+        else:
+            self.rowptr, self.colind, self.values = rowptr, colind, values
+        self.nnz = int(self.rowptr[-1].item())
+        self.op = sharded.RowBlockSpmm(self.rowptr, self.colind, self.values, n, k, rank, world)
+        self.op.x_local.copy_(X[self.r0:self.r1])
+        del X
+        self.op.gather()
+        self.X = self.op.X_full[:n]
+        self.Y = torch.empty((self.r1 - self.r0, k), dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
     def config(self):
-        return {"workload": self.name, "rows": self.N, "nnz": self.nnz, "k": self.k,
+        return {"workload": self.name, "rows": self.N, "nnz": self.nnz_global_, "k": self.k,
                 "max_row": self.max_len, "median_row": self.median_len,
                 "index_layout": "rowptr int64, colind int32",
                 "generator": f"torch CUDA generator seed {self.seed} (device)",
-                "l2": "inputs >> L2", "parallelism": "replica"}
+                "l2": "inputs >> L2",
+                "sharding": (f"row blocks x{self.world}, NCCL all-gather of X "
+                             f"({self.op.gather_bytes / 1e9:.2f} GB received per rank per step) "
+                             "then the local SpMM" if self.world > 1 else "none"),
+                "parallelism": f"rowblock{self.world}"}
+
+    def _work(self, nnz, rows):
+        # SURVEY 8(d): nnz*(s_v+s_i) + (N+1)*s_p + Ncols*K*s_v + N*K*s_v
+        return nnz * 12 + (rows + 1) * 8 + self.N * self.k * 8 + rows * self.k * 8
 
     def work_global(self):
-        return self.work_local() * self.world
+        return self._work(self.nnz_global_, self.N)
 
     def work_local(self):
-        return self.nnz * 12 + (self.N + 1) * 8 + self.N * self.k * 8 * 2
+        # the local SpMM's algorithmic bytes (its X gathers can touch every row of X)
+        return self._work(self.nnz, self.r1 - self.r0)
 
     def launches_per_step(self):
         return 4 if self.max_len > 2048 else 1
@@ -433,19 +513,38 @@ class PowerLawSpmm(Workload):
                 "long_rows_list/work, spmm_long_chunk/combine")
 
     def step(self):
-        self.lb.spmm_csr(self.rowptr, self.colind, self.values, self.X, self.Y, nnz=self.nnz)
+        self.op.multiply(self.Y, stream=self.stream)
+
+    def exact_variant(self, steps):
+        """N > 1: the X-replicated time (local SpMM only, no all-gather)."""
+        if self.world == 1:
+            return None
+        for _ in range(3):
+            self.op.multiply(self.Y, stream=self.stream, replicated=True)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(self.world)
+        torch.cuda.synchronize()
+        a.record(self.stream)
+        for _ in range(steps):
+            self.op.multiply(self.Y, stream=self.stream, replicated=True)
+        b.record(self.stream)
+        torch.cuda.synchronize()
+        t = max_over_ranks(a.elapsed_time(b) / 1e3 / steps, self.world)
+        return {"x_replicated": {"value": round(self.work_global() / t / 1e9, 3), "unit": "GB/s",
+                                 "ms_per_step": round(t * 1e3, 4),
+                                 "note": "X resident on every GPU: local SpMM only"}}
 
     def e2e(self, steps, warmup):
-        """X (the dense operand) host-modified every step, Y read back."""
+        """This rank's rows of X host-modified every step (DualView sync of the
+        slot, then the all-gather when N > 1), Y read back."""
         from paper_2509_25605_b200.dualview import DualView
-        xs = DualView.from_host(self.X.cpu(), "X", device_buffer=self.X)
+        xs = DualView.from_host(self.op.x_local.cpu(), "X", device_buffer=self.op.x_local)
         ys = DualView.allocate(tuple(self.Y.shape), torch.float64, "Y")
 
         def one():
             xs.modify_host()
             xs.sync_device(self.stream)
-            self.lb.spmm_csr(self.rowptr, self.colind, self.values, xs.device_view(),
-                             ys.device_view(), nnz=self.nnz)
+            self.op.multiply(ys.device_view(), stream=self.stream)
             ys.modify_device()
             ys.sync_host(self.stream)
 
@@ -602,13 +701,15 @@ class GcnLayer(Workload):
     def config(self):
         return {"workload": self.name, "rows": self.N, "nnz": self.nnz, "features": self.f,
                 "max_row": self.max_len, "parallelism": "replica",
+                "bytes": "compulsory: A_hat + X + W + H (no A_hat X intermediate)",
                 "l2": "inputs > L2 (X 256 MB)"}
 
     def work_local(self):
+        # compulsory bytes of the layer: A_hat (int32 colind + f32 values, int64
+        # rowptr), X, W read once, H written once.  The A_hat X intermediate is
+        # not counted (the fused kernel never materialises it)
         f, n = self.f, self.N
-        spmm = self.nnz * 8 + (n + 1) * 8 + n * f * 4 + n * f * 4
-        dense = n * f * 4 + f * f * 4 + n * f * 4
-        return spmm + dense
+        return self.nnz * 8 + (n + 1) * 8 + n * f * 4 + f * f * 4 + n * f * 4
 
     def work_global(self):
         return self.work_local() * self.world
@@ -617,8 +718,8 @@ class GcnLayer(Workload):
         return 4 if self.max_len > 2048 else 2
 
     def kernel_name(self):
-        return ("spmm_batch_kernel<float> + spmm_seq_long_pipe_kernel (exact-order hub rows) + "
-                "gemm_exact_narrow_kernel<relu> (reference order)")
+        return ("spmm_batch_kernel<float> + spmm_seq_long_pipe_kernel (exact-order hub rows, "
+                "16-column groups) + gemm_exact_narrow_kernel<relu> (reference order)")
 
     def step(self):
         self.lb.gcn_layer(self.rowptr, self.colind, self.values, self.X, self.W, self.H,
@@ -815,16 +916,21 @@ def main():
     for _ in range(args.warmup):
         wl.step()
     torch.cuda.synchronize()
+    if hasattr(wl, "capture_graphs"):
+        wl.capture_graphs()
+        for _ in range(args.warmup):
+            wl.step()
+        torch.cuda.synchronize()
     barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
     per_step = []
     with ClockSampler(local) as clk:
         barrier(world)
         torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
+        for s0, s1 in step_events:
             if wl.flush is not None:
                 wl.flush.fill_(1)
             s0.record(stream)
@@ -890,7 +996,7 @@ def main():
         "gpu_launches_source": ("CUDA activity trace of one untimed step x steps" if census
                                 else "static count per step x steps"),
         **({"kernels": census} if census else {}),
-        **({"exact_mode": exact_variant} if exact_variant else {}),
+        **({getattr(wl, "variant_key", "exact_mode"): exact_variant} if exact_variant else {}),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -105,12 +105,17 @@ int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int r
                              const void* x, void* y, int dtype, void* stream);
 /* What the analysis chose: out[0] = longest row, out[1] = vector length of the
  * vector-lane kernel (0 = row-stream tile kernel), out[2] = number of tiles,
- * out[3] = exact flag.  Regular structures (longest row <= max(64, 8 x mean))
+ * out[3] = flags: bit 0 exact mode, bit 1 warp-block kernel.  Regular
+ * structures (longest row <= max(64, 8 x mean))
  * run the vector-lane kernel with VL = pow2floor(mean / 6) in [1, 8]: fp64 and
  * integer rows as the emitted TeamPolicy mapping (shuffle-tree reduce, the
  * Kokkos ThreadVectorRange semantics), fp32 rows — and every dtype once
  * lapis_b200_csr_plan_set_exact(plan, 1) — folded in the reference's
- * sequential order (bit-identical).  Irregular structures run the tile kernel. */
+ * sequential order (bit-identical).  With LAPIS_B200_SPMV_KERNEL=wb a monotone
+ * rowptr runs the warp-block kernel instead (32 rows per warp, coalesced entry
+ * stream, per-row ascending fold: bit-identical in every mode; measured slower
+ * than the vector kernel on the stencils, so not chosen by default).
+ * Irregular structures run the tile kernel. */
 int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out4);
 int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact);
 

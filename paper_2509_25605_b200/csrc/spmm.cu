@@ -207,12 +207,57 @@ __device__ __forceinline__ void sty_row(T* p, const T (&v)[CPL]) {
   *reinterpret_cast<V*>(p) = w;
 }
 
-template <class T, class RP, class CI, int CPL, int U>
+// ------------------------------------------------ fused GCN epilogue (fp32)
+// H[row, :] = relu(AX[row, :] W) for one row held by the warp as 2 values per
+// lane (lane l: AX[row, 2l], AX[row, 2l+1]; fin = fout = 64), W staged in shared
+// memory.  The reference order of the GCN's linalg.matmul (oracle/ir/gcn_f32.mlir,
+// interp.py:711-722): k ascending from 0.0f, mul and add each rounded — the same
+// arithmetic as gemm_exact_narrow_kernel — then the cmpf ogt + select ReLU.
+// Not inlined: it is called from every row-end point of the unrolled batch loop.
+constexpr int GCN_F = 64;
+__device__ __noinline__ void gcn_row_epilogue(float a0, float a1, const float* __restrict__ Ws,
+                                              float* __restrict__ hrow, int lane) {
+  float o0 = 0.0f, o1 = 0.0f;
+  const float2* w2 = reinterpret_cast<const float2*>(Ws) + lane;
+#pragma unroll 8
+  for (int kb = 0; kb < 32; ++kb) {
+    const float x0 = __shfl_sync(0xffffffffu, a0, kb);
+    const float x1 = __shfl_sync(0xffffffffu, a1, kb);
+    const float2 b0 = w2[(2 * kb) * (GCN_F / 2)];
+    const float2 b1 = w2[(2 * kb + 1) * (GCN_F / 2)];
+    o0 = __fadd_rn(o0, __fmul_rn(x0, b0.x));
+    o1 = __fadd_rn(o1, __fmul_rn(x0, b0.y));
+    o0 = __fadd_rn(o0, __fmul_rn(x1, b1.x));
+    o1 = __fadd_rn(o1, __fmul_rn(x1, b1.y));
+  }
+  float2 h;
+  h.x = (o0 > 0.0f) ? o0 : 0.0f;
+  h.y = (o1 > 0.0f) ? o1 : 0.0f;
+  reinterpret_cast<float2*>(hrow)[lane] = h;
+}
+
+template <class T, class RP, class CI, int CPL, int U, bool EPI = false>
 __global__ void __launch_bounds__(256, 4)
 spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                   const CI* __restrict__ colind, const T* __restrict__ values,
-                  const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+                  const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
+                  const T* __restrict__ W = nullptr) {
   const int lane = threadIdx.x & 31;
+  // EPI (fp32, k = 64, CPL = 2): Y is H, each finished row goes through the
+  // GCN epilogue with W staged in shared memory
+  __shared__ __align__(16) float Ws[EPI ? GCN_F * GCN_F : 1];
+  if constexpr (EPI) {
+    for (int t = threadIdx.x; t < GCN_F * GCN_F; t += blockDim.x) Ws[t] = W[t];
+    __syncthreads();
+  }
+  auto store_row = [&](int64_t row, const T (&a)[CPL], int64_t c0) {
+    if constexpr (EPI) {
+      static_assert(CPL == 2, "GCN epilogue: fin = 64");
+      gcn_row_epilogue(a[0], a[1], Ws, Y + row * ldy, lane);
+    } else {
+      sty_row<T, CPL>(Y + row * ldy + c0, a);
+    }
+  };
   const int64_t nbatch = (nrows + 31) >> 5;
   const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t bt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; bt < nbatch; bt += wstride) {
@@ -267,7 +312,7 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
               if (t0 + u < cnt) {
                 const int64_t j = j0 + t0 + u;
                 while (j == nxt) {  // rows that end here (empty rows included)
-                  sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
+                  store_row(r0 + cur, acc, c0);
 #pragma unroll
                   for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
                   ++cur;
@@ -282,7 +327,7 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
           my_val = nx_val;
         }
         for (; cur < rb; ++cur) {  // the run's last rows (and trailing empty rows)
-          sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
+          store_row(r0 + cur, acc, c0);
 #pragma unroll
           for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
         }
@@ -311,6 +356,24 @@ struct LongRows {
   int64_t* work_beg;   // [wcap] first entry of item
   int64_t* first;      // [cap] first item of listed row i
 };
+
+// rows the batch kernel skipped (long rows) hold AX in H after the long-row
+// kernels; one warp per listed row applies the GCN epilogue in place
+__global__ void __launch_bounds__(256)
+gcn_long_rows_epilogue_kernel(const float* __restrict__ W, float* __restrict__ H, int64_t ldh,
+                              const LongRows lr) {
+  __shared__ __align__(16) float Ws[GCN_F * GCN_F];
+  for (int t = threadIdx.x; t < GCN_F * GCN_F; t += blockDim.x) Ws[t] = W[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t n = *lr.count;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * 8) {
+    float* hrow = H + lr.rows[i] * ldh;
+    const float2 a = reinterpret_cast<const float2*>(hrow)[lane];
+    __syncwarp();
+    gcn_row_epilogue(a.x, a.y, Ws, hrow, lane);
+  }
+}
 
 template <class RP>
 __global__ void long_rows_list_kernel(int64_t nrows, const RP* __restrict__ rowptr, LongRows lr) {
@@ -356,13 +419,21 @@ __global__ void __launch_bounds__(1024) long_rows_work_kernel(const RP* __restri
   }
 }
 
-// Pipelined version (the one launched): warps 0-1 fold, one thread per dense
-// column, in ascending entry order; warps 2-7 stream the row's entries into a
-// PIPE_NS-stage shared-memory ring with cp.async (values + the X-row slices,
-// 8-byte copies), their colind loads running one stage further ahead, so the
-// fold never waits on a gather and the longest row costs ~its sequential add
-// chain instead of one gather latency per 32 entries.
-constexpr int PIPE_NS = 6, PIPE_SEQ = 128, PIPE_KC = 64, PIPE_LOADERS = 6;
+// Pipelined version (the one launched): one CTA per (hub row, group of 16
+// dense columns) — the row's 64 independent add chains run on 4 SMs, each
+// gathering 64 B of every referenced X row.  Warp 0 folds (one thread per
+// column, ascending entry order, the reference's rounding); warp 1 streams
+// the row's colind PIPE_CD stages ahead into a PIPE_CR-slot shared-memory ring
+// (cp.async, its own commit groups); warps 2-7 stream values and the X-row
+// slices of stage s + PIPE_NS - 1 into a PIPE_NS-stage ring, reading the
+// column indices from shared memory (four entries per warp instruction, one
+// 8-byte pair per lane).  With colind that far ahead no loader ever waits on
+// an index load, so a stage costs about its 128-add chain; the chain of the
+// longest row (config 4: 70k entries) is the floor.
+constexpr int PIPE_NS = 10, PIPE_SEQ = 128, PIPE_KC = 16, PIPE_LOADERS = 6;
+constexpr int PIPE_CR = 32, PIPE_CD = 24;  // colind ring slots, prefetch distance (stages)
+static_assert(PIPE_CD <= PIPE_CR + PIPE_NS - 3, "colind slot reused while still read");
+static_assert(PIPE_CD >= PIPE_NS, "colind prefetch shorter than the data ring");
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -376,78 +447,88 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
+template <class CI>
+constexpr size_t pipe_smem_bytes() {
+  return (size_t)PIPE_NS * PIPE_SEQ * (PIPE_KC + 1) * sizeof(float) +
+         (size_t)PIPE_CR * PIPE_SEQ * sizeof(CI);
+}
+
 template <class RP, class CI>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
 spmm_seq_long_pipe_kernel(int64_t k, const RP* __restrict__ rowptr,
                           const CI* __restrict__ colind, const float* __restrict__ values,
                           const float* __restrict__ X, int64_t ldx, float* __restrict__ Y,
                           int64_t ldy, const LongRows lr) {
-  constexpr int CPW = PIPE_SEQ / PIPE_LOADERS + 1;  // entries per loader warp per stage (22)
   extern __shared__ __align__(16) unsigned char pipe_smem[];
   float* xs = reinterpret_cast<float*>(pipe_smem);            // [NS][SEQ][KC]
   float* vs = xs + PIPE_NS * PIPE_SEQ * PIPE_KC;               // [NS][SEQ]
+  CI* cs = reinterpret_cast<CI*>(vs + PIPE_NS * PIPE_SEQ);     // [CR][SEQ]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nlong = *lr.count;
-  for (int64_t li = blockIdx.x; li < nlong; li += gridDim.x) {
-  const int64_t r = lr.rows[li];
-  const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
   const bool loader = warp >= 2;
   const int lw = warp - 2;
-  const int64_t nst = (e - b + PIPE_SEQ - 1) / PIPE_SEQ;
-  for (int64_t c0 = 0; c0 < k; c0 += PIPE_KC) {
+  const int64_t nlong = *lr.count;
+  const int64_t ncg = (k + PIPE_KC - 1) / PIPE_KC;  // column groups per row
+  for (int64_t item = blockIdx.x; item < nlong * ncg; item += gridDim.x) {
+    const int64_t r = lr.rows[item / ncg];
+    const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
+    const int64_t nst = (e - b + PIPE_SEQ - 1) / PIPE_SEQ;
+    const int64_t c0 = (item % ncg) * PIPE_KC;
     const int kc = (int)((k - c0) < PIPE_KC ? (k - c0) : PIPE_KC);
-    const bool pairs = (kc % 2 == 0) && (ldx % 2 == 0) && ((uintptr_t)X % 8 == 0);
-    // colind of the loader warp's entries of the NEXT stage to issue: lane u
-    // holds entry lw + 6u (one load per lane, issued a stage ahead), the
-    // issuing loop broadcasts it by shuffle
-    // kept in the index type: widening right after the load would make the
-    // loader wait for it here instead of at its use one stage later
-    CI my_col = CI(0);
-    auto load_cols = [&](int64_t s) {
-      const int64_t jb = b + s * PIPE_SEQ;
-      const int64_t lim = (s < nst) ? e - jb : 0;
-      const int jj = lw + PIPE_LOADERS * lane;
-      my_col = (lane < CPW && jj < PIPE_SEQ && jj < lim) ? __ldg(colind + jb + jj) : CI(0);
-    };
-    auto issue = [&](int64_t s) {
-      if (s < nst) {
-        const int slot = (int)(s % PIPE_NS);
-        const int64_t j0 = b + s * PIPE_SEQ;
+    const bool pairs = (kc == PIPE_KC) && (ldx % 2 == 0) && ((uintptr_t)X % 8 == 0);
+    auto issue_cols = [&](int64_t t) {  // warp 1
+      if (t < nst) {
+        const int64_t j0 = b + t * PIPE_SEQ;
         const int n = (int)((e - j0) < PIPE_SEQ ? (e - j0) : PIPE_SEQ);
-        const int lt = threadIdx.x - 64;
-        if (lt < n) cp_async4(&vs[slot * PIPE_SEQ + lt], values + j0 + lt);
-        if (lt + 192 < n) cp_async4(&vs[slot * PIPE_SEQ + lt + 192], values + j0 + lt + 192);
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-          const int jj = lw + PIPE_LOADERS * u;
-          const int64_t cu = (int64_t)__shfl_sync(0xffffffffu, my_col, u);
-          if (jj < n) {
-            const float* src = X + cu * ldx + c0;
-            float* dst = &xs[(slot * PIPE_SEQ + jj) * PIPE_KC];
-            if (pairs) {
-              if (2 * lane < kc) cp_async8(dst + 2 * lane, src + 2 * lane);
-            } else {
-              for (int cc = lane; cc < kc; cc += 32) cp_async4(dst + cc, src + cc);
-            }
-          }
+        CI* dst = cs + (int)(t % PIPE_CR) * PIPE_SEQ;
+        for (int i = lane; i < n; i += 32) {
+          if constexpr (sizeof(CI) == 8) cp_async8(dst + i, colind + j0 + i);
+          else cp_async4(dst + i, colind + j0 + i);
         }
       }
       cp_commit();  // one group per stage, possibly empty: uniform wait counts
     };
-    if (loader) {
-      for (int s = 0; s < PIPE_NS - 1; ++s) {
-        load_cols(s);
-        issue(s);
+    auto issue = [&](int64_t t) {  // warps 2-7
+      if (t < nst) {
+        const int slot = (int)(t % PIPE_NS);
+        const int64_t j0 = b + t * PIPE_SEQ;
+        const int n = (int)((e - j0) < PIPE_SEQ ? (e - j0) : PIPE_SEQ);
+        const CI* cr = cs + (int)(t % PIPE_CR) * PIPE_SEQ;
+        const int lt = threadIdx.x - 64;
+        if (lt < n) cp_async4(&vs[slot * PIPE_SEQ + lt], values + j0 + lt);
+        if (lt + 192 < n) cp_async4(&vs[slot * PIPE_SEQ + lt + 192], values + j0 + lt + 192);
+        if (pairs) {
+          // lane: entry (lane / 8) of a group of 4, column pair (lane % 8)
+          for (int jj = 4 * lw + (lane >> 3); jj < n; jj += 4 * PIPE_LOADERS) {
+            const int64_t cu = (int64_t)cr[jj];
+            cp_async8(&xs[(slot * PIPE_SEQ + jj) * PIPE_KC + 2 * (lane & 7)],
+                      X + cu * ldx + c0 + 2 * (lane & 7));
+          }
+        } else {
+          for (int jj = lw; jj < n; jj += PIPE_LOADERS) {
+            const int64_t cu = (int64_t)cr[jj];
+            if (lane < kc) cp_async4(&xs[(slot * PIPE_SEQ + jj) * PIPE_KC + lane], X + cu * ldx + c0 + lane);
+          }
+        }
       }
-      load_cols(PIPE_NS - 1);
+      cp_commit();
+    };
+    if (warp == 1) {
+      for (int t = 0; t < PIPE_CD; ++t) issue_cols(t);
+      cp_wait<PIPE_CD - PIPE_NS + 1>();  // colind of stages 0 .. NS-2 landed
     }
+    __syncthreads();
+    if (loader)
+      for (int t = 0; t < PIPE_NS - 1; ++t) issue(t);
     float acc = 0.0f;
     for (int64_t s = 0; s < nst; ++s) {
-      if (loader) cp_wait<PIPE_NS - 2>();  // this thread's copies of stage s landed
-      __syncthreads();                      // everyone's copies of stage s visible; slot s-1 free
+      if (loader) cp_wait<PIPE_NS - 2>();   // this thread's copies of stage s landed
+      if (warp == 1) {
+        issue_cols(s + PIPE_CD);
+        cp_wait<PIPE_CD - PIPE_NS + 1>();   // colind of stage s + NS - 1 landed
+      }
+      __syncthreads();                      // stage s and colind of s + NS - 1 visible
       if (loader) {
-        issue(s + PIPE_NS - 1);             // into slot (s-1) % NS
-        load_cols(s + PIPE_NS);
+        issue(s + PIPE_NS - 1);             // into slot (s - 1) % NS
       } else if ((int)threadIdx.x < kc) {
         const int slot = (int)(s % PIPE_NS);
         const int64_t j0 = b + s * PIPE_SEQ;
@@ -465,10 +546,9 @@ spmm_seq_long_pipe_kernel(int64_t k, const RP* __restrict__ rowptr,
         for (; jj < n; ++jj) acc = __fadd_rn(acc, __fmul_rn(vr[jj], xr[jj * PIPE_KC]));
       }
     }
-    if (loader) cp_wait<0>();
-    __syncthreads();  // the ring is reused by the next column block
+    if (loader || warp == 1) cp_wait<0>();
+    __syncthreads();  // the rings are reused by the next item
     if ((int)threadIdx.x < kc) Y[r * ldy + c0 + threadIdx.x] = acc;
-  }
   }
 }
 
@@ -548,7 +628,9 @@ template <class T, class RP, class CI>
 struct SpmmOp {
   static int run(int64_t nrows, int64_t nnz, int64_t k, const void* rowptr, const void* colind,
                  const void* values, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                 cudaStream_t st) {
+                 cudaStream_t st, const void* W = nullptr) {
+    // W != nullptr: fused GCN layer (fp32, k = 64 through the batch kernel;
+    // gcn_layer checks the preconditions), Y is H
     const int64_t blocks = (nrows + SPMM_WARPS - 1) / SPMM_WARPS;
     if (blocks > 0x7fffffffLL) return fail(LAPIS_B200_ERR_ARG, "spmm: too many rows");
     const bool grp = (k < 64) && (k % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
@@ -565,8 +647,23 @@ struct SpmmOp {
       if (gblocks < 1) gblocks = 1;
 #define LB_BAT(CC) spmm_batch_kernel<T, RP, CI, CC, 8><<<(unsigned)gblocks, 256, 0, st>>>( \
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy)
-      if (cpl == 4) LB_BAT(4); else if (cpl == 2) LB_BAT(2); else LB_BAT(1);
+      bool fused = false;
+      if constexpr (std::is_same<T, float>::value) {
+        if (W) {
+          if (cpl != 2 || k != GCN_F) return fail(LAPIS_B200_ERR_ARG, "gcn fused: k must be 64");
+          spmm_batch_kernel<float, RP, CI, 2, 8, true><<<(unsigned)gblocks, 256, 0, st>>>(
+              nrows, k, (const RP*)rowptr, (const CI*)colind, (const float*)values,
+              (const float*)X, ldx, (float*)Y, ldy, (const float*)W);
+          fused = true;
+        }
+      }
+      if (!fused) {
+        if (W) return fail(LAPIS_B200_ERR_ARG, "gcn fused: fp32 only");
+        if (cpl == 4) LB_BAT(4); else if (cpl == 2) LB_BAT(2); else LB_BAT(1);
+      }
 #undef LB_BAT
+    } else if (W) {
+      return fail(LAPIS_B200_ERR_ARG, "gcn fused: needs the batch kernel's layout");
     } else if (grp) {
       const int64_t lanes_per_row = k >= 64 ? 16 : (k >= 32 ? 8 : (k >= 16 ? 4 : (k >= 8 ? 2 : 1)));
       int64_t gblocks = (nrows * lanes_per_row + 255) / 256;
@@ -615,17 +712,24 @@ struct SpmmOp {
       rc = check_launch("long_rows_list_kernel");
     }
     if constexpr (std::is_same<T, float>::value) {
-      constexpr size_t pipe_smem = (size_t)PIPE_NS * PIPE_SEQ * (PIPE_KC + 1) * sizeof(float);
+      constexpr size_t pipe_smem = pipe_smem_bytes<CI>();
       if (rc == LAPIS_B200_OK)
         rc = check_cuda(cudaFuncSetAttribute(spmm_seq_long_pipe_kernel<RP, CI>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pipe_smem), "smem attr (seq pipe)");
       if (rc == LAPIS_B200_OK) {
-        const int64_t g = cap < sms ? cap : sms;
+        const int64_t items = cap * ((k + PIPE_KC - 1) / PIPE_KC);
+        const int64_t g = items < (int64_t)sms * 2 ? items : (int64_t)sms * 2;
         spmm_seq_long_pipe_kernel<RP, CI><<<(unsigned)g, 256, pipe_smem, st>>>(
             k, (const RP*)rowptr, (const CI*)colind, (const float*)values, (const float*)X, ldx,
             (float*)Y, ldy, lr);
         rc = check_launch("spmm_seq_long_pipe_kernel");
+      }
+      if (rc == LAPIS_B200_OK && W) {
+        const int64_t g = (cap + 7) / 8 < sms ? (cap + 7) / 8 : sms;
+        gcn_long_rows_epilogue_kernel<<<(unsigned)g, 256, 0, st>>>((const float*)W, (float*)Y,
+                                                                     ldy, lr);
+        rc = check_launch("gcn_long_rows_epilogue_kernel");
       }
       cudaFreeAsync(ws, st);
       return rc;
@@ -662,6 +766,20 @@ struct SpmmOp {
     return rc;
   }
 };
+
+// GCN layer H = relu((A X) W) in one pass over A (fp32, fin = fout = 64; the
+// caller checks): the batch kernel applies W and the ReLU to each finished row
+int spmm_gcn_fused(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes,
+                   const void* colind, int ci_bytes, const void* values, const void* X,
+                   int64_t ldx, const void* W, void* H, int64_t ldh, cudaStream_t st) {
+  if (rp_bytes == 8 && ci_bytes == 4)
+    return SpmmOp<float, int64_t, int32_t>::run(nrows, nnz, GCN_F, rowptr, colind, values, X, ldx, H, ldh, st, W);
+  if (rp_bytes == 8 && ci_bytes == 8)
+    return SpmmOp<float, int64_t, int64_t>::run(nrows, nnz, GCN_F, rowptr, colind, values, X, ldx, H, ldh, st, W);
+  if (rp_bytes == 4 && ci_bytes == 4)
+    return SpmmOp<float, int32_t, int32_t>::run(nrows, nnz, GCN_F, rowptr, colind, values, X, ldx, H, ldh, st, W);
+  return SpmmOp<float, int32_t, int64_t>::run(nrows, nnz, GCN_F, rowptr, colind, values, X, ldx, H, ldh, st, W);
+}
 
 int spmm_csr(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const void* rowptr,
              int rp_bytes, const void* colind, int ci_bytes, const void* values, const void* X,

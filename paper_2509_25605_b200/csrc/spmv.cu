@@ -25,10 +25,16 @@
 //    mapping of golden/cpp/spmv.hpp:45-66 — one row per VL lanes
 //    (Kokkos thread -> sub-warp, vector -> lane), ThreadVectorRange reduce as
 //    a shuffle tree, single(PerThread) store by lane 0.
+//
+// 3. spmv_warpblock_kernel (plans of regular, monotone, short-row structures):
+//    32 rows per warp, their contiguous entry range streamed with coalesced
+//    loads into a warp-private shared-memory window, each lane folding its own
+//    row in ascending order (bit-identical).
 #include "common.cuh"
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 namespace lapis_b200 {
@@ -36,6 +42,11 @@ namespace lapis_b200 {
 constexpr int TILE_KEYS = 1024;                   // rows + nonzeros owned per tile (plan grain)
 constexpr int LONG_ROW = 512;                     // last-row length handled in shared memory
 constexpr int TILE_CAP = TILE_KEYS + LONG_ROW;    // products staged per tile
+// plan: mean row length below which the warp-block kernel is chosen by default.
+// 0 = never: measured on B200 (C1 5-point: 35.7 us vs 30.1 us for the VL = 1
+// vector kernel; C5 exact mode 4.35 vs 4.27 TB/s), so it is only selected by
+// LAPIS_B200_SPMV_KERNEL=wb
+constexpr double WARPBLOCK_MAX_MEAN = 0.0;
 
 // ---------------------------------------------------------------- plan
 // tile_row[c]  = first row owned by tile c (c in [0, ntiles]; tile_row[ntiles] = nrows)
@@ -358,22 +369,87 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
   }
 }
 
-// structure analysis for the plan: longest row
+// ------------------------------------------------------- warp-block kernel
+// A warp owns 32 consecutive rows, whose entries form ONE contiguous range
+// [rowptr[r0], rowptr[r0+32]) when rowptr is monotone (the plan checks).  The
+// range is streamed in rounds of 32*U entries: each lane issues U coalesced
+// colind/values loads and U x gathers up front (all independent, so a warp has
+// 3U loads in flight), stores the products in a warp-private shared-memory
+// window, and then each lane folds ITS row's products of the window in
+// ascending j.  Every row sum is therefore the reference's sequential sum bit
+// for bit (interp.py:808-811), whatever the row lengths, while every global
+// load instruction reads 32 consecutive entries.  Short regular rows (C1: 5
+// per row) are the case the vector kernel serves worst: one row per lane there
+// reads 5 strided entries with about 2 loads in flight per thread.
+template <class T, class RP, class CI, int U>
+__global__ void __launch_bounds__(256)
+spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
+                      const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
+  constexpr int CAP = 32 * U;
+  __shared__ T win[8][CAP];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T* __restrict__ my = win[w];
+  const int64_t nblk = (nrows + 31) >> 5;
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t blk = (int64_t)blockIdx.x * 8 + w; blk < nblk; blk += stride) {
+    const int64_t row = (blk << 5) + lane;
+    const int64_t last = min(nrows, (blk << 5) + 32);
+    int64_t b = 0, e = 0;
+    if (row < nrows) {
+      b = (int64_t)rowptr[row];
+      e = (int64_t)rowptr[row + 1];
+    }
+    const int64_t lo = __shfl_sync(0xffffffffu, b, 0);
+    const int64_t hi = (int64_t)rowptr[last];  // one line, shared by the warp
+    if (row >= nrows) b = e = hi;
+    T acc = Arith<T>::zero();
+    for (int64_t base = lo; base < hi; base += CAP) {
+      CI c[U];
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = base + u * 32 + lane;
+        c[u] = j < hi ? colind[j] : CI(0);
+        v[u] = j < hi ? values[j] : T(0);
+      }
+      T p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = base + u * 32 + lane;
+        p[u] = j < hi ? __ldg(x + (int64_t)c[u]) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) my[u * 32 + lane] = Arith<T>::mul(v[u], p[u]);
+      __syncwarp();
+      const int64_t s = max(b, base), t = min(e, base + CAP);
+      for (int64_t j = s; j < t; ++j) acc = Arith<T>::add(acc, my[j - base]);
+      __syncwarp();
+    }
+    if (row < nrows) y[row] = acc;
+  }
+}
+
+// structure analysis for the plan: longest row, and whether rowptr is monotone
+// (stats[1] != 0 when some row has rowptr[r+1] < rowptr[r])
 template <class RP>
 __global__ void row_stats_kernel(int64_t nrows, const RP* __restrict__ rowptr,
-                                 unsigned long long* __restrict__ max_len) {
+                                 unsigned long long* __restrict__ stats) {
   int64_t local = 0;
+  int desc = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t len = (int64_t)rowptr[r + 1] - (int64_t)rowptr[r];
     local = len > local ? len : local;
+    desc |= len < 0;
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     const int64_t o = __shfl_xor_sync(0xffffffffu, local, off);
     local = o > local ? o : local;
   }
-  if ((threadIdx.x & 31) == 0 && local > 0) atomicMax(max_len, (unsigned long long)local);
+  desc = __any_sync(0xffffffffu, desc);
+  if ((threadIdx.x & 31) == 0 && local > 0) atomicMax(stats, (unsigned long long)local);
+  if ((threadIdx.x & 31) == 0 && desc) atomicOr(stats + 1, 1ull);
 }
 
 // ================================================================ host side
@@ -384,6 +460,7 @@ struct CsrPlanImpl {
   int64_t max_len = 0;          // longest row
   int exact_vl = 0;             // > 0: regular structure -> vector kernel with this VL
   int exact = 0;                // 1: fp64 / int rows folded in the reference order too
+  int warpblock = 0;            // 1: regular monotone structure -> warp-block kernel
 };
 
 static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
@@ -469,6 +546,30 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
   return check_launch("spmv_vector_kernel");
 }
 
+template <class T, class RP, class CI>
+static int launch_warpblock_t(int64_t nrows, const void* rowptr, const void* colind,
+                              const void* values, const void* x, void* y, cudaStream_t st) {
+  auto kern = spmv_warpblock_kernel<T, RP, CI, 8>;
+  static thread_local int configured_dev = -1;
+  static thread_local int ctas_per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {  // one resident wave of the persistent grid
+    LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, 256, 0),
+                      "occupancy"));
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+    configured_dev = dev;
+  }
+  const int64_t nblk = (nrows + 31) / 32;
+  int64_t blocks = (nblk + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * ctas_per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, 256, 0, st>>>(
+      nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y);
+  return check_launch("spmv_warpblock_kernel");
+}
+
 template <class T, class RP, class CI, bool EXACT>
 static int dispatch_vl(int vl, int64_t nrows, const void* rowptr, const void* colind,
                        const void* values, const void* x, void* y, cudaStream_t st) {
@@ -514,6 +615,13 @@ struct VecOp {
   static int run(int vl, int64_t nrows, const void* rp, const void* ci, const void* v,
                  const void* x, void* y, cudaStream_t st) {
     return dispatch_vl<T, RP, CI, false>(vl, nrows, rp, ci, v, x, y, st);
+  }
+};
+template <class T, class RP, class CI>
+struct WarpBlockOp {
+  static int run(int64_t nrows, const void* rp, const void* ci, const void* v, const void* x,
+                 void* y, cudaStream_t st) {
+    return launch_warpblock_t<T, RP, CI>(nrows, rp, ci, v, x, y, st);
   }
 };
 template <class T, class RP, class CI>
@@ -563,8 +671,8 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
 // key-balanced tile kernel.  One device->host read at plan creation.
 static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaStream_t st) {
   unsigned long long* d = nullptr;
-  LB_TRY(check_cuda(cudaMallocAsync((void**)&d, sizeof(unsigned long long), st), "alloc(stats)"));
-  int rc = check_cuda(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st), "memset(stats)");
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&d, 2 * sizeof(unsigned long long), st), "alloc(stats)"));
+  int rc = check_cuda(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), st), "memset(stats)");
   if (rc == LAPIS_B200_OK) {
     const int64_t blocks = std::min<int64_t>((p->nrows + 255) / 256, (int64_t)num_sms() * 8);
     if (rp_bytes == 8)
@@ -573,13 +681,14 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
       row_stats_kernel<int32_t><<<(unsigned)blocks, 256, 0, st>>>(p->nrows, (const int32_t*)rowptr, d);
     rc = check_launch("row_stats_kernel");
   }
-  unsigned long long h = 0;
+  unsigned long long h[2] = {0, 0};
   if (rc == LAPIS_B200_OK)
-    rc = check_cuda(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "stats D2H");
+    rc = check_cuda(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "stats D2H");
   if (rc == LAPIS_B200_OK) rc = check_cuda(cudaStreamSynchronize(st), "stats sync");
   cudaFreeAsync(d, st);
   if (rc != LAPIS_B200_OK) return rc;
-  p->max_len = (int64_t)h;
+  p->max_len = (int64_t)h[0];
+  const bool monotone = h[1] == 0;
   const double mean = p->nrows > 0 ? (double)p->nnz / (double)p->nrows : 0.0;
   int vl = 1;
   while (vl < 8 && (double)(vl * 2) * 6.0 <= mean) vl *= 2;
@@ -589,6 +698,13 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
   p->exact_vl = (force && vl > 0) ? vl : (regular ? vl : 0);
   const char* ex = getenv("LAPIS_B200_SPMV_EXACT");
   p->exact = (ex && atoi(ex) != 0) ? 1 : 0;
+  // warp-block kernel: regular, monotone structures with short rows
+  // (LAPIS_B200_SPMV_KERNEL = wb / vec forces the choice for tuning runs)
+  const char* kf = getenv("LAPIS_B200_SPMV_KERNEL");
+  bool wb = regular && monotone && !force && mean < WARPBLOCK_MAX_MEAN;
+  if (kf && !strcmp(kf, "wb")) wb = monotone;
+  if (kf && !strcmp(kf, "vec")) wb = false;
+  p->warpblock = wb ? 1 : 0;
   return LAPIS_B200_OK;
 }
 
@@ -623,7 +739,7 @@ int csr_plan_info(void* plan, int64_t* out4) {
   out4[0] = p->max_len;
   out4[1] = p->exact_vl;
   out4[2] = p->ntiles;
-  out4[3] = p->exact;
+  out4[3] = p->exact | (p->warpblock << 1);
   return LAPIS_B200_OK;
 }
 
@@ -648,6 +764,9 @@ int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
   if (!p) return fail(LAPIS_B200_ERR_ARG, "spmv: null plan");
   LB_TRY(validate(p->nrows, 0, p->nnz, rowptr, rp_bytes, colind, ci_bytes, values, x, y, dtype));
   if (p->nrows == 0) return LAPIS_B200_OK;
+  if (p->warpblock)  // reference order: exact for every dtype and mode
+    return dispatch_types<WarpBlockOp>(dtype, rp_bytes, ci_bytes, p->nrows, rowptr, colind,
+                                       values, x, y, st);
   if (p->exact_vl > 0) {
     // fp32 always folds in the reference order (its 1e-5 contract cannot absorb
     // reassociation on long rows); fp64 / ints take the emitted-mapping tree

@@ -118,11 +118,13 @@ class CsrPlan:
         """The analysis result: longest row and the kernel the plan dispatches to."""
         out = (C.c_int64 * 4)()
         check(_capi.lib().lapis_b200_csr_plan_info(self._handle, out), "csr_plan_info")
-        vl, exact = int(out[1]), bool(out[3])
+        vl, exact, wb = int(out[1]), bool(out[3] & 1), bool(out[3] & 2)
         kind = "exact" if exact else "tree (exact for f32)"
+        kernel = (f"spmv_vector_kernel<VL={vl}, {kind}>" if vl else "spmv_tile_kernel")
+        if wb:
+            kernel = "spmv_warpblock_kernel (exact)"
         return {"max_row_len": int(out[0]), "vector_length": vl, "exact": exact,
-                "ntiles": int(out[2]),
-                "kernel": f"spmv_vector_kernel<VL={vl}, {kind}>" if vl else "spmv_tile_kernel"}
+                "warpblock": wb, "ntiles": int(out[2]), "kernel": kernel}
 
     def spmv(self, colind, values, x, y=None, *, stream=None) -> torch.Tensor:
         for t, n in ((colind, "colind"), (values, "values"), (x, "x")):

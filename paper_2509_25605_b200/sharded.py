@@ -170,3 +170,62 @@ class RowBlockSpmv:
                 self.plans[(lo, hi)].spmv(self.colind, self.values, x_full, y_local[lo:hi],
                                           stream=stream)
         return y_local
+
+
+# --------------------------------------------------------------------- SpMM
+def equal_row_ranges(nrows: int, world: int) -> list[tuple[int, int]]:
+    """Row blocks of exactly ceil(nrows / world) rows (the last one shorter), so
+    that every rank's block occupies the same-sized slot of an all-gathered
+    buffer and a GLOBAL row index addresses that buffer directly."""
+    c = -(-nrows // world) if world > 0 else 0
+    return [(min(nrows, r * c), min(nrows, (r + 1) * c)) for r in range(world)]
+
+
+class RowBlockSpmm:
+    """Y_local = A[row_begin:row_end, :] X for a row-sharded dense operand X
+    (SURVEY 8(e), config 3 / the GCN features): rank r owns the rows
+    [r*c, r*c + c) of A, X and Y (c = ceil(N / world)), colind stays GLOBAL.
+
+    The exchange step is one NCCL all-gather of X into a [world*c, k] buffer
+    (in place: this rank's slot is the send buffer), after which the local
+    SpMM kernel reads any X row by its global index.  A power-law matrix
+    references essentially every column from every shard, so the halo
+    exchange of RowBlockSpmv would degenerate into the same all-gather; the
+    collective is used directly (NVLS-capable over NVSwitch).  Rows are never
+    split, so every Y entry is the reference's ascending sum (bit-identical to
+    one GPU)."""
+
+    def __init__(self, rowptr: torch.Tensor, colind: torch.Tensor, values: torch.Tensor,
+                 nrows_global: int, k: int, rank: int, world: int, group=None):
+        self.rowptr, self.colind, self.values = rowptr, colind, values
+        self.N, self.k, self.rank, self.world, self.group = nrows_global, k, rank, world, group
+        self.ranges = equal_row_ranges(nrows_global, world)
+        self.row_begin, self.row_end = self.ranges[rank]
+        self.chunk = -(-nrows_global // world)
+        self.nnz = int(rowptr[-1].item() - rowptr[0].item())
+        self.X_full = torch.zeros((world * self.chunk, k), dtype=values.dtype,
+                                  device=values.device)
+
+    @property
+    def x_local(self) -> torch.Tensor:
+        """This rank's rows of X (write them here before a multiply)."""
+        return self.X_full[self.rank * self.chunk:self.rank * self.chunk
+                           + (self.row_end - self.row_begin)]
+
+    @property
+    def gather_bytes(self) -> int:
+        """Bytes this rank receives per all-gather."""
+        return (self.world - 1) * self.chunk * self.k * self.X_full.element_size()
+
+    def gather(self) -> None:
+        if self.world > 1:
+            slot = self.X_full[self.rank * self.chunk:(self.rank + 1) * self.chunk]
+            dist.all_gather_into_tensor(self.X_full, slot, group=self.group)
+
+    def multiply(self, Y_local: torch.Tensor, stream=None, replicated: bool = False):
+        """All-gather X (unless it is already replicated), then the local SpMM."""
+        from .kernels import spmm_csr
+        if not replicated:
+            self.gather()
+        return spmm_csr(self.rowptr, self.colind, self.values, self.X_full[:self.N], Y_local,
+                        nnz=self.nnz, stream=stream)

@@ -35,3 +35,19 @@ def test_gcn_hub_rows_bitexact(cuda_device, fin, fout):
     W = rng.uniform(-1 / 8, 1 / 8, (fin, fout)).astype(np.float32)
     H = lb.gcn_layer(cu(rowptr), cu(colind), cu(values), cu(X), cu(W)).cpu().numpy()
     assert bits_equal(H, O.gcn(rowptr, colind, values, X, W))
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_gcn_fused_and_two_stage_bitexact(cuda_device, monkeypatch, fused):
+    # fin = fout = 64 fp32: the fused single-pass kernel (opt-in) and the
+    # two-stage default give the reference's bits, hub rows included
+    monkeypatch.setenv("LAPIS_B200_GCN_FUSED", fused)
+    rng = np.random.default_rng(11)
+    rowptr, colind, values = ragged_csr(rng, 4100, 6000, max_len=30, empty_every=13,
+                                        long_rows={0: 5999, 77: 2049, 4099: 4000},
+                                        dtype=np.float32)
+    values = np.abs(values)
+    X = rng.uniform(0, 1, (6000, 64)).astype(np.float32)
+    W = rng.uniform(-1 / 8, 1 / 8, (64, 64)).astype(np.float32)
+    H = lb.gcn_layer(cu(rowptr), cu(colind), cu(values), cu(X), cu(W)).cpu().numpy()
+    assert bits_equal(H, O.gcn(rowptr, colind, values, X, W))

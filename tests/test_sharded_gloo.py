@@ -79,3 +79,53 @@ def test_sharded_exchange_and_reassembly(world, points, n):
         r0, r1 = ranges[rank]
         assert 0 <= a <= b <= r1 - r0
         assert (b - a) >= (r1 - r0) - 2 * halo
+
+
+def _spmm_worker(rank, world, port, nrows, k, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(__file__))
+        from matrices import powerlaw_csr
+        from oracle import oracle as O
+        rowptr, colind, values = powerlaw_csr(np.random.default_rng(7), nrows, mean=6.0)
+        X = np.random.default_rng(8).uniform(-1, 1, (nrows, k))
+        ranges = sharded.equal_row_ranges(nrows, world)
+        r0, r1 = ranges[rank]
+        lrp = torch.from_numpy(rowptr[r0:r1 + 1] - rowptr[r0])
+        lci = torch.from_numpy(colind[rowptr[r0]:rowptr[r1]])
+        lv = torch.from_numpy(values[rowptr[r0]:rowptr[r1]])
+        op = sharded.RowBlockSpmm(lrp, lci, lv, nrows, k, rank, world)
+        assert (op.row_begin, op.row_end) == (r0, r1)
+        op.x_local.copy_(torch.from_numpy(X[r0:r1]))
+        op.gather()
+        # every rank now holds all of X at its global row indices
+        assert np.array_equal(op.X_full[:nrows].numpy(), X)
+        Y = O.spmm_csr(lrp.numpy(), lci.numpy(), lv.numpy(), op.X_full[:nrows].numpy())
+        q.put((rank, Y.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nrows", [(2, 301), (3, 250)])
+def test_sharded_spmm_allgather_reassembly(world, nrows):
+    from matrices import powerlaw_csr
+    from oracle import oracle as O
+    k = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + world * 10 + nrows % 7
+    procs = [ctx.Process(target=_spmm_worker, args=(r, world, port, nrows, k, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rowptr, colind, values = powerlaw_csr(np.random.default_rng(7), nrows, mean=6.0)
+    X = np.random.default_rng(8).uniform(-1, 1, (nrows, k))
+    want = O.spmm_csr(rowptr, colind, values, X)
+    got = np.concatenate([np.frombuffer(r[1], dtype=np.float64).reshape(-1, k) for r in res])
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

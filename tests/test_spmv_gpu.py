@@ -212,3 +212,40 @@ def test_plan_picks_exact_vector_for_stencils(cuda_device):
     rng = np.random.default_rng(5)
     rowptr, colind, values = powerlaw_csr(rng, 20000, mean=12.0)
     assert lb.CsrPlan(cu(rowptr)).info()["vector_length"] == 0  # irregular -> tile kernel
+
+
+@pytest.mark.parametrize("nrows", [1, 31, 33, 3000])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int64, np.int32])
+def test_warpblock_kernel_bitexact(cuda_device, monkeypatch, nrows, dtype):
+    # warp-block kernel forced on ragged rows (empty rows, rows far longer than
+    # its 256-entry window): every row is the reference's sequential sum
+    monkeypatch.setenv("LAPIS_B200_SPMV_KERNEL", "wb")
+    rng = np.random.default_rng(nrows)
+    longs = {0: 700, nrows - 1: 1300} if nrows > 2 else {}
+    rowptr, colind, values = ragged_csr(rng, nrows, 2500, max_len=20, empty_every=7,
+                                        long_rows=longs, dtype=dtype)
+    x = (rng.integers(-9, 9, 2500) if np.issubdtype(dtype, np.integer)
+         else rng.uniform(-1, 1, 2500)).astype(dtype)
+    plan = lb.CsrPlan(cu(rowptr))
+    assert plan.info()["warpblock"], plan.info()
+    y = host(plan.spmv(cu(colind), cu(values), cu(x)))
+    assert bits_equal(y, O.spmv_csr(rowptr, colind, values, x))
+
+
+def test_warpblock_offset_rowptr(cuda_device, monkeypatch):
+    # a row slice whose rowptr does not start at 0 (a shard's view)
+    monkeypatch.setenv("LAPIS_B200_SPMV_KERNEL", "wb")
+    rp, ci, v = lb.synth_stencil(5, 70)
+    rph, cih, vh = host(rp), host(ci), host(v)
+    r0, r1 = 101, 4000
+    sub = rp[r0:r1 + 1]
+    plan = lb.CsrPlan(sub)
+    assert plan.info()["warpblock"]
+    x = np.random.default_rng(3).uniform(-1, 1, rph.size - 1)
+    y = host(plan.spmv(ci, v, cu(x)))
+    want = O.spmv_csr(rph, cih, vh, x)[r0:r1]
+    assert bits_equal(y, want)
+    # a descending rowptr entry rules the warp-block kernel out
+    bad = rph[:50].copy()
+    bad[10] = bad[12]
+    assert not lb.CsrPlan(cu(bad)).info()["warpblock"]
