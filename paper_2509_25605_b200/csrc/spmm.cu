@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(256, 4)
 spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                   const CI* __restrict__ colind, const T* __restrict__ values,
                   const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
-                  const T* __restrict__ W = nullptr) {
+                  const T* __restrict__ W = nullptr,
+                  unsigned long long* __restrict__ next = nullptr) {
   const int lane = threadIdx.x & 31;
   // EPI (fp32, k = 64, CPL = 2): Y is H, each finished row goes through the
   // GCN epilogue with W staged in shared memory
@@ -260,7 +261,17 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
   };
   const int64_t nbatch = (nrows + 31) >> 5;
   const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t bt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; bt < nbatch; bt += wstride) {
+  // batches of 32 rows are handed out one at a time from a global counter
+  // (`next`, zeroed per call): row lengths vary by orders of magnitude, and a
+  // static grid-stride split leaves SMs with finished warps that cannot take
+  // a new CTA until the slowest warp of theirs is done
+  auto grab = [&]() -> int64_t {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(next, 1ull);
+    return (int64_t)__shfl_sync(0xffffffffu, t, 0);
+  };
+  for (int64_t bt = next ? grab() : (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+       bt < nbatch; bt = next ? grab() : bt + wstride) {
     const int64_t r0 = bt << 5;
     const int nr = (int)((nrows - r0) < 32 ? (nrows - r0) : 32);
     const int64_t rp_l = (int64_t)rowptr[r0 + (lane < nr ? lane : nr)];
@@ -624,6 +635,16 @@ inline bool spmm_force_row() {
   return v == 1;
 }
 
+// LAPIS_B200_SPMM_STATIC=1: static grid-stride batch assignment (A/B runs)
+inline bool spmm_static() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LAPIS_B200_SPMM_STATIC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <class T, class RP, class CI>
 struct SpmmOp {
   static int run(int64_t nrows, int64_t nnz, int64_t k, const void* rowptr, const void* colind,
@@ -645,15 +666,26 @@ struct SpmmOp {
       const int64_t cap = (int64_t)num_sms() * 8;
       if (gblocks > cap) gblocks = cap;
       if (gblocks < 1) gblocks = 1;
+      unsigned long long* next = nullptr;
+      if (!spmm_static()) {
+        LB_TRY(check_cuda(cudaMallocAsync((void**)&next, sizeof(*next), st), "alloc(spmm counter)"));
+        const int mrc = check_cuda(cudaMemsetAsync(next, 0, sizeof(*next), st), "memset(spmm counter)");
+        if (mrc != LAPIS_B200_OK) { cudaFreeAsync(next, st); return mrc; }
+      }
+      struct FreeNext {
+        unsigned long long* p; cudaStream_t s;
+        ~FreeNext() { if (p) cudaFreeAsync(p, s); }
+      } free_next{next, st};
 #define LB_BAT(CC) spmm_batch_kernel<T, RP, CI, CC, 8><<<(unsigned)gblocks, 256, 0, st>>>( \
-          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy)
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, \
+          nullptr, next)
       bool fused = false;
       if constexpr (std::is_same<T, float>::value) {
         if (W) {
           if (cpl != 2 || k != GCN_F) return fail(LAPIS_B200_ERR_ARG, "gcn fused: k must be 64");
           spmm_batch_kernel<float, RP, CI, 2, 8, true><<<(unsigned)gblocks, 256, 0, st>>>(
               nrows, k, (const RP*)rowptr, (const CI*)colind, (const float*)values,
-              (const float*)X, ldx, (float*)Y, ldy, (const float*)W);
+              (const float*)X, ldx, (float*)Y, ldy, (const float*)W, next);
           fused = true;
         }
       }
