@@ -931,8 +931,12 @@ def main():
         torch.cuda.synchronize()
         ev0.record(stream)
         for s0, s1 in step_events:
-            if wl.flush is not None:
-                wl.flush.fill_(1)
+            if wl.flush is None:
+                # back-to-back steps bracketed by ev0 / ev1 only: an event pair
+                # per step would add its own gaps to a ~20 us step (config 1)
+                wl.step()
+                continue
+            wl.flush.fill_(1)
             s0.record(stream)
             wl.step()
             s1.record(stream)
@@ -940,10 +944,10 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
-    kern = [a.elapsed_time(b) / 1e3 for a, b in per_step]
     # with an L2 flush between steps, the step time excludes the flush
-    t_local = (ev0.elapsed_time(ev1) / 1e3 / args.steps if wl.flush is None
-               else float(np.mean(kern)))
+    total = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    kern = [a.elapsed_time(b) / 1e3 for a, b in per_step] if per_step else [total]
+    t_local = total if wl.flush is None else float(np.mean(kern))
     t = max_over_ranks(t_local, world)
     kern_avg = max_over_ranks(float(np.mean(kern)), world)
     scale = 1e9 if wl.unit == "GB/s" else 1e12

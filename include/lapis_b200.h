@@ -119,6 +119,36 @@ int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int r
 int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out4);
 int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact);
 
+/* Row-block-sharded SpMV over NCCL (SURVEY 8(b) "sharded spmv_csr_rowblock with
+ * an ncclComm_t", 8(e); the native counterpart of sharded.py's RowBlockSpmv).
+ * Rank `rank` of `world` owns the global rows [row_begins[rank],
+ * row_begins[rank+1]) (row_begins has world + 1 entries); its rowptr is the
+ * shard's, rebased to 0, colind holds GLOBAL column indices, x_full is indexed by
+ * global column with this rank's slice in place.  Creation (synchronous,
+ * collective over `comm`) finds, per owner, the interval of columns the shard
+ * reads, all-gathers those intervals and splits the shard at the longest run
+ * of rows with only local columns.  Each multiply moves exactly the needed x
+ * slabs with ncclSend/ncclRecv on a private stream, overlapped with the
+ * interior rows, then multiplies the boundary rows: results are bit-identical
+ * to the unsharded multiply.  comm may be NULL when world == 1.
+ * The communicator: lapis_b200_nccl_unique_id on one rank, broadcast its 128
+ * bytes, lapis_b200_nccl_comm_init on every rank (NCCL is dlopen'ed).
+ * rowblock_info: out[0..1] = interior run [a, b); then per peer p
+ * out[2+4p .. 5+4p] = needs lo, hi, sends lo, hi. */
+typedef struct lapis_b200_rowblock_s* lapis_b200_rowblock;
+int lapis_b200_nccl_unique_id(void* out128);
+int lapis_b200_nccl_comm_init(const void* id128, int world, int rank, void** out_comm);
+int lapis_b200_nccl_comm_destroy(void* comm);
+int lapis_b200_rowblock_create(void* comm, int rank, int world, const int64_t* row_begins,
+                               const void* rowptr, int rowptr_bytes, const void* colind,
+                               int colind_bytes, int64_t nnz, int exact, void* stream,
+                               lapis_b200_rowblock* out);
+int lapis_b200_rowblock_info(lapis_b200_rowblock rb, int64_t* out);
+int lapis_b200_spmv_csr_rowblock(lapis_b200_rowblock rb, const void* rowptr, int rowptr_bytes,
+                                 const void* colind, int colind_bytes, const void* values,
+                                 void* x_full, void* y_local, int dtype, void* stream);
+int lapis_b200_rowblock_destroy(lapis_b200_rowblock rb);
+
 /* Structure validation (synchronous: reads two flags back).  The reference
  * interpreter bounds-checks every load (interp.py:269-276); the tuned kernels
  * do not, so the executor validates a CSR once before using them.

@@ -37,6 +37,14 @@ _SIGNATURES = {
     "lapis_b200_last_error": ([], C.c_char_p),
     "lapis_b200_version": ([], _INT),
     "lapis_b200_init": ([_INT], _INT),
+    "lapis_b200_nccl_unique_id": ([_VP], _INT),
+    "lapis_b200_nccl_comm_init": ([_VP, _INT, _INT, _VP], _INT),
+    "lapis_b200_nccl_comm_destroy": ([_VP], _INT),
+    "lapis_b200_rowblock_create": ([_VP, _INT, _INT, _VP, _VP, _INT, _VP, _INT, _I64, _INT, _VP,
+                                    _VP], _INT),
+    "lapis_b200_rowblock_info": ([_VP, _VP], _INT),
+    "lapis_b200_spmv_csr_rowblock": ([_VP, _VP, _INT, _VP, _INT, _VP, _VP, _VP, _INT, _VP], _INT),
+    "lapis_b200_rowblock_destroy": ([_VP], _INT),
     "lapis_b200_finalize": ([], _INT),
     "lapis_b200_csr_vector_length": ([_I64, _I64, _I64], _I64),
     "lapis_b200_spmv_csr": ([_I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _VP, _INT, _INT,

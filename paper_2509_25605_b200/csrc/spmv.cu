@@ -771,7 +771,9 @@ int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
     // fp32 always folds in the reference order (its 1e-5 contract cannot absorb
     // reassociation on long rows); fp64 / ints take the emitted-mapping tree
     // (ThreadVectorRange reduce) unless exact mode was requested
-    if (p->exact || dtype == LAPIS_B200_F32)
+    // (VL = 1: both are the sequential row sum; the exact kernel's two-entry
+    // unroll keeps more loads in flight — C1 21.5 vs 26 us measured)
+    if (p->exact || dtype == LAPIS_B200_F32 || p->exact_vl == 1)
       return dispatch_types<VecExactOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,
                                         colind, values, x, y, st);
     return dispatch_types<VecOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,

@@ -119,7 +119,7 @@ class CsrPlan:
         out = (C.c_int64 * 4)()
         check(_capi.lib().lapis_b200_csr_plan_info(self._handle, out), "csr_plan_info")
         vl, exact, wb = int(out[1]), bool(out[3] & 1), bool(out[3] & 2)
-        kind = "exact" if exact else "tree (exact for f32)"
+        kind = "exact" if (exact or vl == 1) else "tree (exact for f32)"
         kernel = (f"spmv_vector_kernel<VL={vl}, {kind}>" if vl else "spmv_tile_kernel")
         if wb:
             kernel = "spmv_warpblock_kernel (exact)"

@@ -229,3 +229,90 @@ class RowBlockSpmm:
             self.gather()
         return spmm_csr(self.rowptr, self.colind, self.values, self.X_full[:self.N], Y_local,
                         nnz=self.nnz, stream=stream)
+
+
+# ------------------------------------------------- native (C-ABI) row blocks
+class NcclComm:
+    """A communicator of the backend's own (lapis_b200_nccl_comm_init): rank 0
+    draws the NCCL unique id, the process group broadcasts its 128 bytes."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import ctypes as C
+        from . import _capi
+        from ._capi import check
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            check(_capi.lib().lapis_b200_nccl_unique_id(uid), "nccl_unique_id")
+        if world > 1:
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, 0, group=group)
+            uid = (C.c_char * 128).from_buffer_copy(bytes(t.cpu().tolist()))
+        handle = C.c_void_p()
+        check(_capi.lib().lapis_b200_nccl_comm_init(uid, world, rank, C.byref(handle)),
+              "nccl_comm_init")
+        self.handle, self.rank, self.world = handle, rank, world
+
+    def close(self) -> None:
+        from . import _capi
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            _capi.lib().lapis_b200_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+class NativeRowBlockSpmv:
+    """RowBlockSpmv through the C ABI (lapis_b200_rowblock_*): the same
+    exchange plan, interior/boundary split and overlap, run natively with the
+    backend's own NCCL communicator.  rowptr rebased to 0, colind global."""
+
+    def __init__(self, rowptr: torch.Tensor, colind: torch.Tensor, values: torch.Tensor,
+                 ranges, rank: int, world: int, comm: NcclComm | None = None,
+                 exact: bool = False, stream=None):
+        import ctypes as C
+        from . import _capi
+        from ._capi import check
+        from .kernels import _idx_bytes, _ptr, _stream
+        self.rowptr, self.colind, self.values = rowptr, colind, values
+        self.rank, self.world = rank, world
+        begins = (C.c_int64 * (world + 1))(*([lo for lo, _ in ranges] + [ranges[-1][1]]))
+        nnz = int(rowptr[-1].item())
+        handle = C.c_void_p()
+        check(_capi.lib().lapis_b200_rowblock_create(
+            comm.handle if comm is not None else None, rank, world, begins, _ptr(rowptr),
+            _idx_bytes(rowptr, "rowptr"), _ptr(colind), _idx_bytes(colind, "colind"), nnz,
+            int(bool(exact)), _stream(stream), C.byref(handle)), "rowblock_create")
+        self._handle = handle
+
+    def info(self) -> dict:
+        import ctypes as C
+        from . import _capi
+        from ._capi import check
+        out = (C.c_int64 * (2 + 4 * self.world))()
+        check(_capi.lib().lapis_b200_rowblock_info(self._handle, out), "rowblock_info")
+        v = list(out)
+        return {"interior": (v[0], v[1]),
+                "needs": [(v[2 + 4 * p], v[3 + 4 * p]) for p in range(self.world)],
+                "sends": [(v[4 + 4 * p], v[5 + 4 * p]) for p in range(self.world)]}
+
+    def multiply(self, x_full: torch.Tensor, y_local: torch.Tensor, stream=None) -> torch.Tensor:
+        from . import _capi
+        from ._capi import check
+        from .kernels import _dtype, _idx_bytes, _ptr, _stream
+        check(_capi.lib().lapis_b200_spmv_csr_rowblock(
+            self._handle, _ptr(self.rowptr), _idx_bytes(self.rowptr, "rowptr"), _ptr(self.colind),
+            _idx_bytes(self.colind, "colind"), _ptr(self.values), _ptr(x_full), _ptr(y_local),
+            _dtype(self.values, "values"), _stream(stream)), "spmv_csr_rowblock")
+        return y_local
+
+    def close(self) -> None:
+        from . import _capi
+        if getattr(self, "_handle", None) is not None and self._handle.value:
+            _capi.lib().lapis_b200_rowblock_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

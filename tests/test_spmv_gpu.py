@@ -249,3 +249,31 @@ def test_warpblock_offset_rowptr(cuda_device, monkeypatch):
     bad = rph[:50].copy()
     bad[10] = bad[12]
     assert not lb.CsrPlan(cu(bad)).info()["warpblock"]
+
+
+@pytest.mark.parametrize("points,n", [(27, 14), (5, 90)])
+def test_native_rowblock_world1(cuda_device, points, n):
+    # the C-ABI row-block path with the backend's own NCCL communicator
+    # (world 1 on one GPU): bit-identical to the plan multiply
+    from paper_2509_25605_b200 import sharded
+    rp, ci, v = lb.synth_stencil(points, n)
+    N = rp.numel() - 1
+    comm = sharded.NcclComm(0, 1)
+    op = sharded.NativeRowBlockSpmv(rp, ci, v, [(0, N)], 0, 1, comm, exact=True)
+    info = op.info()
+    assert info["interior"] == (0, N)
+    x = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, N)).cuda()
+    y = torch.empty(N, dtype=torch.float64, device="cuda")
+    op.multiply(x, y)
+    want = O.spmv_csr(host(rp), host(ci), host(v), host(x))
+    assert bits_equal(host(y), want)
+    op.close()
+    comm.close()
+
+
+def test_native_rowblock_rejects_unrebased_rowptr(cuda_device):
+    from paper_2509_25605_b200 import sharded
+    rp, ci, v = lb.synth_stencil(5, 30)
+    sub = rp[100:200 + 1]
+    with pytest.raises(lb.BackendError):
+        sharded.NativeRowBlockSpmv(sub, ci, v, [(100, 200)], 0, 1, None)
