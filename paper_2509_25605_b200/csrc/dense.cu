@@ -109,8 +109,11 @@ gemm_exact_kernel(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int6
 // walking k in the reference order with separately rounded mul / add — the
 // same result as gemm_exact_kernel bit for bit, at ~1 shared load per 16
 // floating-point operations (B read as broadcast 16-byte vectors).
-constexpr int EN_MAX = 64, EN_ROWS = 256, EN_COLS = 16, EN_RPT = 4;
-constexpr size_t EN_SMEM = (size_t)(EN_MAX * EN_MAX + EN_ROWS * (EN_MAX + 1)) * sizeof(float);
+// A is staged TRANSPOSED (AsT[k][row], row pitch EN_ROWS + 4), so a thread's
+// four A values of one k are a single 16-byte shared load: 5 shared loads
+// (1 + 4 of B) per 128 floating-point instructions instead of 8.
+constexpr int EN_MAX = 64, EN_ROWS = 256, EN_COLS = 16, EN_RPT = 4, EN_PITCH = EN_ROWS + 4;
+constexpr size_t EN_SMEM = (size_t)(EN_MAX * EN_MAX + EN_MAX * EN_PITCH) * sizeof(float);
 
 template <bool RELU>
 __global__ void __launch_bounds__(256)
@@ -119,7 +122,7 @@ gemm_exact_narrow_kernel(int64_t m, int n, int k, const float* __restrict__ A, i
                          int64_t ldc) {
   extern __shared__ __align__(16) float en_smem[];
   float* Bs = en_smem;                          // [EN_MAX][EN_MAX]
-  float* As = en_smem + EN_MAX * EN_MAX;        // [EN_ROWS][EN_MAX + 1]
+  float* AsT = en_smem + EN_MAX * EN_MAX;       // [EN_MAX][EN_PITCH]
   for (int t = threadIdx.x; t < EN_MAX * EN_MAX; t += blockDim.x) {
     const int r = t / EN_MAX, c = t % EN_MAX;
     Bs[t] = (r < k && c < n) ? B[(int64_t)r * ldb + c] : 0.0f;
@@ -145,8 +148,8 @@ gemm_exact_narrow_kernel(int64_t m, int n, int k, const float* __restrict__ A, i
       for (int u = 0; u < EN_ROWS * EN_MAX / 4 / 256; ++u) {
         const int t = threadIdx.x + 256 * u;
         const int r = t / (EN_MAX / 4), c4 = (t % (EN_MAX / 4)) * 4;
-        float* d = As + r * (EN_MAX + 1) + c4;
-        d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+        float* d = AsT + c4 * EN_PITCH + r;
+        d[0] = v[u].x; d[EN_PITCH] = v[u].y; d[2 * EN_PITCH] = v[u].z; d[3 * EN_PITCH] = v[u].w;
       }
     } else {
       for (int t0 = 0; t0 < EN_ROWS * EN_MAX; t0 += 256 * 8) {
@@ -160,7 +163,7 @@ gemm_exact_narrow_kernel(int64_t m, int n, int k, const float* __restrict__ A, i
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int t = t0 + threadIdx.x + 256 * u;
-          As[(t / EN_MAX) * (EN_MAX + 1) + t % EN_MAX] = v[u];
+          AsT[(t % EN_MAX) * EN_PITCH + t / EN_MAX] = v[u];
         }
       }
     }
@@ -171,9 +174,8 @@ gemm_exact_narrow_kernel(int64_t m, int n, int k, const float* __restrict__ A, i
 #pragma unroll
       for (int q = 0; q < EN_COLS; ++q) acc[i][q] = 0.0f;
     for (int kk = 0; kk < k; ++kk) {
-      float a[EN_RPT];
-#pragma unroll
-      for (int i = 0; i < EN_RPT; ++i) a[i] = As[(rg * EN_RPT + i) * (EN_MAX + 1) + kk];
+      const float4 a4 = *reinterpret_cast<const float4*>(AsT + kk * EN_PITCH + rg * EN_RPT);
+      const float a[EN_RPT] = {a4.x, a4.y, a4.z, a4.w};
       float bv[EN_COLS];
       const float4* brow = reinterpret_cast<const float4*>(Bs + kk * EN_MAX + cg * EN_COLS);
 #pragma unroll
@@ -186,14 +188,24 @@ gemm_exact_narrow_kernel(int64_t m, int n, int k, const float* __restrict__ A, i
 #pragma unroll
         for (int q = 0; q < EN_COLS; ++q) acc[i][q] = __fadd_rn(acc[i][q], __fmul_rn(a[i], bv[q]));
     }
+    const bool vec_c = (n == EN_MAX) && (ldc % 4 == 0) && ((uintptr_t)C % 16 == 0);
 #pragma unroll
     for (int i = 0; i < EN_RPT; ++i) {
       const int64_t row = r0 + rg * EN_RPT + i;
       if (row >= m) continue;
+      float o[EN_COLS];
 #pragma unroll
-      for (int q = 0; q < EN_COLS; ++q) {
-        const int c = cg * EN_COLS + q;
-        if (c < n) C[row * ldc + c] = RELU ? ((acc[i][q] > 0.0f) ? acc[i][q] : 0.0f) : acc[i][q];
+      for (int q = 0; q < EN_COLS; ++q) o[q] = RELU ? ((acc[i][q] > 0.0f) ? acc[i][q] : 0.0f) : acc[i][q];
+      if (vec_c) {
+        float4* d = reinterpret_cast<float4*>(C + row * ldc + cg * EN_COLS);
+#pragma unroll
+        for (int q = 0; q < EN_COLS / 4; ++q) d[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < EN_COLS; ++q) {
+          const int c = cg * EN_COLS + q;
+          if (c < n) C[row * ldc + c] = o[q];
+        }
       }
     }
   }
