@@ -220,14 +220,30 @@ __global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float*
                                   int64_t lda, float* __restrict__ hi, float* __restrict__ lo,
                                   Guard guard) {
   if (guard_skip(guard)) return;
-  const int64_t total = m * kp;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / kp, j = t % kp;
-    const float a = j < k ? A[i * lda + j] : 0.0f;
-    const float h = tf32_rna(a);
-    hi[t] = h;
-    lo[t] = tf32_rna(a - h);
+  // a CTA per row (grid-stride), 4 consecutive elements per thread: 16-byte
+  // loads when the row pitch allows, 16-byte stores (kp % 4 == 0), no
+  // per-element 64-bit division
+  const bool vec = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0);
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    const float* ar = A + i * lda;
+    float4* hr = reinterpret_cast<float4*>(hi + i * kp);
+    float4* lr = reinterpret_cast<float4*>(lo + i * kp);
+    for (int64_t j4 = threadIdx.x; j4 < kp / 4; j4 += blockDim.x) {
+      const int64_t j = 4 * j4;
+      float4 a;
+      if (vec && j + 3 < k) {
+        a = *reinterpret_cast<const float4*>(ar + j);
+      } else {
+        a.x = j < k ? ar[j] : 0.0f;
+        a.y = j + 1 < k ? ar[j + 1] : 0.0f;
+        a.z = j + 2 < k ? ar[j + 2] : 0.0f;
+        a.w = j + 3 < k ? ar[j + 3] : 0.0f;
+      }
+      const float4 h = make_float4(tf32_rna(a.x), tf32_rna(a.y), tf32_rna(a.z), tf32_rna(a.w));
+      hr[j4] = h;
+      lr[j4] = make_float4(tf32_rna(a.x - h.x), tf32_rna(a.y - h.y), tf32_rna(a.z - h.z),
+                           tf32_rna(a.w - h.w));
+    }
   }
 }
 
@@ -236,21 +252,28 @@ __global__ void split_transpose_kernel(int64_t k, int64_t n, int64_t kp, const f
                                        int64_t ldb, float* __restrict__ hi, float* __restrict__ lo,
                                        Guard guard) {
   if (guard_skip(guard)) return;
-  __shared__ float tile[32][33];
-  const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  // 64 (k) x 64 (n) tile, 256 threads: coalesced 128-byte row loads, 8-byte
+  // stores of consecutive k pairs (kp is a multiple of 4)
+  __shared__ float tile[64][65];
+  const int64_t k0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t kk = k0 + r, nn = n0 + tx;
-    tile[r][tx] = (kk < k && nn < n) ? B[kk * ldb + nn] : 0.0f;
+  for (int r = ty; r < 64; r += 8) {
+    const int64_t kk = k0 + r;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t nn = n0 + tx + 32 * h;
+      tile[r][tx + 32 * h] = (kk < k && nn < n) ? B[kk * ldb + nn] : 0.0f;
+    }
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t nn = n0 + r, kk = k0 + tx;
+  const int64_t kk = k0 + 2 * tx;
+  for (int r = ty; r < 64; r += 8) {
+    const int64_t nn = n0 + r;
     if (nn < n && kk < kp) {
-      const float a = tile[tx][r];
-      const float h = tf32_rna(a);
-      hi[nn * kp + kk] = h;
-      lo[nn * kp + kk] = tf32_rna(a - h);
+      const float a0 = tile[2 * tx][r], a1 = tile[2 * tx + 1][r];
+      const float h0 = tf32_rna(a0), h1 = tf32_rna(a1);
+      *reinterpret_cast<float2*>(hi + nn * kp + kk) = make_float2(h0, h1);
+      *reinterpret_cast<float2*>(lo + nn * kp + kk) = make_float2(tf32_rna(a0 - h0), tf32_rna(a1 - h1));
     }
   }
 }
@@ -307,9 +330,9 @@ int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, i
     const float* Ab = (const float*)A + b * sA;
     const float* Bb = (const float*)B + b * sB;
     float* Cb = (float*)C + b * sC;
-    const int64_t sblocks = std::min<int64_t>((m * kp + 255) / 256, (int64_t)num_sms() * 16);
+    const int64_t sblocks = std::min<int64_t>(m, (int64_t)num_sms() * 16);
     split_rows_kernel<<<(unsigned)sblocks, 256, 0, st>>>(m, k, kp, Ab, lda, ah, al, guard);
-    dim3 tg((unsigned)((n + 31) / 32), (unsigned)((kp + 31) / 32));
+    dim3 tg((unsigned)((n + 63) / 64), (unsigned)((kp + 63) / 64));
     split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl, guard);
     rc = check_launch("tf32 split");
     CUtensorMap mah, mal, mbh, mbl;
