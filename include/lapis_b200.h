@@ -111,11 +111,13 @@ int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int r
  * integer rows as the emitted TeamPolicy mapping (shuffle-tree reduce, the
  * Kokkos ThreadVectorRange semantics), fp32 rows — and every dtype once
  * lapis_b200_csr_plan_set_exact(plan, 1) — folded in the reference's
- * sequential order (bit-identical).  With LAPIS_B200_SPMV_KERNEL=wb a monotone
- * rowptr runs the warp-block kernel instead (32 rows per warp, coalesced entry
- * stream, per-row ascending fold: bit-identical in every mode; measured slower
- * than the vector kernel on the stencils, so not chosen by default).
- * Irregular structures run the tile kernel. */
+ * sequential order (bit-identical).  Irregular structures with a monotone
+ * rowptr run the warp-block kernel (blocks of 32 rows handed out dynamically,
+ * their contiguous entry range streamed with coalesced loads, each row folded
+ * in ascending order by its lane; rows longer than 512 entries folded by the
+ * whole warp as a fixed tree unless exact mode or fp32); other irregular
+ * structures run the row-stream tile kernel (bit-identical for rows <= 512).
+ * LAPIS_B200_SPMV_KERNEL = wb / vec / tile forces a kernel (tuning runs). */
 int lapis_b200_csr_plan_info(lapis_b200_csr_plan plan, int64_t* out4);
 int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact);
 

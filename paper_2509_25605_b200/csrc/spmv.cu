@@ -381,17 +381,26 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
 // load instruction reads 32 consecutive entries.  Short regular rows (C1: 5
 // per row) are the case the vector kernel serves worst: one row per lane there
 // reads 5 strided entries with about 2 loads in flight per thread.
-template <class T, class RP, class CI, int U>
+template <class T, class RP, class CI, int U, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
-                      const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
+                      const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
+                      unsigned long long* __restrict__ next) {
   constexpr int CAP = 32 * U;
   __shared__ T win[8][CAP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   T* __restrict__ my = win[w];
   const int64_t nblk = (nrows + 31) >> 5;
   const int64_t stride = (int64_t)gridDim.x * 8;
-  for (int64_t blk = (int64_t)blockIdx.x * 8 + w; blk < nblk; blk += stride) {
+  // blocks of 32 rows from a per-call counter when given (irregular rows: a
+  // static split leaves SMs idle behind their slowest warp), else grid-stride
+  auto grab = [&]() -> int64_t {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(next, 1ull);
+    return (int64_t)__shfl_sync(0xffffffffu, t, 0);
+  };
+  for (int64_t blk = next ? grab() : (int64_t)blockIdx.x * 8 + w; blk < nblk;
+       blk = next ? grab() : blk + stride) {
     const int64_t row = (blk << 5) + lane;
     const int64_t last = min(nrows, (blk << 5) + 32);
     int64_t b = 0, e = 0;
@@ -422,7 +431,31 @@ spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
       for (int u = 0; u < U; ++u) my[u * 32 + lane] = Arith<T>::mul(v[u], p[u]);
       __syncwarp();
       const int64_t s = max(b, base), t = min(e, base + CAP);
-      for (int64_t j = s; j < t; ++j) acc = Arith<T>::add(acc, my[j - base]);
+      if constexpr (EXACT) {
+        for (int64_t j = s; j < t; ++j) acc = Arith<T>::add(acc, my[j - base]);
+      } else {
+        // a row's segment of more than 32 products in this window (a hub row)
+        // is folded by the whole warp — lane-strided partials, fixed xor
+        // tree, added to the owner's sum in window order (deterministic, the
+        // ThreadVectorRange reduce); shorter segments by their own lane in order
+        // (rows of <= LONG_ROW entries always fold in order: bit-identical,
+        // the tile kernel's contract)
+        const bool coop = (t - s > 32) && (e - b > LONG_ROW);
+        unsigned big = __ballot_sync(0xffffffffu, coop);
+        while (big) {
+          const int owner = __ffs(big) - 1;
+          big &= big - 1;
+          const int64_t os = __shfl_sync(0xffffffffu, s, owner);
+          const int64_t ot = __shfl_sync(0xffffffffu, t, owner);
+          T part = Arith<T>::zero();
+          for (int64_t j = os + lane; j < ot; j += 32) part = Arith<T>::add(part, my[j - base]);
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) part = Arith<T>::add(part, shfl_xor(part, off));
+          if (lane == owner) acc = Arith<T>::add(acc, part);
+        }
+        if (!coop)
+          for (int64_t j = s; j < t; ++j) acc = Arith<T>::add(acc, my[j - base]);
+      }
       __syncwarp();
     }
     if (row < nrows) y[row] = acc;
@@ -460,7 +493,7 @@ struct CsrPlanImpl {
   int64_t max_len = 0;          // longest row
   int exact_vl = 0;             // > 0: regular structure -> vector kernel with this VL
   int exact = 0;                // 1: fp64 / int rows folded in the reference order too
-  int warpblock = 0;            // 1: regular monotone structure -> warp-block kernel
+  int warpblock = 0;            // 1: warp-block kernel (irregular monotone structures)
 };
 
 static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
@@ -548,25 +581,31 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
 
 template <class T, class RP, class CI>
 static int launch_warpblock_t(int64_t nrows, const void* rowptr, const void* colind,
-                              const void* values, const void* x, void* y, cudaStream_t st) {
-  auto kern = spmv_warpblock_kernel<T, RP, CI, 8>;
+                              const void* values, const void* x, void* y, int exact,
+                              unsigned long long* next, cudaStream_t st) {
+  auto kern = exact ? spmv_warpblock_kernel<T, RP, CI, 8, true>
+                    : spmv_warpblock_kernel<T, RP, CI, 8, false>;
   static thread_local int configured_dev = -1;
-  static thread_local int ctas_per_sm = 0;
+  static thread_local int ctas_per_sm[2] = {0, 0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {  // one resident wave of the persistent grid
-    LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, 256, 0),
-                      "occupancy"));
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
+    for (int ex = 0; ex < 2; ++ex) {
+      auto kk = ex ? spmv_warpblock_kernel<T, RP, CI, 8, true> : spmv_warpblock_kernel<T, RP, CI, 8, false>;
+      LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm[ex], kk, 256, 0),
+                        "occupancy"));
+      if (ctas_per_sm[ex] < 1) ctas_per_sm[ex] = 1;
+    }
     configured_dev = dev;
   }
   const int64_t nblk = (nrows + 31) / 32;
   int64_t blocks = (nblk + 7) / 8;
-  const int64_t cap = (int64_t)num_sms() * ctas_per_sm;
+  const int64_t cap = (int64_t)num_sms() * ctas_per_sm[exact ? 1 : 0];
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, 256, 0, st>>>(
-      nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y);
+  if (next) LB_TRY(check_cuda(cudaMemsetAsync(next, 0, sizeof(*next), st), "memset(spmv counter)"));
+  kern<<<(unsigned)blocks, 256, 0, st>>>(nrows, (const RP*)rowptr, (const CI*)colind,
+                                         (const T*)values, (const T*)x, (T*)y, next);
   return check_launch("spmv_warpblock_kernel");
 }
 
@@ -620,8 +659,14 @@ struct VecOp {
 template <class T, class RP, class CI>
 struct WarpBlockOp {
   static int run(int64_t nrows, const void* rp, const void* ci, const void* v, const void* x,
-                 void* y, cudaStream_t st) {
-    return launch_warpblock_t<T, RP, CI>(nrows, rp, ci, v, x, y, st);
+                 void* y, int exact, cudaStream_t st) {
+    // the block counter: a per-call stream-ordered allocation (pool-cached),
+    // so multiplies with one plan on several streams never share it
+    unsigned long long* next = nullptr;
+    LB_TRY(check_cuda(cudaMallocAsync((void**)&next, sizeof(*next), st), "alloc(spmv counter)"));
+    const int rc = launch_warpblock_t<T, RP, CI>(nrows, rp, ci, v, x, y, exact, next, st);
+    cudaFreeAsync(next, st);
+    return rc;
   }
 };
 template <class T, class RP, class CI>
@@ -698,12 +743,14 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
   p->exact_vl = (force && vl > 0) ? vl : (regular ? vl : 0);
   const char* ex = getenv("LAPIS_B200_SPMV_EXACT");
   p->exact = (ex && atoi(ex) != 0) ? 1 : 0;
-  // warp-block kernel: regular, monotone structures with short rows
-  // (LAPIS_B200_SPMV_KERNEL = wb / vec forces the choice for tuning runs)
+  // warp-block kernel: irregular monotone structures (power-law rows: 1.46 vs
+  // 1.73 ms for the tile kernel on config 3's matrix, before the dynamic
+  // blocks and the cooperative hub-row fold); LAPIS_B200_SPMV_KERNEL = wb /
+  // vec / tile forces a choice for tuning runs
   const char* kf = getenv("LAPIS_B200_SPMV_KERNEL");
-  bool wb = regular && monotone && !force && mean < WARPBLOCK_MAX_MEAN;
+  bool wb = monotone && !force && (!regular || mean < WARPBLOCK_MAX_MEAN);
   if (kf && !strcmp(kf, "wb")) wb = monotone;
-  if (kf && !strcmp(kf, "vec")) wb = false;
+  if (kf && (!strcmp(kf, "vec") || !strcmp(kf, "tile"))) wb = false;
   p->warpblock = wb ? 1 : 0;
   return LAPIS_B200_OK;
 }
@@ -721,6 +768,7 @@ int csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rp_bytes
   cudaGetDevice(&p->device);
   int rc = check_cuda(cudaMalloc((void**)&p->tile_row, 2 * (p->ntiles + 1) * sizeof(int64_t)),
                       "cudaMalloc(plan)");
+
   if (rc == LAPIS_B200_OK && nrows > 0)
     rc = launch_partition(nrows, rowptr, rp_bytes, p->ntiles, p->tile_row, st);
   if (rc == LAPIS_B200_OK && nrows > 0) rc = analyse_rows(p, rowptr, rp_bytes, st);
@@ -764,9 +812,10 @@ int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
   if (!p) return fail(LAPIS_B200_ERR_ARG, "spmv: null plan");
   LB_TRY(validate(p->nrows, 0, p->nnz, rowptr, rp_bytes, colind, ci_bytes, values, x, y, dtype));
   if (p->nrows == 0) return LAPIS_B200_OK;
-  if (p->warpblock)  // reference order: exact for every dtype and mode
+  if (p->warpblock)  // rows <= LONG_ROW in order; longer: warp tree unless exact / fp32
     return dispatch_types<WarpBlockOp>(dtype, rp_bytes, ci_bytes, p->nrows, rowptr, colind,
-                                       values, x, y, st);
+                                       values, x, y,
+                                       (p->exact || dtype == LAPIS_B200_F32) ? 1 : 0, st);
   if (p->exact_vl > 0) {
     // fp32 always folds in the reference order (its 1e-5 contract cannot absorb
     // reassociation on long rows); fp64 / ints take the emitted-mapping tree

@@ -122,7 +122,8 @@ class CsrPlan:
         kind = "exact" if (exact or vl == 1) else "tree (exact for f32)"
         kernel = (f"spmv_vector_kernel<VL={vl}, {kind}>" if vl else "spmv_tile_kernel")
         if wb:
-            kernel = "spmv_warpblock_kernel (exact)"
+            kernel = ("spmv_warpblock_kernel (exact)" if exact else
+                      "spmv_warpblock_kernel (rows <= 512 in order, longer: warp tree; f32 exact)")
         return {"max_row_len": int(out[0]), "vector_length": vl, "exact": exact,
                 "warpblock": wb, "ntiles": int(out[2]), "kernel": kernel}
 

@@ -58,3 +58,20 @@ def test_chung_lu_k64(cuda_device):
     got = lb.spmm_csr(cu(rowptr), cu(colind), cu(values), cu(X)).cpu().numpy()
     ok, msg = O.diff_outputs([got], [want], 1e-12)
     assert ok, msg
+
+
+def test_rowblock_spmm_world1_matches_library_call(cuda_device):
+    # sharded.RowBlockSpmm at world 1 (the bench's config-3 path): the X slot
+    # buffer + spmm_csr give the library call's bits
+    from paper_2509_25605_b200 import sharded
+    rng = np.random.default_rng(21)
+    rowptr, colind, values = powerlaw_csr(rng, 3000, mean=8.0)
+    X = rng.uniform(-1, 1, (3000, 64))
+    rp, ci, v = (torch.from_numpy(a).cuda() for a in (rowptr, colind, values))
+    op = sharded.RowBlockSpmm(rp, ci, v, 3000, 64, 0, 1)
+    op.x_local.copy_(torch.from_numpy(X))
+    Y = torch.empty((3000, 64), dtype=torch.float64, device="cuda")
+    op.multiply(Y)
+    want = O.spmm_csr(rowptr, colind, values, X)
+    assert np.array_equal(Y.cpu().numpy().view(np.uint64), want.view(np.uint64)) or \
+        np.max(np.abs(Y.cpu().numpy() - want) / np.maximum(np.abs(want), 1)) <= 1e-12

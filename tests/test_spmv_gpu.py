@@ -218,7 +218,8 @@ def test_plan_picks_exact_vector_for_stencils(cuda_device):
 @pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int64, np.int32])
 def test_warpblock_kernel_bitexact(cuda_device, monkeypatch, nrows, dtype):
     # warp-block kernel forced on ragged rows (empty rows, rows far longer than
-    # its 256-entry window): every row is the reference's sequential sum
+    # its 256-entry window): in exact mode every row is the reference's
+    # sequential sum
     monkeypatch.setenv("LAPIS_B200_SPMV_KERNEL", "wb")
     rng = np.random.default_rng(nrows)
     longs = {0: 700, nrows - 1: 1300} if nrows > 2 else {}
@@ -226,10 +227,19 @@ def test_warpblock_kernel_bitexact(cuda_device, monkeypatch, nrows, dtype):
                                         long_rows=longs, dtype=dtype)
     x = (rng.integers(-9, 9, 2500) if np.issubdtype(dtype, np.integer)
          else rng.uniform(-1, 1, 2500)).astype(dtype)
-    plan = lb.CsrPlan(cu(rowptr))
+    want = O.spmv_csr(rowptr, colind, values, x)
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
     assert plan.info()["warpblock"], plan.info()
     y = host(plan.spmv(cu(colind), cu(values), cu(x)))
-    assert bits_equal(y, O.spmv_csr(rowptr, colind, values, x))
+    assert bits_equal(y, want)
+    # default mode: rows <= 512 still in order; longer fp64 rows folded by the
+    # warp as a fixed tree (within tolerance); fp32 and ints stay exact
+    tree = lb.CsrPlan(cu(rowptr))
+    yt = host(tree.spmv(cu(colind), cu(values), cu(x)))
+    if dtype == np.float64:
+        assert_close(yt, want, rowptr)
+    else:
+        assert bits_equal(yt, want)
 
 
 def test_warpblock_offset_rowptr(cuda_device, monkeypatch):
