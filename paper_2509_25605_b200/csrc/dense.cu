@@ -14,6 +14,8 @@
 // gemm_tf32x3.cu and gemm_dmma.cu.
 #include "common.cuh"
 
+#include <cstdlib>
+
 #include <type_traits>
 
 #include <cfloat>
@@ -244,6 +246,125 @@ row_fold_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
   if (row < m) y[row] = acc;
 }
 
+// Pipelined row fold (the launched one for matvec / axis-1 reduce): a CTA owns
+// 32 rows at a time (lane r of warp 0 folds row r in ascending column order —
+// the reference's sequential order, bit-identical), and all 8 warps stream
+// the rows' column panels into an RP_STAGES-deep shared-memory ring with
+// cp.async, so up to RP_STAGES - 1 panels (32 rows x RP_COLS x 8 B each) are
+// in flight per SM while warp 0 folds the current one.  Persistent over row
+// blocks.  Row pitch RP_COLS + 1 keeps the folder's column reads to <= 2-way
+// bank conflicts.
+constexpr int RP_ROWS = 32, RP_STAGES = 6;
+template <class T> struct RpCols { static constexpr int v = 512 / sizeof(T); };  // 128 f64 / 256 f32
+
+__device__ __forceinline__ void rp_cp(void* dst, const void* src, int bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d), "l"(src) : "memory");
+}
+
+// VEC16 (rows 16-byte aligned, n a multiple of 16 bytes): 16-byte cp.async
+// (4x fewer requests per byte — the per-SM limit on outstanding requests is
+// what bounds this kernel) and 16-byte shared loads in the fold; the pitch
+// C + 16 B keeps those loads conflict-free (8 lanes per phase)
+template <class T, bool VEC16> struct RpPitch {
+  static constexpr int v = RpCols<T>::v + (VEC16 ? 16 / (int)sizeof(T) : 1);
+};
+
+template <class T, bool VEC16>
+constexpr size_t rp_smem_bytes() {
+  return (size_t)RP_STAGES * (RP_ROWS * RpPitch<T, VEC16>::v + RpCols<T>::v) * sizeof(T);
+}
+
+__device__ __forceinline__ void rp_cp16(void* dst, const void* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
+}
+
+template <class T, bool DOT, bool VEC16>
+__global__ void __launch_bounds__(256)
+row_fold_pipe_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
+                     const T* __restrict__ x, T* __restrict__ y, int comb) {
+  constexpr int C = RpCols<T>::v, P = RpPitch<T, VEC16>::v, V = 16 / sizeof(T);
+  using V16 = typename std::conditional<sizeof(T) == 8, longlong2, int4>::type;
+  extern __shared__ __align__(16) unsigned char rp_raw[];
+  T* tiles = reinterpret_cast<T*>(rp_raw);                      // [S][ROWS][P]
+  T* xs = tiles + RP_STAGES * RP_ROWS * P;                       // [S][C]
+  const int t = threadIdx.x;
+  const int64_t nst = (n + C - 1) / C;
+  const int64_t nrb = (m + RP_ROWS - 1) / RP_ROWS;
+  for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+    const int64_t row0 = rb * RP_ROWS;
+    auto issue = [&](int64_t s) {
+      if (s < nst) {
+        const int slot = (int)(s % RP_STAGES);
+        const int64_t c0 = s * C;
+        T* tl = tiles + slot * RP_ROWS * P;
+        if (VEC16) {
+          for (int e = t; e < RP_ROWS * (C / V); e += 256) {
+            const int r = e / (C / V), c = (e % (C / V)) * V;
+            if (row0 + r < m && c0 + c < n) rp_cp16(tl + r * P + c, A + (row0 + r) * lda + c0 + c);
+          }
+          if (DOT && t < C / V && c0 + t * V < n) rp_cp16(xs + slot * C + t * V, x + c0 + t * V);
+        } else {
+          for (int e = t; e < RP_ROWS * C; e += 256) {
+            const int r = e / C, c = e % C;
+            if (row0 + r < m && c0 + c < n) rp_cp(tl + r * P + c, A + (row0 + r) * lda + c0 + c, sizeof(T));
+          }
+          if (DOT)
+            for (int c = t; c < C; c += 256)
+              if (c0 + c < n) rp_cp(xs + slot * C + c, x + c0 + c, sizeof(T));
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int s = 0; s < RP_STAGES - 1; ++s) issue(s);
+    T acc = DOT ? Arith<T>::zero() : identity<T>(comb);
+    for (int64_t s = 0; s < nst; ++s) {
+      asm volatile("cp.async.wait_group %0;" :: "n"(RP_STAGES - 2) : "memory");
+      __syncthreads();                 // stage s visible; slot of s - 1 free
+      issue(s + RP_STAGES - 1);
+      if (t < RP_ROWS) {
+        const int slot = (int)(s % RP_STAGES);
+        const T* tr = tiles + slot * RP_ROWS * P + t * P;
+        const T* xr = xs + slot * C;
+        const int cend = (int)((n - s * C) < C ? (n - s * C) : C);
+        int q = 0;
+        // groups of 16: all 16 (32) shared loads issued before the in-order
+        // chain, so the fold costs ~its dependent adds, not a load latency each
+        for (; q + 16 <= cend; q += 16) {
+          T a[16], b[16];
+          if (VEC16) {
+#pragma unroll
+            for (int u = 0; u < 16; u += V) {
+              const V16 va = *reinterpret_cast<const V16*>(tr + q + u);
+              memcpy(&a[u], &va, 16);
+              if (DOT) {
+                const V16 vb = *reinterpret_cast<const V16*>(xr + q + u);
+                memcpy(&b[u], &vb, 16);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              a[u] = tr[q + u];
+              if (DOT) b[u] = xr[q + u];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            acc = DOT ? Arith<T>::add(acc, Arith<T>::mul(a[u], b[u])) : combine(acc, a[u], comb);
+        }
+        for (; q < cend; ++q)
+          acc = DOT ? Arith<T>::add(acc, Arith<T>::mul(tr[q], xr[q])) : combine(acc, tr[q], comb);
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();                   // the ring is reused by the next row block
+    if (t < RP_ROWS && row0 + t < m) y[row0 + t] = acc;
+  }
+}
+
 // column fold (axis 0): one thread per column, rows in ascending order
 template <class T>
 __global__ void col_fold_kernel(int64_t rows, int64_t cols, const T* __restrict__ src,
@@ -320,10 +441,39 @@ int gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, in
 template <class T, bool DOT>
 static int launch_row_fold(int64_t m, int64_t n, const void* A, int64_t lda, const void* x,
                            void* y, int comb, cudaStream_t st) {
-  const int64_t blocks = (m + RF_ROWS - 1) / RF_ROWS;
-  row_fold_kernel<T, DOT><<<(unsigned)blocks, RF_ROWS, 0, st>>>(m, n, (const T*)A, lda,
-                                                                  (const T*)x, (T*)y, comb);
-  return check_launch("row_fold_kernel");
+  if (m == 0) return LAPIS_B200_OK;
+  if (getenv("LAPIS_B200_ROWFOLD_OLD")) {
+    const int64_t blocks = (m + RF_ROWS - 1) / RF_ROWS;
+    row_fold_kernel<T, DOT><<<(unsigned)blocks, RF_ROWS, 0, st>>>(m, n, (const T*)A, lda,
+                                                                    (const T*)x, (T*)y, comb);
+    return check_launch("row_fold_kernel");
+  }
+  const bool vec16 = ((lda * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)A % 16 == 0) &&
+                     ((n * (int64_t)sizeof(T)) % 16 == 0) && (!DOT || (uintptr_t)x % 16 == 0);
+  const size_t smem = vec16 ? rp_smem_bytes<T, true>() : rp_smem_bytes<T, false>();
+  auto kern = vec16 ? row_fold_pipe_kernel<T, DOT, true> : row_fold_pipe_kernel<T, DOT, false>;
+  static thread_local int configured_dev = -1;
+  static thread_local int per_sm_v[2] = {1, 1};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    for (int v = 0; v < 2; ++v) {
+      auto kv = v ? row_fold_pipe_kernel<T, DOT, true> : row_fold_pipe_kernel<T, DOT, false>;
+      const size_t sv = v ? rp_smem_bytes<T, true>() : rp_smem_bytes<T, false>();
+      LB_TRY(check_cuda(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sv), "smem attr (row fold)"));
+      LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_v[v], kv, 256, sv),
+                        "occupancy (row fold)"));
+      if (per_sm_v[v] < 1) per_sm_v[v] = 1;
+    }
+    configured_dev = dev;
+  }
+  const int per_sm = per_sm_v[vec16 ? 1 : 0];
+  int64_t blocks = (m + RP_ROWS - 1) / RP_ROWS;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, 256, smem, st>>>(m, n, (const T*)A, lda, (const T*)x, (T*)y, comb);
+  return check_launch("row_fold_pipe_kernel");
 }
 
 // C = relu(A B) in the reference order (GCN second stage, oracle/ir/gcn_f32.mlir)
