@@ -559,6 +559,7 @@ class PowerLawSpmm(Workload):
         rp = rp - rp[0]
         X = self.X.cpu().numpy()
         threads = min(threads, 2)   # each thread block replicates X (5 GB) on the stub
+        self.cpu_threads_used = threads
         Yref, times = R.spmm_csr(rp, ci, v, X, reps=reps, threads=threads)
         nnz = int(rp[-1])
         work = nnz * 12 + (b - a + 1) * 8 + (b - a) * self.k * 8 * 2
@@ -749,6 +750,7 @@ class GcnLayer(Workload):
         v = self.values[rp[0]:rp[-1]].cpu().numpy()
         rp = rp - rp[0]
         threads = min(threads, 4)   # each block replicates X (256 MB) on the stub
+        self.cpu_threads_used = threads
         Href, times = R.gcn(rp, ci, v, self.X.cpu().numpy(), self.W.cpu().numpy(), reps=reps,
                             threads=threads)
         nnz = int(rp[-1])
@@ -791,6 +793,68 @@ def powerlaw_csr_device(n, mean, alpha, seed):
     return rowptr, cols.contiguous(), values
 
 
+class DenseMatvec(Workload):
+    """linalg.matvec / LAPIS::gemv (SURVEY a10, fixture tests/fixtures/matvec_f64.mlir
+    scaled up): y = A x, A 16384 x 16384 f64 U(-1,1) seed 6 (2.1 GB > L2, no
+    flush needed), folded in the reference order (bit-identical).  N > 1:
+    independent replicas."""
+
+    name = "matvec: linalg.matvec f64 16384 x 16384 (row_fold_pipe_kernel, reference order)"
+    scaling = "weak"
+
+    def __init__(self, args, rank, world, n=16384):
+        import paper_2509_25605_b200 as lb
+        self.lb, self.args, self.world, self.n = lb, args, world, n
+        self.stream = torch.cuda.current_stream()
+        g = torch.Generator(device="cuda").manual_seed(6)
+        self.A = torch.rand((n, n), generator=g, dtype=torch.float64, device="cuda") * 2 - 1
+        self.x = torch.rand(n, generator=g, dtype=torch.float64, device="cuda") * 2 - 1
+        self.y = torch.empty(n, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def config(self):
+        return {"workload": self.name, "rows": self.n, "cols": self.n, "l2": "A 2.1 GB >> L2",
+                "parallelism": "replica"}
+
+    def work_local(self):
+        return (self.n * self.n + 2 * self.n) * 8
+
+    def work_global(self):
+        return self.work_local() * self.world
+
+    def kernel_name(self):
+        return "row_fold_pipe_kernel<double, DOT, 16-byte> (32 rows per CTA, 6-stage cp.async ring)"
+
+    def step(self):
+        self.lb.gemv(self.A, self.x, self.y, stream=self.stream)
+
+    def e2e(self, steps, warmup):
+        """x host-modified every step, y read back (A resident)."""
+        from paper_2509_25605_b200.dualview import DualView
+        xs = DualView.from_host(self.x.cpu(), "x", device_buffer=self.x)
+        ys = DualView.allocate((self.n,), torch.float64, "y")
+
+        def one():
+            xs.modify_host()
+            xs.sync_device(self.stream)
+            self.lb.gemv(self.A, xs.device_view(), ys.device_view(), stream=self.stream)
+            ys.modify_device()
+            ys.sync_host(self.stream)
+
+        return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
+
+    def cpu_reference(self, rows_sample, threads, reps):
+        from oracle import ref as R
+        rows = min(self.n, max(1, rows_sample // 4000))   # 1000 rows = 131 MB
+        self.cpu_threads_used = 1
+        A = self.A[:rows].cpu().numpy()
+        yref, times = R.matvec(A, self.x.cpu().numpy(), reps=reps)
+        work = (rows * self.n + self.n + rows) * 8
+        desc = (f"rows [0, {rows}) of the same A: reference emitted Kokkos C++ of "
+                "oracle/ir/matvec_f64.mlir on its serial stub, 1 thread")
+        return yref, self.y[:rows].cpu().numpy(), times, work, desc, 1e-12
+
+
 WORKLOADS = {
     "c5": lambda args, r, w: StencilSpmv(args, r, w, 27, args.n or 585, x_seed=5),
     "c1": lambda args, r, w: StencilSpmv(args, r, w, 5, args.n or 1000, x_seed=1),
@@ -799,6 +863,7 @@ WORKLOADS = {
     "c2f64": lambda args, r, w: DenseMatmul(args, r, w, torch.float64, args.n or 4096),
     "c4": lambda args, r, w: GcnLayer(args, r, w, args.n or 1_000_000),
     "mtx": lambda args, r, w: MtxSpmv(args, r, w),
+    "gemv": lambda args, r, w: DenseMatvec(args, r, w, args.n or 16384),
 }
 
 
@@ -816,7 +881,8 @@ def cpu_baseline(wl, args, threads):
         want, got, times, work, desc, tol = wl.cpu_reference(args.cpu_rows, threads, reps)
         t = float(np.median(times))
     scale = 1e9 if wl.unit == "GB/s" else 1e12
-    base = {"value": round(work / t / scale, 4), "unit": wl.unit, "cores": threads,
+    base = {"value": round(work / t / scale, 4), "unit": wl.unit,
+            "cores": getattr(wl, "cpu_threads_used", threads),
             "kind": "reference", "sample": desc + f", median of {len(times)} reps",
             "seconds_per_rep": t}
     parity = {"sample_elements": int(np.asarray(want).size), **parity_report(got, want, tol)}
@@ -845,7 +911,7 @@ def run_reference_arm(args, rank, world):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": wl.scaling,
            "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic", "config": wl.config(),
-           "cpu_baseline": {"value": round(value, 4), "unit": wl.unit, "cores": threads,
+           "cpu_baseline": {"value": round(value, 4), "unit": wl.unit, "cores": getattr(wl, "cpu_threads_used", threads),
                             "kind": "reference", "sample": desc},
            "e2e": {"value": round(value, 4), "unit": wl.unit, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
