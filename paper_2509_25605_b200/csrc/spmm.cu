@@ -237,7 +237,8 @@ __device__ __noinline__ void gcn_row_epilogue(float a0, float a1, const float* _
 }
 
 // L2 prefetch of the next gather group (default on; LAPIS_B200_SPMM_PREFETCH=0
-// disables): C3 10.64 -> 10.05 ms, C4 1.64 -> 1.55 ms measured
+// disables; N = gather groups ahead, 1 measured best: C3 10.05 / 11.6 / 13.8 ms
+// at 1 / 2 / 3, C4 1.64 -> 1.55 ms at 1)
 __constant__ int spmm_prefetch_on;
 
 template <class T, class RP, class CI, int CPL, int U, bool EPI = false>
@@ -314,7 +315,7 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
               // L2 prefetch of the NEXT group's X rows (no registers held): lane
               // l touches line (l / U) of entry t0 + U + l % U; past the chunk
               // end the next chunk's entries (colind already loaded) are used
-              const int pe = t0 + U + (lane % U);
+              const int pe = t0 + U * spmm_prefetch_on + (lane % U);
               const int64_t pc = pe < 32 ? __shfl_sync(0xffffffffu, my_col, pe & 31)
                                          : __shfl_sync(0xffffffffu, nx_col, pe & 31);
               const int64_t pj = j0 + pe;
@@ -689,7 +690,9 @@ struct SpmmOp {
         cudaGetDevice(&d);
         if (pf_dev != d) {
           const char* e = getenv("LAPIS_B200_SPMM_PREFETCH");  // "0" disables (A/B)
-          const int on = (e && e[0] == '0') ? 0 : 1;
+          int on = e ? atoi(e) : 1;  // prefetch distance in gather groups (0 = off)
+          if (on < 0) on = 0;
+          if (on > 4) on = 4;
           cudaMemcpyToSymbol(spmm_prefetch_on, &on, sizeof(on));
           pf_dev = d;
         }
