@@ -116,9 +116,17 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("LAPIS_BENCH_SHARE_GPU") == "1":
+        # correctness runs of the N > 1 path on a one-GPU box: every rank on
+        # cuda:0, gloo for the process group (NCCL refuses two ranks per GPU);
+        # the timings of such a run mean nothing
+        local = 0
     if world > 1 and args.impl != "reference":
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("LAPIS_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif world > 1:
         dist.init_process_group("gloo")
     return rank, world, local
@@ -127,7 +135,8 @@ def dist_setup(args):
 def max_over_ranks(v: float, world: int) -> float:
     if world == 1:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64,
+                     device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -286,6 +295,14 @@ class StencilSpmv(Workload):
         torch.cuda.synchronize()
         self.graphs = graphs
         self.graph_note = f"each step replays a captured CUDA graph of the multiply ({len(graphs)} graphs, one per input copy)"
+
+    def sharded_parity(self):
+        if self.N > 50_000_000:
+            return None
+        rp, ci, v = self.lb.synth_stencil(self.points, self.n)
+        plan = self.lb.CsrPlan(rp)
+        y = plan.spmv(ci, v, self.x)
+        return bool(torch.equal(y[self.r0:self.r1], self.last_y))
 
     def exact_variant(self, steps):
         """The same multiply with every row folded in the reference order (plan
@@ -467,6 +484,8 @@ class PowerLawSpmm(Workload):
         self.max_len = int(lens.max().item())
         self.median_len = float(lens.double().median().item())
         self.r0, self.r1 = sharded.equal_row_ranges(n, world)[rank]
+        self.full = ((rowptr, colind, values, X.clone())
+                     if world > 1 and n * k * 8 < (2 << 30) else None)
         if world > 1:
             a, b = int(rowptr[self.r0].item()), int(rowptr[self.r1].item())
             self.rowptr = (rowptr[self.r0:self.r1 + 1] - a).contiguous()
@@ -514,6 +533,13 @@ class PowerLawSpmm(Workload):
 
     def step(self):
         self.op.multiply(self.Y, stream=self.stream)
+
+    def sharded_parity(self):
+        if self.full is None:
+            return None
+        rp, ci, v, X = self.full
+        Y = self.lb.spmm_csr(rp, ci, v, X)
+        return bool(torch.equal(Y[self.r0:self.r1], self.Y))
 
     def exact_variant(self, steps):
         """N > 1: the X-replicated time (local SpMM only, no all-gather)."""
@@ -957,7 +983,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="problem size override")
+    ap.add_argument("--n", "--problem-size", dest="n", type=int, default=0,
+                    help="problem size override")
     ap.add_argument("--cpu-rows", type=int, default=4_000_000)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -1041,6 +1068,16 @@ def main():
     census = launch_census(wl)
     wl.step()   # the parity sample below checks the headline kernel's output
     torch.cuda.synchronize()
+    sharded_parity = None
+    if world > 1 and hasattr(wl, "sharded_parity"):
+        # this rank's rows of the sharded result against the unsharded
+        # multiply of the whole matrix on the same device (small runs only)
+        ok = wl.sharded_parity()
+        if ok is not None:
+            bad = torch.tensor([0.0 if ok else 1.0], dtype=torch.float64,
+                               device="cpu" if dist.get_backend() == "gloo" else "cuda")
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            sharded_parity = {"bitexact_vs_unsharded_all_ranks": bool(bad.item() == 0.0)}
     e2e_dt, hb, db = wl.e2e(args.e2e_steps, 2)
     e2e_dt = max_over_ranks(e2e_dt, world)
     out = {
@@ -1068,6 +1105,7 @@ def main():
         **({"kernels": census} if census else {}),
         **({getattr(wl, "variant_key", "exact_mode"): exact_variant} if exact_variant else {}),
         "clocks": clk.summary(),
+        **({"sharded_parity": sharded_parity} if sharded_parity else {}),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         base, parity = cpu_baseline(wl, args, os.cpu_count() or 1)

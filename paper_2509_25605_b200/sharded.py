@@ -93,6 +93,8 @@ def build_exchange_plan(colind: torch.Tensor, ranges, rank: int, world: int,
 def exchange(plan: ExchangePlan, x_full: torch.Tensor, group=None):
     """Post the halo slabs (P2P) — returns the request list; x_full is indexed by
     GLOBAL column and already holds this rank's own slice."""
+    if x_full.is_cuda and dist.get_backend(group) == "gloo":
+        return _exchange_staged(plan, x_full, group)
     ops = []
     for p in range(plan.world):
         if p == plan.rank:
@@ -104,6 +106,29 @@ def exchange(plan: ExchangePlan, x_full: torch.Tensor, group=None):
         if hi > lo:
             ops.append(dist.P2POp(dist.irecv, x_full[lo:hi], p, group=group))
     return dist.batch_isend_irecv(ops) if ops else []
+
+
+def _exchange_staged(plan: ExchangePlan, x_full: torch.Tensor, group=None):
+    """gloo moves host tensors only: the same slabs through host copies,
+    completed before returning (correctness runs of the N > 1 path on one
+    GPU; the product path is NCCL)."""
+    ops, staged = [], []
+    for p in range(plan.world):
+        if p == plan.rank:
+            continue
+        lo, hi = plan.sends[p]
+        if hi > lo:
+            ops.append(dist.P2POp(dist.isend, x_full[lo:hi].cpu(), p, group=group))
+        lo, hi = plan.needs[p]
+        if hi > lo:
+            buf = torch.empty_like(x_full[lo:hi], device="cpu")
+            ops.append(dist.P2POp(dist.irecv, buf, p, group=group))
+            staged.append((lo, hi, buf))
+    for r in (dist.batch_isend_irecv(ops) if ops else []):
+        r.wait()
+    for lo, hi, buf in staged:
+        x_full[lo:hi].copy_(buf)
+    return []
 
 
 def interior_run(rowptr: torch.Tensor, colind: torch.Tensor, own: tuple[int, int]) -> tuple[int, int]:
@@ -220,6 +245,11 @@ class RowBlockSpmm:
     def gather(self) -> None:
         if self.world > 1:
             slot = self.X_full[self.rank * self.chunk:(self.rank + 1) * self.chunk]
+            if self.X_full.is_cuda and dist.get_backend(self.group) == "gloo":
+                host = self.X_full.cpu()   # correctness runs on one GPU (gloo)
+                dist.all_gather_into_tensor(host, slot.cpu(), group=self.group)
+                self.X_full.copy_(host)
+                return
             dist.all_gather_into_tensor(self.X_full, slot, group=self.group)
 
     def multiply(self, Y_local: torch.Tensor, stream=None, replicated: bool = False):

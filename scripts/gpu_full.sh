@@ -6,9 +6,10 @@ TAG=${1:-full}; OUT=gpurun_out/$TAG; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi.txt
 timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.txt
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
-for W in ${WORKLOADS:-c5 c1 c3 c4 c2f32 c2f64}; do
+for W in ${WORKLOADS:-c5 c1 c3 c4 c2f32 c2f64 gemv}; do
   timeout 900 python bench.py --workload $W ${BENCH_ARGS} > $OUT/bench_$W.json 2> $OUT/bench_$W.err
 done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 if [ -n "$NCU" ]; then
   for W in ${NCU_WORKLOADS:-c3 c4}; do
     timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
@@ -19,8 +20,8 @@ if [ -n "$NCU" ]; then
       -o $OUT/full_${NCU_W:-c3} python bench.py --workload ${NCU_W:-c3} --steps 1 --warmup 3 --no-cpu --e2e-steps 1 > $OUT/ncu_full.log 2>&1
   fi
 fi
-tail -3 $OUT/pytest_gpu.txt; cat $OUT/smoke.txt
-for W in ${WORKLOADS:-c5 c1 c3 c4 c2f32 c2f64}; do
+tail -3 $OUT/pytest_gpu.txt; cat $OUT/smoke.txt; tail -c 400 $OUT/bench_reference.json
+for W in ${WORKLOADS:-c5 c1 c3 c4 c2f32 c2f64 gemv}; do
   python - "$OUT/bench_$W.json" <<'PY' || tail -5 $OUT/bench_$W.err
 import json, sys
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
