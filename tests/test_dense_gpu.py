@@ -173,3 +173,28 @@ def test_ozaki_certification_falls_back(cuda_device, dt, lo):
     got = host(lb.gemm(cu(A), cu(B), mode="ozaki"))
     ok, msg = O.diff_outputs([got], [O.matmul(A, B)], 1e-12 if dt == np.float64 else 1e-5)
     assert ok, msg
+
+
+@pytest.mark.parametrize("m,n,dtype", [(1000, 1537, np.float64), (333, 4096, np.float32),
+                                       (70, 4100, np.float64), (65, 3, np.float32),
+                                       (129, 2050, np.int64), (40, 999, np.int32)])
+def test_gemv_pipelined_fold_bitexact(cuda_device, m, n, dtype):
+    # both copy paths of row_fold_pipe_kernel (16-byte when the row pitch and n
+    # allow, element-wise otherwise), partial row blocks and column panels
+    rng = np.random.default_rng(m + n)
+    if np.issubdtype(dtype, np.integer):
+        A = rng.integers(-2**30, 2**30, (m, n)).astype(dtype)   # wraps
+        x = rng.integers(-9, 9, n).astype(dtype)
+    else:
+        A = rng.uniform(-1, 1, (m, n)).astype(dtype)
+        x = rng.uniform(-1, 1, n).astype(dtype)
+    assert bits_equal(host(lb.gemv(cu(A), cu(x))), O.matvec(A, x))
+
+
+@pytest.mark.parametrize("comb", ["add", "mul", "min", "max"])
+@pytest.mark.parametrize("dtype", [np.float64, np.int64, np.float32])
+def test_reduce_rows_pipelined_bitexact(cuda_device, comb, dtype):
+    rng = np.random.default_rng(3)
+    src = (rng.integers(-5, 6, (300, 517)) if np.issubdtype(dtype, np.integer)
+           else rng.uniform(0.5, 1.5, (300, 517))).astype(dtype)
+    assert bits_equal(host(lb.reduce2d(cu(src), 1, comb)), O.reduce2d(src, 1, comb))
