@@ -571,7 +571,16 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
                            const void* values, const void* x, void* y, cudaStream_t st) {
   const int threads = 256;
   int64_t blocks = (nrows * VL + threads - 1) / threads;
-  const int64_t cap = (int64_t)num_sms() * 64;
+  // grid cap in CTAs per SM (LAPIS_B200_SPMV_BLOCKS_PER_SM for tuning runs).
+  // Measured on C5 (200M rows, VL = 4): 8 / 64 / 256 / 1024 / 4096 / uncapped
+  // -> 13.9 / 12.8 / 12.0 / 11.9 / 12.2 / 13.3 ms: many short-lived CTAs
+  // balance better than a few long grid-stride walkers, and neighbouring CTAs
+  // stream neighbouring rows (x reuse in L2)
+  static const int64_t per_sm = [] {
+    const char* e = getenv("LAPIS_B200_SPMV_BLOCKS_PER_SM");
+    return (int64_t)(e ? atoi(e) : 1024);
+  }();
+  const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   spmv_vector_kernel<T, RP, CI, VL, EXACT><<<(unsigned)blocks, threads, 0, st>>>(
