@@ -82,8 +82,12 @@ int64_t lapis_b200_csr_vector_length(int64_t nrows, int64_t nnz, int64_t max_vec
  * semantics interp.py:798-812).
  *   rowptr_bytes, colind_bytes in {4, 8} (i32 or i64/index);
  *   dtype in {F32, F64, I32, I64} for values / x / y;
- *   vector_length = 0: tiled row-stream kernel (rows up to 512 entries are
- *     summed sequentially in ascending order, bit-identical to the reference);
+ *   vector_length = 0: a device-side choice, no host round trip: one pass over
+ *     rowptr (longest row, monotonicity), then regular structures run the
+ *     vector-lane kernel in exact mode (every row bit-identical), irregular
+ *     ones the warp-block kernel and non-monotone rowptrs the tiled row-stream
+ *     kernel (both: rows up to 512 entries summed in ascending order,
+ *     bit-identical; longer fp64 rows as a fixed tree, within tolerance);
  *   vector_length = 1..32 (power of two): the emitted TeamPolicy mapping with
  *     that vector length (one row per `vector_length` lanes, shuffle tree). */
 int lapis_b200_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz,

@@ -48,6 +48,22 @@ constexpr int TILE_CAP = TILE_KEYS + LONG_ROW;    // products staged per tile
 // LAPIS_B200_SPMV_KERNEL=wb
 constexpr double WARPBLOCK_MAX_MEAN = 0.0;
 
+// Device-side kernel choice for calls without a plan (lapis_b200_spmv_csr,
+// vector_length = 0): a stats pass writes {longest row, descending flag};
+// the regular-structure kernel and the tile kernel are both launched and each
+// returns at once unless the stats select it (no host round trip).
+struct RowGuard {
+  const unsigned long long* stats = nullptr;  // nullptr: no guard
+  long long thresh = 0;                       // regular iff monotone && max_len <= thresh
+  int want = 0;  // 1 regular, 2 monotone irregular, 3 non-monotone
+};
+__device__ __forceinline__ bool row_guard_skip(const RowGuard& g) {
+  if (!g.stats) return false;
+  const bool monotone = g.stats[1] == 0;
+  const int cls = !monotone ? 3 : ((long long)g.stats[0] <= g.thresh ? 1 : 2);
+  return cls != g.want;
+}
+
 // ---------------------------------------------------------------- plan
 // tile_row[c]  = first row owned by tile c (c in [0, ntiles]; tile_row[ntiles] = nrows)
 // tile_nnz[c]  = rowptr[tile_row[c]] (absolute), so a tile can start streaming
@@ -55,7 +71,8 @@ constexpr double WARPBLOCK_MAX_MEAN = 0.0;
 template <class RP>
 __global__ void tile_partition_kernel(int64_t nrows, const RP* __restrict__ rowptr,
                                       int64_t ntiles, int64_t* __restrict__ tile_row,
-                                      int64_t* __restrict__ tile_nnz) {
+                                      int64_t* __restrict__ tile_nnz, RowGuard guard = RowGuard()) {
+  if (row_guard_skip(guard)) return;
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r > nrows) return;
   const int64_t base = (int64_t)rowptr[0];
@@ -161,7 +178,8 @@ __global__ void __launch_bounds__(NT)
 spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                  const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
                  const int64_t* __restrict__ tile_row, const int64_t* __restrict__ tile_nnz,
-                 int64_t ntiles, int tma_ok) {
+                 int64_t ntiles, int tma_ok, RowGuard guard = RowGuard()) {
+  if (row_guard_skip(guard)) return;
   using L = StreamSmem<T, CI, ST>;
   constexpr int PER = (TILE_CAP + NT - 1) / NT;        // streamed entries per thread
   constexpr int RPER = (TILE_KEYS + NT - 1) / NT;      // owned rows per thread
@@ -322,7 +340,9 @@ spmv_tile_kernel(const RP* __restrict__ rowptr, const CI* __restrict__ colind,
 template <class T, class RP, class CI, int VL, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
-                   const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y) {
+                   const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
+                   RowGuard guard = RowGuard()) {
+  if (row_guard_skip(guard)) return;
   const int lane = threadIdx.x & (VL - 1);
   const unsigned gmask = (VL == 32) ? 0xffffffffu
                                     : (((1u << VL) - 1u) << ((threadIdx.x & 31) & ~(VL - 1)));
@@ -385,7 +405,8 @@ template <class T, class RP, class CI, int U, bool EXACT>
 __global__ void __launch_bounds__(256)
 spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                       const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
-                      unsigned long long* __restrict__ next) {
+                      unsigned long long* __restrict__ next, RowGuard guard = RowGuard()) {
+  if (row_guard_skip(guard)) return;
   constexpr int CAP = 32 * U;
   __shared__ T win[8][CAP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -502,23 +523,23 @@ static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
 }
 
 int launch_partition(int64_t nrows, const void* rowptr, int rp_bytes, int64_t ntiles,
-                     int64_t* tile_row, cudaStream_t st) {
+                     int64_t* tile_row, cudaStream_t st, RowGuard guard = RowGuard()) {
   const int threads = 256;
   const int64_t blocks = (nrows + 1 + threads - 1) / threads;
   int64_t* tile_nnz = tile_row + (ntiles + 1);
   if (rp_bytes == 8)
     tile_partition_kernel<int64_t><<<(unsigned)blocks, threads, 0, st>>>(
-        nrows, (const int64_t*)rowptr, ntiles, tile_row, tile_nnz);
+        nrows, (const int64_t*)rowptr, ntiles, tile_row, tile_nnz, guard);
   else
     tile_partition_kernel<int32_t><<<(unsigned)blocks, threads, 0, st>>>(
-        nrows, (const int32_t*)rowptr, ntiles, tile_row, tile_nnz);
+        nrows, (const int32_t*)rowptr, ntiles, tile_row, tile_nnz, guard);
   return check_launch("tile_partition_kernel");
 }
 
 template <class T, class RP, class CI, int NT, int ST>
 static int launch_tile_cfg(int64_t ntiles, const void* rowptr, const void* colind,
                            const void* values, const void* x, void* y, const int64_t* tile_row,
-                           cudaStream_t st) {
+                           cudaStream_t st, RowGuard guard) {
   using L = StreamSmem<T, CI, ST>;
   auto kern = spmv_tile_kernel<T, RP, CI, NT, ST>;
   static thread_local int configured_dev = -1;
@@ -540,7 +561,7 @@ static int launch_tile_cfg(int64_t ntiles, const void* rowptr, const void* colin
   const int64_t* tile_nnz = tile_row + (ntiles + 1);
   kern<<<(unsigned)grid, NT, L::TOTAL, st>>>((const RP*)rowptr, (const CI*)colind,
                                              (const T*)values, (const T*)x, (T*)y, tile_row,
-                                             tile_nnz, ntiles, tma_ok);
+                                             tile_nnz, ntiles, tma_ok, guard);
   return check_launch("spmv_tile_kernel");
 }
 
@@ -557,18 +578,19 @@ static int spmv_cfg() {
 template <class T, class RP, class CI>
 static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
                          const void* values, const void* x, void* y, const int64_t* tile_row,
-                         cudaStream_t st) {
+                         cudaStream_t st, RowGuard g = RowGuard()) {
   switch (spmv_cfg()) {
-    case 1: return launch_tile_cfg<T, RP, CI, 128, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st);
-    case 2: return launch_tile_cfg<T, RP, CI, 256, 3>(ntiles, rowptr, colind, values, x, y, tile_row, st);
-    case 3: return launch_tile_cfg<T, RP, CI, 128, 3>(ntiles, rowptr, colind, values, x, y, tile_row, st);
-    default: return launch_tile_cfg<T, RP, CI, 256, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st);
+    case 1: return launch_tile_cfg<T, RP, CI, 128, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st, g);
+    case 2: return launch_tile_cfg<T, RP, CI, 256, 3>(ntiles, rowptr, colind, values, x, y, tile_row, st, g);
+    case 3: return launch_tile_cfg<T, RP, CI, 128, 3>(ntiles, rowptr, colind, values, x, y, tile_row, st, g);
+    default: return launch_tile_cfg<T, RP, CI, 256, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st, g);
   }
 }
 
 template <class T, class RP, class CI, int VL, bool EXACT>
 static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind,
-                           const void* values, const void* x, void* y, cudaStream_t st) {
+                           const void* values, const void* x, void* y, cudaStream_t st,
+                           RowGuard guard = RowGuard()) {
   const int threads = 256;
   int64_t blocks = (nrows * VL + threads - 1) / threads;
   // grid cap in CTAs per SM (LAPIS_B200_SPMV_BLOCKS_PER_SM for tuning runs).
@@ -584,14 +606,14 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   spmv_vector_kernel<T, RP, CI, VL, EXACT><<<(unsigned)blocks, threads, 0, st>>>(
-      nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y);
+      nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, guard);
   return check_launch("spmv_vector_kernel");
 }
 
 template <class T, class RP, class CI>
 static int launch_warpblock_t(int64_t nrows, const void* rowptr, const void* colind,
                               const void* values, const void* x, void* y, int exact,
-                              unsigned long long* next, cudaStream_t st) {
+                              unsigned long long* next, cudaStream_t st, RowGuard guard) {
   auto kern = exact ? spmv_warpblock_kernel<T, RP, CI, 8, true>
                     : spmv_warpblock_kernel<T, RP, CI, 8, false>;
   static thread_local int configured_dev = -1;
@@ -614,20 +636,21 @@ static int launch_warpblock_t(int64_t nrows, const void* rowptr, const void* col
   if (blocks < 1) blocks = 1;
   if (next) LB_TRY(check_cuda(cudaMemsetAsync(next, 0, sizeof(*next), st), "memset(spmv counter)"));
   kern<<<(unsigned)blocks, 256, 0, st>>>(nrows, (const RP*)rowptr, (const CI*)colind,
-                                         (const T*)values, (const T*)x, (T*)y, next);
+                                         (const T*)values, (const T*)x, (T*)y, next, guard);
   return check_launch("spmv_warpblock_kernel");
 }
 
 template <class T, class RP, class CI, bool EXACT>
 static int dispatch_vl(int vl, int64_t nrows, const void* rowptr, const void* colind,
-                       const void* values, const void* x, void* y, cudaStream_t st) {
+                       const void* values, const void* x, void* y, cudaStream_t st,
+                       RowGuard g = RowGuard()) {
   switch (vl) {
-    case 1: return launch_vector_t<T, RP, CI, 1, EXACT>(nrows, rowptr, colind, values, x, y, st);
-    case 2: return launch_vector_t<T, RP, CI, 2, EXACT>(nrows, rowptr, colind, values, x, y, st);
-    case 4: return launch_vector_t<T, RP, CI, 4, EXACT>(nrows, rowptr, colind, values, x, y, st);
-    case 8: return launch_vector_t<T, RP, CI, 8, EXACT>(nrows, rowptr, colind, values, x, y, st);
-    case 16: return launch_vector_t<T, RP, CI, 16, EXACT>(nrows, rowptr, colind, values, x, y, st);
-    case 32: return launch_vector_t<T, RP, CI, 32, EXACT>(nrows, rowptr, colind, values, x, y, st);
+    case 1: return launch_vector_t<T, RP, CI, 1, EXACT>(nrows, rowptr, colind, values, x, y, st, g);
+    case 2: return launch_vector_t<T, RP, CI, 2, EXACT>(nrows, rowptr, colind, values, x, y, st, g);
+    case 4: return launch_vector_t<T, RP, CI, 4, EXACT>(nrows, rowptr, colind, values, x, y, st, g);
+    case 8: return launch_vector_t<T, RP, CI, 8, EXACT>(nrows, rowptr, colind, values, x, y, st, g);
+    case 16: return launch_vector_t<T, RP, CI, 16, EXACT>(nrows, rowptr, colind, values, x, y, st, g);
+    case 32: return launch_vector_t<T, RP, CI, 32, EXACT>(nrows, rowptr, colind, values, x, y, st, g);
   }
   return fail(LAPIS_B200_ERR_ARG, "spmv: vector_length must be 0 or a power of two <= 32");
 }
@@ -654,8 +677,16 @@ static int dispatch_types(int dtype, int rp_bytes, int ci_bytes, Args&&... args)
 template <class T, class RP, class CI>
 struct TileOp {
   static int run(int64_t ntiles, const void* rp, const void* ci, const void* v,
-                 const void* x, void* y, const int64_t* tr, cudaStream_t st) {
-    return launch_tile_t<T, RP, CI>(ntiles, rp, ci, v, x, y, tr, st);
+                 const void* x, void* y, const int64_t* tr, cudaStream_t st,
+                 RowGuard g = RowGuard()) {
+    return launch_tile_t<T, RP, CI>(ntiles, rp, ci, v, x, y, tr, st, g);
+  }
+};
+template <class T, class RP, class CI>
+struct VecExactGuardedOp {
+  static int run(int vl, int64_t nrows, const void* rp, const void* ci, const void* v,
+                 const void* x, void* y, cudaStream_t st, RowGuard g) {
+    return dispatch_vl<T, RP, CI, true>(vl, nrows, rp, ci, v, x, y, st, g);
   }
 };
 template <class T, class RP, class CI>
@@ -668,12 +699,12 @@ struct VecOp {
 template <class T, class RP, class CI>
 struct WarpBlockOp {
   static int run(int64_t nrows, const void* rp, const void* ci, const void* v, const void* x,
-                 void* y, int exact, cudaStream_t st) {
+                 void* y, int exact, cudaStream_t st, RowGuard g = RowGuard()) {
     // the block counter: a per-call stream-ordered allocation (pool-cached),
     // so multiplies with one plan on several streams never share it
     unsigned long long* next = nullptr;
     LB_TRY(check_cuda(cudaMallocAsync((void**)&next, sizeof(*next), st), "alloc(spmv counter)"));
-    const int rc = launch_warpblock_t<T, RP, CI>(nrows, rp, ci, v, x, y, exact, next, st);
+    const int rc = launch_warpblock_t<T, RP, CI>(nrows, rp, ci, v, x, y, exact, next, st, g);
     cudaFreeAsync(next, st);
     return rc;
   }
@@ -708,15 +739,45 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
   if (nrows == 0) return LAPIS_B200_OK;
   if (vl != 0) return dispatch_types<VecOp>(dtype, rp_bytes, ci_bytes, vl, nrows, rowptr, colind,
                                             values, x, y, st);
+  // no plan: one stats pass over rowptr on the device, then both candidate
+  // kernels launched behind a device guard — the exact vector kernel (the
+  // plan's choice for regular structures, bit-identical) or the partition +
+  // tile kernel (irregular / non-monotone) — so the call stays asynchronous
   const int64_t ntiles = ntiles_for(nrows, nnz);
-  int64_t* tile_row = nullptr;
-  LB_TRY(check_cuda(cudaMallocAsync((void**)&tile_row, 2 * (ntiles + 1) * sizeof(int64_t), st),
-                    "cudaMallocAsync(tile_row)"));
-  int rc = launch_partition(nrows, rowptr, rp_bytes, ntiles, tile_row, st);
+  int64_t* ws = nullptr;
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, (2 * (ntiles + 1) + 2) * sizeof(int64_t), st),
+                    "cudaMallocAsync(spmv workspace)"));
+  unsigned long long* stats = reinterpret_cast<unsigned long long*>(ws + 2 * (ntiles + 1));
+  int64_t* tile_row = ws;
+  int rc = check_cuda(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st), "memset(stats)");
+  if (rc == LAPIS_B200_OK) {
+    const int64_t blocks = std::min<int64_t>((nrows + 255) / 256, (int64_t)num_sms() * 8);
+    if (rp_bytes == 8)
+      row_stats_kernel<int64_t><<<(unsigned)blocks, 256, 0, st>>>(nrows, (const int64_t*)rowptr, stats);
+    else
+      row_stats_kernel<int32_t><<<(unsigned)blocks, 256, 0, st>>>(nrows, (const int32_t*)rowptr, stats);
+    rc = check_launch("row_stats_kernel");
+  }
+  const double mean = (double)nnz / (double)nrows;
+  int cvl = 1;
+  while (cvl < 8 && (double)(cvl * 2) * 6.0 <= mean) cvl *= 2;
+  RowGuard greg, gwb, girr;
+  greg.stats = gwb.stats = girr.stats = stats;
+  greg.thresh = gwb.thresh = girr.thresh = (long long)std::max(64.0, 8.0 * mean);  // analyse_rows
+  greg.want = 1;  // regular: exact vector kernel
+  gwb.want = 2;   // monotone irregular: warp-block kernel (the plan's choice)
+  girr.want = 3;  // non-monotone rowptr: partition + tile kernel
+  if (rc == LAPIS_B200_OK)
+    rc = dispatch_types<VecExactGuardedOp>(dtype, rp_bytes, ci_bytes, cvl, nrows, rowptr, colind,
+                                           values, x, y, st, greg);
+  if (rc == LAPIS_B200_OK)
+    rc = dispatch_types<WarpBlockOp>(dtype, rp_bytes, ci_bytes, nrows, rowptr, colind, values, x,
+                                     y, dtype == LAPIS_B200_F32 ? 1 : 0, st, gwb);
+  if (rc == LAPIS_B200_OK) rc = launch_partition(nrows, rowptr, rp_bytes, ntiles, tile_row, st, girr);
   if (rc == LAPIS_B200_OK)
     rc = dispatch_types<TileOp>(dtype, rp_bytes, ci_bytes, ntiles, rowptr, colind, values, x, y,
-                                (const int64_t*)tile_row, st);
-  cudaFreeAsync(tile_row, st);
+                                (const int64_t*)tile_row, st, girr);
+  cudaFreeAsync(ws, st);
   return rc;
 }
 
