@@ -254,10 +254,12 @@ row_fold_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
 // in flight per SM while warp 0 folds the current one.  Persistent over row
 // blocks.  Row pitch RP_COLS + 1 keeps the folder's column reads to <= 2-way
 // bank conflicts.
-constexpr int RP_ROWS = 32, RP_STAGES = 6;
-// 256-byte column panels: ~54 KB of ring per CTA, 4 CTAs (4 folding warps)
-// per SM.  Measured at 16384^2 (f64 matvec / f64 reduce / f32 matvec):
-// 128 B 0.52 / 0.55 / 0.28 ms, 256 B 0.46 / 0.41 / 0.23 ms, 512 B 0.61 / 0.44 / 0.28 ms
+constexpr int RP_ROWS = 32, RP_STAGES = 4;
+// 256-byte column panels, 4 stages: ~36 KB of ring per CTA, 6 CTAs (6 folding
+// warps) per SM — the fold, one warp per CTA, is what limits the kernel.
+// Measured at 16384^2 (f64 matvec / f64 reduce / f32 matvec), 6 stages:
+// 128 B 0.52 / 0.55 / 0.28 ms, 256 B 0.46 / 0.41 / 0.23 ms, 512 B 0.61 / 0.44 / 0.28 ms;
+// 256 B with 3 / 4 stages: 0.42 / 0.39 / 0.22 and 0.43 / 0.37 / 0.21 ms
 constexpr int RP_PANEL_BYTES = 256;
 template <class T> struct RpCols { static constexpr int v = RP_PANEL_BYTES / sizeof(T); };
 
