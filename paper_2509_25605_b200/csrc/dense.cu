@@ -248,15 +248,19 @@ row_fold_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
 
 // Pipelined row fold (the launched one for matvec / axis-1 reduce): a CTA owns
 // 32 rows at a time (lane r of warp 0 folds row r in ascending column order —
-// the reference's sequential order, bit-identical), and all 8 warps stream
+// the reference's sequential order, bit-identical), and all 4 warps stream
 // the rows' column panels into an RP_STAGES-deep shared-memory ring with
 // cp.async, so up to RP_STAGES - 1 panels (32 rows x RP_COLS x 8 B each) are
 // in flight per SM while warp 0 folds the current one.  Persistent over row
 // blocks.  Row pitch RP_COLS + 1 keeps the folder's column reads to <= 2-way
 // bank conflicts.
-constexpr int RP_ROWS = 32, RP_STAGES = 4;
-// 256-byte column panels, 4 stages: ~36 KB of ring per CTA, 6 CTAs (6 folding
-// warps) per SM — the fold, one warp per CTA, is what limits the kernel.
+// 128 threads (one folding warp + three streaming), 3 stages: ~27 KB per CTA,
+// 8 CTAs (folding warps) per SM.  Measured at 16384^2, f64 matvec / f64
+// reduce / f32 matvec: 256 thr x 4 stages 0.427 / 0.374 / 0.211 ms, 128 x 4
+// 0.422 / 0.367 / 0.207, 128 x 3 0.398 / 0.376 / 0.205, 64 x 3 0.391 / 0.393 / 0.210
+constexpr int RP_ROWS = 32, RP_STAGES = 3, RP_THREADS = 128;
+// 256-byte column panels (the fold, one warp per CTA, is what limits the
+// kernel, so more, smaller CTAs per SM win).
 // Measured at 16384^2 (f64 matvec / f64 reduce / f32 matvec), 6 stages:
 // 128 B 0.52 / 0.55 / 0.28 ms, 256 B 0.46 / 0.41 / 0.23 ms, 512 B 0.61 / 0.44 / 0.28 ms;
 // 256 B with 3 / 4 stages: 0.42 / 0.39 / 0.22 and 0.43 / 0.37 / 0.21 ms
@@ -288,7 +292,7 @@ __device__ __forceinline__ void rp_cp16(void* dst, const void* src) {
 }
 
 template <class T, bool DOT, bool VEC16>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(RP_THREADS)
 row_fold_pipe_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
                      const T* __restrict__ x, T* __restrict__ y, int comb) {
   constexpr int C = RpCols<T>::v, P = RpPitch<T, VEC16>::v, V = 16 / sizeof(T);
@@ -307,18 +311,18 @@ row_fold_pipe_kernel(int64_t m, int64_t n, const T* __restrict__ A, int64_t lda,
         const int64_t c0 = s * C;
         T* tl = tiles + slot * RP_ROWS * P;
         if (VEC16) {
-          for (int e = t; e < RP_ROWS * (C / V); e += 256) {
+          for (int e = t; e < RP_ROWS * (C / V); e += RP_THREADS) {
             const int r = e / (C / V), c = (e % (C / V)) * V;
             if (row0 + r < m && c0 + c < n) rp_cp16(tl + r * P + c, A + (row0 + r) * lda + c0 + c);
           }
           if (DOT && t < C / V && c0 + t * V < n) rp_cp16(xs + slot * C + t * V, x + c0 + t * V);
         } else {
-          for (int e = t; e < RP_ROWS * C; e += 256) {
+          for (int e = t; e < RP_ROWS * C; e += RP_THREADS) {
             const int r = e / C, c = e % C;
             if (row0 + r < m && c0 + c < n) rp_cp(tl + r * P + c, A + (row0 + r) * lda + c0 + c, sizeof(T));
           }
           if (DOT)
-            for (int c = t; c < C; c += 256)
+            for (int c = t; c < C; c += RP_THREADS)
               if (c0 + c < n) rp_cp(xs + slot * C + c, x + c0 + c, sizeof(T));
         }
       }
@@ -468,7 +472,7 @@ static int launch_row_fold(int64_t m, int64_t n, const void* A, int64_t lda, con
       const size_t sv = v ? rp_smem_bytes<T, true>() : rp_smem_bytes<T, false>();
       LB_TRY(check_cuda(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sv), "smem attr (row fold)"));
-      LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_v[v], kv, 256, sv),
+      LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_v[v], kv, RP_THREADS, sv),
                         "occupancy (row fold)"));
       if (per_sm_v[v] < 1) per_sm_v[v] = 1;
     }
@@ -478,7 +482,7 @@ static int launch_row_fold(int64_t m, int64_t n, const void* A, int64_t lda, con
   int64_t blocks = (m + RP_ROWS - 1) / RP_ROWS;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, 256, smem, st>>>(m, n, (const T*)A, lda, (const T*)x, (T*)y, comb);
+  kern<<<(unsigned)blocks, RP_THREADS, smem, st>>>(m, n, (const T*)A, lda, (const T*)x, (T*)y, comb);
   return check_launch("row_fold_pipe_kernel");
 }
 
