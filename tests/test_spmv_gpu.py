@@ -287,3 +287,20 @@ def test_native_rowblock_rejects_unrebased_rowptr(cuda_device):
     sub = rp[100:200 + 1]
     with pytest.raises(lb.BackendError):
         sharded.NativeRowBlockSpmv(sub, ci, v, [(100, 200)], 0, 1, None)
+
+
+def test_no_plan_call_device_dispatch(cuda_device):
+    # lapis_b200_spmv_csr without a plan (the emitted C++'s LAPIS::spmv_csr):
+    # a regular stencil takes the exact vector kernel (VL 4: every row
+    # bit-identical), a power-law matrix the warp-block kernel (rows <= 512
+    # bit-identical, hub rows within tolerance)
+    rp, ci, v = lb.synth_stencil(27, 24)
+    x = np.random.default_rng(1).uniform(-1, 1, rp.numel() - 1)
+    y = host(lb.spmv_csr(rp, ci, v, cu(x)))
+    assert bits_equal(y, O.spmv_csr(host(rp), host(ci), host(v), x))
+    rng = np.random.default_rng(2)
+    rowptr, colind, values = powerlaw_csr(rng, 30000, mean=10.0)
+    assert np.diff(rowptr).max() > 512
+    x2 = rng.uniform(-1, 1, 30000)
+    y2 = host(lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x2)))
+    assert_close(y2, O.spmv_csr(rowptr, colind, values, x2), rowptr)
