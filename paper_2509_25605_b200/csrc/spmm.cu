@@ -236,10 +236,17 @@ __device__ __noinline__ void gcn_row_epilogue(float a0, float a1, const float* _
   reinterpret_cast<float2*>(hrow)[lane] = h;
 }
 
-// L2 prefetch of the next gather group (default on; LAPIS_B200_SPMM_PREFETCH=0
-// disables; N = gather groups ahead, 1 measured best: C3 10.05 / 11.6 / 13.8 ms
-// at 1 / 2 / 3, C4 1.64 -> 1.55 ms at 1)
-__constant__ int spmm_prefetch_on;
+// L2 prefetch of the next gather group (kernel argument `pf`, default 1;
+// LAPIS_B200_SPMM_PREFETCH=0 disables, N = gather groups ahead; 1 measured
+// best: C3 10.05 / 11.6 / 13.8 ms at 1 / 2 / 3, C4 1.64 -> 1.55 ms at 1)
+inline int spmm_prefetch_distance() {
+  static const int pf = [] {
+    const char* e = getenv("LAPIS_B200_SPMM_PREFETCH");
+    int v = e ? atoi(e) : 1;
+    return v < 0 ? 0 : (v > 4 ? 4 : v);
+  }();
+  return pf;
+}
 
 template <class T, class RP, class CI, int CPL, int U, bool EPI = false>
 __global__ void __launch_bounds__(256, 4)
@@ -247,7 +254,7 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                   const CI* __restrict__ colind, const T* __restrict__ values,
                   const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
                   const T* __restrict__ W = nullptr,
-                  unsigned long long* __restrict__ next = nullptr) {
+                  unsigned long long* __restrict__ next = nullptr, int pf = 1) {
   const int lane = threadIdx.x & 31;
   // EPI (fp32, k = 64, CPL = 2): Y is H, each finished row goes through the
   // GCN epilogue with W staged in shared memory
@@ -311,11 +318,11 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
           T nx_val = T(0);
           if (j0 + 32 + lane < je) { nx_col = (int64_t)colind[j0 + 32 + lane]; nx_val = values[j0 + 32 + lane]; }
           for (int t0 = 0; t0 < cnt; t0 += U) {
-            if (spmm_prefetch_on) {
+            if (pf) {
               // L2 prefetch of the NEXT group's X rows (no registers held): lane
               // l touches line (l / U) of entry t0 + U + l % U; past the chunk
               // end the next chunk's entries (colind already loaded) are used
-              const int pe = t0 + U * spmm_prefetch_on + (lane % U);
+              const int pe = t0 + U * pf + (lane % U);
               const int64_t pc = pe < 32 ? __shfl_sync(0xffffffffu, my_col, pe & 31)
                                          : __shfl_sync(0xffffffffu, nx_col, pe & 31);
               const int64_t pj = j0 + pe;
@@ -684,19 +691,7 @@ struct SpmmOp {
       const int64_t cap = (int64_t)num_sms() * 8;
       if (gblocks > cap) gblocks = cap;
       if (gblocks < 1) gblocks = 1;
-      {
-        static thread_local int pf_dev = -1;
-        int d = 0;
-        cudaGetDevice(&d);
-        if (pf_dev != d) {
-          const char* e = getenv("LAPIS_B200_SPMM_PREFETCH");  // "0" disables (A/B)
-          int on = e ? atoi(e) : 1;  // prefetch distance in gather groups (0 = off)
-          if (on < 0) on = 0;
-          if (on > 4) on = 4;
-          cudaMemcpyToSymbol(spmm_prefetch_on, &on, sizeof(on));
-          pf_dev = d;
-        }
-      }
+      const int pf = spmm_prefetch_distance();
       unsigned long long* next = nullptr;
       if (!spmm_static()) {
         LB_TRY(check_cuda(cudaMallocAsync((void**)&next, sizeof(*next), st), "alloc(spmm counter)"));
@@ -709,14 +704,14 @@ struct SpmmOp {
       } free_next{next, st};
 #define LB_BAT(CC) spmm_batch_kernel<T, RP, CI, CC, 8><<<(unsigned)gblocks, 256, 0, st>>>( \
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, \
-          nullptr, next)
+          nullptr, next, pf)
       bool fused = false;
       if constexpr (std::is_same<T, float>::value) {
         if (W) {
           if (cpl != 2 || k != GCN_F) return fail(LAPIS_B200_ERR_ARG, "gcn fused: k must be 64");
           spmm_batch_kernel<float, RP, CI, 2, 8, true><<<(unsigned)gblocks, 256, 0, st>>>(
               nrows, k, (const RP*)rowptr, (const CI*)colind, (const float*)values,
-              (const float*)X, ldx, (float*)Y, ldy, (const float*)W, next);
+              (const float*)X, ldx, (float*)Y, ldy, (const float*)W, next, pf);
           fused = true;
         }
       }
