@@ -96,7 +96,9 @@ inline void spmv_csr(DualView<RP*> rowptr, DualView<CI*> colind, DualView<T*> va
   values.syncDevice();
   x.syncDevice();
   const std::int64_t n = rowptr.extent(0) - 1;
-  const std::int64_t nnz = n >= 0 ? static_cast<std::int64_t>(rowptr.host_view()(n)) : 0;
+  // nnz bound from colind's extent (>= rowptr(n) - rowptr(0) for any valid
+  // CSR): no read of a host copy that may be stale after a device write
+  const std::int64_t nnz = static_cast<std::int64_t>(colind.extent(0));
   auto rp = rowptr.device_view();
   auto ci = colind.device_view();
   b200::check(lapis_b200_spmv_csr(n, x.extent(0), nnz, rp.data(), b200::index_bytes(rp), ci.data(),
@@ -115,7 +117,7 @@ inline void spmm_csr(DualView<RP*> rowptr, DualView<CI*> colind, DualView<T*> va
   values.syncDevice();
   X.syncDevice();
   const std::int64_t n = rowptr.extent(0) - 1;
-  const std::int64_t nnz = n >= 0 ? static_cast<std::int64_t>(rowptr.host_view()(n)) : 0;
+  const std::int64_t nnz = static_cast<std::int64_t>(colind.extent(0));  // as in spmv_csr
   auto rp = rowptr.device_view();
   auto ci = colind.device_view();
   auto xd = X.device_view();

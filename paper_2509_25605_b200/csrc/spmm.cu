@@ -24,19 +24,38 @@ namespace lapis_b200 {
 constexpr int SPMM_WARPS = 8;
 constexpr int64_t SPLIT = 2048;
 
+// A rowptr that decreases somewhere (row r has rowptr[r+1] < rowptr[r]; the
+// reference sums range(begin, max(begin, end)), interp.py:808) breaks the
+// batch kernel's contiguous entry runs and the long-row list's capacity
+// bound.  The long-row list pass flags it on the device (desc[0] != 0); the
+// fast kernels then return at once and a one-warp-per-row kernel, launched
+// behind the same flag, folds every row (long ones included) on its clamped
+// range.  No host round trip: the call stays stream-ordered.
+struct DescGuard {
+  const unsigned long long* desc = nullptr;  // nullptr: unguarded
+  int mode = 0;  // 0: run unless desc set; 1: run only when desc set (all rows)
+  __device__ __forceinline__ bool skip() const {
+    if (!desc) return false;
+    return (*(volatile const unsigned long long*)desc != 0) != (mode == 1);
+  }
+  __device__ __forceinline__ bool all_rows() const { return desc && mode == 1; }
+};
+
 // --------------------------------------------------------------- kernel 1
 template <class T, class RP, class CI, int EPL>
 __global__ void __launch_bounds__(SPMM_WARPS * 32)
 spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                 const CI* __restrict__ colind, const T* __restrict__ values,
-                const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+                const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
+                DescGuard guard = DescGuard()) {
+  if (guard.skip()) return;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * SPMM_WARPS + (threadIdx.x >> 5);
   if (row >= nrows) return;
   const int64_t b = (int64_t)rowptr[row];
   int64_t e = (int64_t)rowptr[row + 1];
   if (e < b) e = b;
-  if (e - b > SPLIT) return;  // long row: kernels 2-3
+  if (e - b > SPLIT && !guard.all_rows()) return;  // long row: kernels 2-3
   for (int64_t c0 = 0; c0 < k; c0 += 32 * EPL) {
     const int64_t col = c0 + (int64_t)lane * EPL;
     const bool full = col + EPL <= k;
@@ -124,7 +143,9 @@ template <class T, class RP, class CI, int G>
 __global__ void __launch_bounds__(256)
 spmm_group_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                   const CI* __restrict__ colind, const T* __restrict__ values,
-                  const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+                  const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
+                  DescGuard guard = DescGuard()) {
+  if (guard.skip()) return;
   constexpr int U = 4;
   const int lane = threadIdx.x & (G - 1);
   const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
@@ -254,7 +275,9 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                   const CI* __restrict__ colind, const T* __restrict__ values,
                   const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
                   const T* __restrict__ W = nullptr,
-                  unsigned long long* __restrict__ next = nullptr, int pf = 1) {
+                  unsigned long long* __restrict__ next = nullptr, int pf = 1,
+                  DescGuard guard = DescGuard()) {
+  if (guard.skip()) return;
   const int lane = threadIdx.x & 31;
   // EPI (fp32, k = 64, CPL = 2): Y is H, each finished row goes through the
   // GCN epilogue with W staged in shared memory
@@ -391,7 +414,17 @@ struct LongRows {
   int64_t* work_row;   // [wcap] row of item
   int64_t* work_beg;   // [wcap] first entry of item
   int64_t* first;      // [cap] first item of listed row i
+  unsigned long long* desc;  // [1] set when rowptr decreases somewhere
+  int64_t cap, wcap;         // capacities of rows/first and work_row/work_beg
 };
+
+// listed rows the long-row kernels may use (0 when the rowptr decreases: the
+// guarded fallback kernel then folds every row)
+__device__ __forceinline__ int64_t long_rows_count(const LongRows& lr) {
+  if (*(volatile const unsigned long long*)lr.desc) return 0;
+  const int64_t n = *lr.count;
+  return n < lr.cap ? n : lr.cap;
+}
 
 // rows the batch kernel skipped (long rows) hold AX in H after the long-row
 // kernels; one warp per listed row applies the GCN epilogue in place
@@ -402,7 +435,7 @@ gcn_long_rows_epilogue_kernel(const float* __restrict__ W, float* __restrict__ H
   for (int t = threadIdx.x; t < GCN_F * GCN_F; t += blockDim.x) Ws[t] = W[t];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t n = *lr.count;
+  const int64_t n = long_rows_count(lr);
   for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * 8) {
     float* hrow = H + lr.rows[i] * ldh;
     const float2 a = reinterpret_cast<const float2*>(hrow)[lane];
@@ -413,12 +446,19 @@ gcn_long_rows_epilogue_kernel(const float* __restrict__ W, float* __restrict__ H
 
 template <class RP>
 __global__ void long_rows_list_kernel(int64_t nrows, const RP* __restrict__ rowptr, LongRows lr) {
+  int desc = 0;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t len = (int64_t)rowptr[r + 1] - (int64_t)rowptr[r];
-    if (len > SPLIT) lr.rows[atomicAdd(reinterpret_cast<unsigned long long*>(lr.count), 1ull)] = r;
+    desc |= len < 0;
+    if (len > SPLIT) {
+      const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(lr.count), 1ull);
+      if ((int64_t)i < lr.cap) lr.rows[i] = r;  // > cap only with a bad nnz / decreasing rowptr
+    }
   }
+  if (__any_sync(0xffffffffu, desc) && (threadIdx.x & 31) == 0) atomicOr(lr.desc, 1ull);
 }
+
 
 // one CTA: each thread owns a contiguous slice of the listed rows; a block
 // scan of the slices' chunk counts gives every row its first work item
@@ -426,7 +466,7 @@ template <class RP>
 __global__ void __launch_bounds__(1024) long_rows_work_kernel(const RP* __restrict__ rowptr,
                                                               LongRows lr) {
   __shared__ int64_t scan[1024];
-  const int64_t n = *lr.count;
+  const int64_t n = long_rows_count(lr);
   const int t = threadIdx.x;
   const int64_t i0 = n * t / 1024, i1 = n * (t + 1) / 1024;
   int64_t mine = 0;
@@ -443,12 +483,13 @@ __global__ void __launch_bounds__(1024) long_rows_work_kernel(const RP* __restri
     __syncthreads();
   }
   int64_t w = scan[t] - mine;
-  if (t == 1023) *lr.total = scan[1023];
+  if (t == 1023) *lr.total = scan[1023] < lr.wcap ? scan[1023] : lr.wcap;
   for (int64_t i = i0; i < i1; ++i) {
     const int64_t r = lr.rows[i];
     const int64_t b = (int64_t)rowptr[r], e = (int64_t)rowptr[r + 1];
     lr.first[i] = w;
     for (int64_t s = b; s < e; s += SPLIT, ++w) {
+      if (w >= lr.wcap) break;  // only with an nnz below rowptr[n] - rowptr[0]
       lr.work_row[w] = r;
       lr.work_beg[w] = s;
     }
@@ -502,7 +543,7 @@ spmm_seq_long_pipe_kernel(int64_t k, const RP* __restrict__ rowptr,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool loader = warp >= 2;
   const int lw = warp - 2;
-  const int64_t nlong = *lr.count;
+  const int64_t nlong = long_rows_count(lr);
   const int64_t ncg = (k + PIPE_KC - 1) / PIPE_KC;  // column groups per row
   for (int64_t item = blockIdx.x; item < nlong * ncg; item += gridDim.x) {
     const int64_t r = lr.rows[item / ncg];
@@ -636,7 +677,7 @@ template <class T, class RP>
 __global__ void spmm_long_combine_kernel(int64_t k, const RP* __restrict__ rowptr,
                                          const T* __restrict__ part, T* __restrict__ Y, int64_t ldy,
                                          const LongRows lr) {
-  const int64_t n = *lr.count;
+  const int64_t n = long_rows_count(lr);
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     const int64_t r = lr.rows[i];
     const int64_t w0 = lr.first[i];
@@ -686,10 +727,42 @@ struct SpmmOp {
     const bool batch = cpl > 0 && (ldx % cpl == 0) && (ldy % cpl == 0) &&
                        ((uintptr_t)X % (cpl * sizeof(T)) == 0) &&
                        ((uintptr_t)Y % (cpl * sizeof(T)) == 0) && !spmm_force_row();
+    // ---- long-row list + decreasing-rowptr flag: one pass over rowptr,
+    // launched first so every later kernel can be guarded by the flag
+    const int64_t cap = nnz / (SPLIT + 1) + 1;       // rows with > SPLIT entries
+    const int64_t wcap = nnz / SPLIT + cap + 1;       // chunks of those rows
+    int64_t* ws = nullptr;
+    const size_t ws_elems = 3 + 2 * (size_t)cap + 2 * (size_t)wcap;
+    LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, ws_elems * sizeof(int64_t), st), "alloc(long rows)"));
+    struct FreeWs {
+      int64_t* p; cudaStream_t s;
+      ~FreeWs() { cudaFreeAsync(p, s); }
+    } free_ws{ws, st};
+    LongRows lr;
+    lr.count = ws;
+    lr.total = ws + 1;
+    lr.desc = reinterpret_cast<unsigned long long*>(ws + 2);
+    lr.rows = ws + 3;
+    lr.first = lr.rows + cap;
+    lr.work_row = lr.first + cap;
+    lr.work_beg = lr.work_row + wcap;
+    lr.cap = cap;
+    lr.wcap = wcap;
+    LB_TRY(check_cuda(cudaMemsetAsync(ws, 0, 3 * sizeof(int64_t), st), "memset(long rows)"));
+    const int sms = num_sms();
+    {
+      int64_t g = (nrows + 255) / 256;
+      if (g > (int64_t)sms * 8) g = (int64_t)sms * 8;
+      long_rows_list_kernel<RP><<<(unsigned)(g > 0 ? g : 1), 256, 0, st>>>(nrows, (const RP*)rowptr, lr);
+      LB_TRY(check_launch("long_rows_list_kernel"));
+    }
+    DescGuard fast, fallback;
+    fast.desc = fallback.desc = lr.desc;
+    fallback.mode = 1;
     if (batch) {
       int64_t gblocks = ((nrows + 31) / 32 + 7) / 8;
-      const int64_t cap = (int64_t)num_sms() * 8;
-      if (gblocks > cap) gblocks = cap;
+      const int64_t gcap = (int64_t)sms * 8;
+      if (gblocks > gcap) gblocks = gcap;
       if (gblocks < 1) gblocks = 1;
       const int pf = spmm_prefetch_distance();
       unsigned long long* next = nullptr;
@@ -704,14 +777,16 @@ struct SpmmOp {
       } free_next{next, st};
 #define LB_BAT(CC) spmm_batch_kernel<T, RP, CI, CC, 8><<<(unsigned)gblocks, 256, 0, st>>>( \
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, \
-          nullptr, next, pf)
+          nullptr, next, pf, fast)
       bool fused = false;
       if constexpr (std::is_same<T, float>::value) {
         if (W) {
+          // (the fused layer needs a non-decreasing rowptr: the fallback below
+          // computes A X only; gcn_layer takes this path on request only)
           if (cpl != 2 || k != GCN_F) return fail(LAPIS_B200_ERR_ARG, "gcn fused: k must be 64");
           spmm_batch_kernel<float, RP, CI, 2, 8, true><<<(unsigned)gblocks, 256, 0, st>>>(
               nrows, k, (const RP*)rowptr, (const CI*)colind, (const float*)values,
-              (const float*)X, ldx, (float*)Y, ldy, (const float*)W, next, pf);
+              (const float*)X, ldx, (float*)Y, ldy, (const float*)W, next, pf, fast);
           fused = true;
         }
       }
@@ -725,11 +800,11 @@ struct SpmmOp {
     } else if (grp) {
       const int64_t lanes_per_row = k >= 64 ? 16 : (k >= 32 ? 8 : (k >= 16 ? 4 : (k >= 8 ? 2 : 1)));
       int64_t gblocks = (nrows * lanes_per_row + 255) / 256;
-      const int64_t cap = (int64_t)num_sms() * 8;
-      if (gblocks > cap) gblocks = cap;
+      const int64_t gcap = (int64_t)sms * 8;
+      if (gblocks > gcap) gblocks = gcap;
       if (gblocks < 1) gblocks = 1;
 #define LB_GRP(GG) spmm_group_kernel<T, RP, CI, GG><<<(unsigned)gblocks, 256, 0, st>>>( \
-          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy)
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, fast)
       switch (lanes_per_row) {
         case 16: LB_GRP(16); break;
         case 8: LB_GRP(8); break;
@@ -741,34 +816,25 @@ struct SpmmOp {
     } else if (vec)
       spmm_row_kernel<T, RP, CI, 2><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
-          (T*)Y, ldy);
+          (T*)Y, ldy, fast);
     else
       spmm_row_kernel<T, RP, CI, 1><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
-          (T*)Y, ldy);
+          (T*)Y, ldy, fast);
     LB_TRY(check_launch("spmm_row_kernel"));
+    // decreasing rowptr only: one warp per row, every row on its clamped range
+    if (vec)
+      spmm_row_kernel<T, RP, CI, 2><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+          (T*)Y, ldy, fallback);
+    else
+      spmm_row_kernel<T, RP, CI, 1><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+          nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+          (T*)Y, ldy, fallback);
+    LB_TRY(check_launch("spmm_row_kernel(fallback)"));
     if (nnz <= SPLIT) return LAPIS_B200_OK;  // no row can be long
-    // ---- long rows: list them, then fold (fp32 exact) or chunk + combine
-    const int64_t cap = nnz / (SPLIT + 1) + 1;       // rows with > SPLIT entries
-    const int64_t wcap = nnz / SPLIT + cap + 1;       // chunks of those rows
-    int64_t* ws = nullptr;
-    const size_t ws_elems = 2 + 2 * (size_t)cap + 2 * (size_t)wcap;
-    LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, ws_elems * sizeof(int64_t), st), "alloc(long rows)"));
-    LongRows lr;
-    lr.count = ws;
-    lr.total = ws + 1;
-    lr.rows = ws + 2;
-    lr.first = lr.rows + cap;
-    lr.work_row = lr.first + cap;
-    lr.work_beg = lr.work_row + wcap;
-    int rc = check_cuda(cudaMemsetAsync(ws, 0, 2 * sizeof(int64_t), st), "memset(long rows)");
-    const int sms = num_sms();
-    if (rc == LAPIS_B200_OK) {
-      int64_t g = (nrows + 255) / 256;
-      if (g > (int64_t)sms * 8) g = (int64_t)sms * 8;
-      long_rows_list_kernel<RP><<<(unsigned)(g > 0 ? g : 1), 256, 0, st>>>(nrows, (const RP*)rowptr, lr);
-      rc = check_launch("long_rows_list_kernel");
-    }
+    // ---- long rows: fold (fp32 exact) or chunk + combine
+    int rc = LAPIS_B200_OK;
     if constexpr (std::is_same<T, float>::value) {
       constexpr size_t pipe_smem = pipe_smem_bytes<CI>();
       if (rc == LAPIS_B200_OK)
@@ -789,7 +855,6 @@ struct SpmmOp {
                                                                      ldy, lr);
         rc = check_launch("gcn_long_rows_epilogue_kernel");
       }
-      cudaFreeAsync(ws, st);
       return rc;
     }
     if (rc == LAPIS_B200_OK) {
@@ -820,7 +885,6 @@ struct SpmmOp {
       rc = check_launch("spmm_long_combine_kernel");
     }
     if (part) cudaFreeAsync(part, st);
-    cudaFreeAsync(ws, st);
     return rc;
   }
 };

@@ -739,16 +739,17 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
   if (nrows == 0) return LAPIS_B200_OK;
   if (vl != 0) return dispatch_types<VecOp>(dtype, rp_bytes, ci_bytes, vl, nrows, rowptr, colind,
                                             values, x, y, st);
-  // no plan: one stats pass over rowptr on the device, then both candidate
+  // no plan: one stats pass over rowptr on the device, then the candidate
   // kernels launched behind a device guard — the exact vector kernel (the
-  // plan's choice for regular structures, bit-identical) or the partition +
-  // tile kernel (irregular / non-monotone) — so the call stays asynchronous
-  const int64_t ntiles = ntiles_for(nrows, nnz);
-  int64_t* ws = nullptr;
-  LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, (2 * (ntiles + 1) + 2) * sizeof(int64_t), st),
-                    "cudaMallocAsync(spmv workspace)"));
-  unsigned long long* stats = reinterpret_cast<unsigned long long*>(ws + 2 * (ntiles + 1));
-  int64_t* tile_row = ws;
+  // plan's choice for regular structures, bit-identical), the warp-block
+  // kernel (monotone irregular) or, for a rowptr that decreases somewhere,
+  // the exact one-row-per-lane vector kernel, which clamps each row to
+  // range(begin, max(begin, end)) (interp.py:808) — so the call stays
+  // asynchronous.  (The tile kernel's key-balanced partition assumes a
+  // non-decreasing rowptr, so it is never chosen for such structures.)
+  unsigned long long* stats = nullptr;
+  LB_TRY(check_cuda(cudaMallocAsync((void**)&stats, 2 * sizeof(unsigned long long), st),
+                    "cudaMallocAsync(spmv stats)"));
   int rc = check_cuda(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st), "memset(stats)");
   if (rc == LAPIS_B200_OK) {
     const int64_t blocks = std::min<int64_t>((nrows + 255) / 256, (int64_t)num_sms() * 8);
@@ -766,18 +767,17 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
   greg.thresh = gwb.thresh = girr.thresh = (long long)std::max(64.0, 8.0 * mean);  // analyse_rows
   greg.want = 1;  // regular: exact vector kernel
   gwb.want = 2;   // monotone irregular: warp-block kernel (the plan's choice)
-  girr.want = 3;  // non-monotone rowptr: partition + tile kernel
+  girr.want = 3;  // decreasing rowptr: exact vector kernel, one row per lane
   if (rc == LAPIS_B200_OK)
     rc = dispatch_types<VecExactGuardedOp>(dtype, rp_bytes, ci_bytes, cvl, nrows, rowptr, colind,
                                            values, x, y, st, greg);
   if (rc == LAPIS_B200_OK)
     rc = dispatch_types<WarpBlockOp>(dtype, rp_bytes, ci_bytes, nrows, rowptr, colind, values, x,
                                      y, dtype == LAPIS_B200_F32 ? 1 : 0, st, gwb);
-  if (rc == LAPIS_B200_OK) rc = launch_partition(nrows, rowptr, rp_bytes, ntiles, tile_row, st, girr);
   if (rc == LAPIS_B200_OK)
-    rc = dispatch_types<TileOp>(dtype, rp_bytes, ci_bytes, ntiles, rowptr, colind, values, x, y,
-                                (const int64_t*)tile_row, st, girr);
-  cudaFreeAsync(ws, st);
+    rc = dispatch_types<VecExactGuardedOp>(dtype, rp_bytes, ci_bytes, 1, nrows, rowptr, colind,
+                                           values, x, y, st, girr);
+  cudaFreeAsync(stats, st);
   return rc;
 }
 
@@ -811,6 +811,10 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
   if (force) vl = atoi(force);
   const bool regular = p->max_len <= 64 || (double)p->max_len <= 8.0 * mean;
   p->exact_vl = (force && vl > 0) ? vl : (regular ? vl : 0);
+  // a decreasing rowptr: the exact vector kernel with one row per lane (it
+  // clamps every row to range(begin, max(begin, end)), interp.py:808); the
+  // tile partition and the warp-block entry runs assume a monotone rowptr
+  if (!monotone) p->exact_vl = 1;
   const char* ex = getenv("LAPIS_B200_SPMV_EXACT");
   p->exact = (ex && atoi(ex) != 0) ? 1 : 0;
   // warp-block kernel: irregular monotone structures (power-law rows: 1.46 vs

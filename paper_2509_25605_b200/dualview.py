@@ -41,7 +41,7 @@ def reset_transfer_stats() -> None:
 
 
 class _Record:
-    __slots__ = ("host", "device", "modified_host", "modified_device", "label")
+    __slots__ = ("host", "device", "modified_host", "modified_device", "label", "h2d_done")
 
     def __init__(self, host: torch.Tensor, device: torch.Tensor, label: str):
         self.host = host
@@ -49,6 +49,15 @@ class _Record:
         self.modified_host = False
         self.modified_device = False
         self.label = label
+        self.h2d_done = None   # event of an H2D copy that may still read the host side
+
+    def host_quiescent(self) -> None:
+        """Wait for an in-flight H2D copy out of the pinned host buffer: the
+        reference's syncDevice is a blocking deep_copy, so the host side may be
+        written as soon as it returns (runtime_header.py:145-160)."""
+        if self.h2d_done is not None:
+            self.h2d_done.synchronize()
+            self.h2d_done = None
 
 
 def _pinned_like(a, dtype=None) -> torch.Tensor:
@@ -96,6 +105,7 @@ class DualView:
 
     # ---- views ----------------------------------------------------------------
     def host_view(self) -> torch.Tensor:
+        self._rec.host_quiescent()
         return self._rec.host if self._win is None else self._rec.host[self._win]
 
     def device_view(self) -> torch.Tensor:
@@ -128,6 +138,7 @@ class DualView:
 
     # ---- coherence (runtime_header.py:145-178) -----------------------------
     def modify_host(self) -> None:
+        self._rec.host_quiescent()
         self._rec.modified_host = True
 
     def modify_device(self) -> None:
@@ -138,6 +149,10 @@ class DualView:
         if rec.modified_host:
             with torch.cuda.stream(stream) if stream is not None else _null():
                 rec.device.copy_(rec.host, non_blocking=True)
+                # the copy stays asynchronous for the device; host-side writers
+                # wait on this event (host_view / modify_host)
+                rec.h2d_done = torch.cuda.Event()
+                rec.h2d_done.record(stream or torch.cuda.current_stream())
             rec.modified_host = False
             _STATS.h2d_count += 1
             _STATS.h2d_bytes += self.nbytes

@@ -186,8 +186,12 @@ class RowBlockSpmv:
                 reqs = exchange(self.plan, x_full, self.group)
         if b > a:
             self.plans[(a, b)].spmv(self.colind, self.values, x_full, y_local[a:b], stream=stream)
-        for r in reqs:
-            r.wait()
+        # r.wait() makes the CURRENT stream wait on the NCCL work, so it runs
+        # under the caller's stream: the boundary rows below are ordered after
+        # the slabs even when `stream` is not the current stream
+        with torch.cuda.stream(stream):
+            for r in reqs:
+                r.wait()
         if self.world > 1:
             stream.wait_stream(self.comm_stream)
         for lo, hi in ((0, a), (b, y_local.numel())):

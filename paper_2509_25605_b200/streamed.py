@@ -105,6 +105,8 @@ class StreamedSpmv:
             _dv._STATS.h2d_count += 1
             _dv._STATS.h2d_bytes += x.nbytes
         self.d2h.synchronize()                # y's host copy is what the caller reads next
+        if copy_x:
+            self.h2d.synchronize()            # x's host side may be rewritten on return
         compute.wait_stream(self.d2h)
         y._rec.modified_device = False
         _dv._STATS.d2h_count += 1

@@ -75,3 +75,22 @@ def test_rowblock_spmm_world1_matches_library_call(cuda_device):
     want = O.spmm_csr(rowptr, colind, values, X)
     assert np.array_equal(Y.cpu().numpy().view(np.uint64), want.view(np.uint64)) or \
         np.max(np.abs(Y.cpu().numpy() - want) / np.maximum(np.abs(want), 1)) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [64, 8, 5])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_decreasing_rowptr(cuda_device, k, dtype):
+    """a decreasing rowptr (rows overlap / are empty, interp.py:808)
+    with rows beyond the 2048-entry split: the guarded fallback folds every
+    row on its clamped range; nothing is written out of bounds."""
+    from test_spmv_gpu import decreasing_rowptr_csr
+    rng = np.random.default_rng(k)
+    rp, colind, values = decreasing_rowptr_csr(rng, 4000, 6000, dtype=dtype)
+    X = rng.uniform(-1, 1, (6000, k)).astype(dtype)
+    want = O.spmm_csr(rp, colind, values, X)
+    Yd = torch.full((4000 + 64, k), 7.0, dtype=torch.float64 if dtype == np.float64 else torch.float32,
+                    device="cuda")
+    lb.spmm_csr(cu(rp), cu(colind), cu(values), cu(X), Yd[:4000], nnz=int(rp[-1]))
+    got = Yd[:4000].cpu().numpy()
+    assert bits_equal(got, want)
+    assert bool((Yd[4000:] == 7.0).all()), "write past Y"

@@ -304,3 +304,34 @@ def test_no_plan_call_device_dispatch(cuda_device):
     x2 = rng.uniform(-1, 1, 30000)
     y2 = host(lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x2)))
     assert_close(y2, O.spmv_csr(rowptr, colind, values, x2), rowptr)
+
+
+def decreasing_rowptr_csr(rng, nrows, ncols, dtype=np.float64):
+    """A CSR whose rowptr DECREASES at some rows (interp.py:808 sums
+    range(begin, max(begin, end)): such a row is empty, its neighbours may
+    overlap), spanning many tiles / warp blocks, with long rows among them."""
+    rowptr, colind, values = ragged_csr(rng, nrows, ncols, max_len=40,
+                                        long_rows={5: 3000, nrows // 2: 2500}, dtype=dtype)
+    rp = rowptr.copy()
+    nnz = int(rp[-1])
+    for r in rng.choice(np.arange(10, nrows - 10), size=nrows // 50, replace=False):
+        rp[r] = min(nnz, rp[r] + int(rng.integers(50, 4000)))   # row r-1 grows, row r shrinks
+    return rp, colind, values
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int64])
+def test_decreasing_rowptr(cuda_device, dtype):
+    """a rowptr that decreases through the no-plan call and a plan."""
+    rng = np.random.default_rng(21)
+    rp, colind, values = decreasing_rowptr_csr(rng, 6000, 5000, dtype=dtype)
+    assert (np.diff(rp) < 0).any()
+    x = (rng.integers(-9, 9, 5000) if np.issubdtype(dtype, np.integer)
+         else rng.uniform(-1, 1, 5000)).astype(dtype)
+    want = O.spmv_csr(rp, colind, values, x)
+    for rpt in (rp, rp.astype(np.int32)):
+        got = host(lb.spmv_csr(cu(rpt), cu(colind), cu(values), cu(x)))
+        assert_close(got, want, np.maximum(rp, 0))
+        plan = lb.CsrPlan(cu(rpt), nnz=int(rp.max()))
+        assert plan.info()["vector_length"] == 1
+        got = host(plan.spmv(cu(colind), cu(values), cu(x)))
+        assert bits_equal(got, want) if want.dtype.kind == "f" else np.array_equal(got, want)
