@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Benchmark of the LAPIS hot path on B200 (contract: one JSON line from rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c1|c3|c2f32|c2f64]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload c5|c1|c3|c4|c2f32|c2f64|gemv|mtx] [--impl ours|reference]
+                    [--extra c1,c2f32,...|none]
 
 Default workload (BASELINE.json config 5, the largest single-GPU config and
 the one the metric's multi-GPU scaling is quoted on): CSR SpMV fp64 on the
@@ -10,21 +11,30 @@ the one the metric's multi-GPU scaling is quoted on): CSR SpMV fp64 on the
 int64 rowptr / int32 colind, row-block sharded over the ranks with the halo
 exchange of x (paper_2509_25605_b200/sharded.py).  A step is one SpMV over the
 whole matrix.  Inputs (69 GB) exceed L2 (126 MB) many times, so no flush is
-needed between steps.  Other workloads (--workload) are config 1 (SpMV, 5-point
-Laplacian, 84 MB < L2: steps rotate over input copies), config 3 (SpMM, K = 64, power-law
-matrix) and config 2 (dense matmul 4096^3, f32 or f64).
+needed between steps.  At N = 1 the same line carries a `workloads` object with
+the other configs measured in the same run (config 1 SpMV, config 2 matmul
+f32 / f64, config 3 SpMM, config 4 GCN layer), each with its roofline, e2e,
+CPU baseline and parity sample.
 
 `value` is device-resident throughput (algorithmic bytes or flops / step time,
 max over ranks); `e2e` repeats the step through the public DualView + C-ABI
 path with the step's inputs copied host->device and the result device->host
 every step (pinned host buffers).  `cpu_baseline` runs the reference's own
 emitted Kokkos C++ on its serial stub (oracle/_ref) on a bounded sample of the
-same workload with the host's threads, and doubles as the parity check of that
-sample against the GPU result.
+same workload — on all host cores (row blocks, bitwise identical) and on one
+core — and doubles as the parity check of that sample against the GPU result.
+
+Inputs: every random number comes from numpy generators defined in
+synth_inputs.py (SURVEY 8(d) seeds), so the reference arm (`--impl
+reference`) builds the very same sample on the host without importing this
+backend; the stencil matrices are generated on the device by the backend and
+on the host by the reference arm (same formula), so the parity sample also
+pins the device generator at full scale.
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -40,7 +50,10 @@ import torch.distributed as dist
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+import synth_inputs as S  # noqa: E402  (numpy only: shared by both arms)
+
 METRIC = "SpMV/SpMM HBM GB/s (% of peak), matmul TFLOP/s, at 1/2/4/8 B200 vs CPU ref"
+EXTRA_DEFAULT = "c1,c2f32,c2f64,c3,c4"
 
 
 # --------------------------------------------------------------------- utilities
@@ -66,7 +79,7 @@ class ClockSampler:
     def __init__(self, device_index: int):
         self.dev = device_index
         self.proc = None
-        self.path = Path(f"/tmp/lapis_clocks_{os.getpid()}.csv")
+        self.path = Path(f"/tmp/lapis_clocks_{os.getpid()}_{time.monotonic_ns()}.csv")
 
     def __enter__(self):
         try:
@@ -172,6 +185,219 @@ def parity_report(got, want, tol):
             "within_tolerance": bool(bitexact or maxrel <= tol)}
 
 
+# ------------------------------------------------- host inputs (both arms)
+_MEMO: dict = {}
+
+
+def memo(key, make):
+    if key not in _MEMO:
+        _MEMO[key] = make()
+    return _MEMO[key]
+
+
+def drop_memo():
+    _MEMO.clear()
+    gc.collect()
+
+
+WORKLOAD_NAMES = {
+    "c5": "config5: CSR SpMV fp64, 3-D 27-point stencil n={n}",
+    "c1": "config1: CSR SpMV fp64, 2-D 5-point Laplacian n={n}",
+    "c3": "config3: CSR x dense SpMM fp64, K=64, power-law (Chung-Lu, Pareto 2.5) {n} rows",
+    "c4": "config4: GCN layer relu((A_hat X) W) fp32, power-law A_hat {n} rows, 64->64",
+    "c2f32": "config2: dense linalg.matmul {n}^3 f32 (mode {mode})",
+    "c2f64": "config2: dense linalg.matmul {n}^3 f64 (mode {mode})",
+    "gemv": "matvec: linalg.matvec f64 {n} x {n} (row_fold_pipe_kernel, reference order)",
+    "mtx": "matrix market SpMV fp64: {mtx}",
+}
+DEFAULT_N = {"c5": 585, "c1": 1000, "c3": 10_000_000, "c4": 1_000_000, "c2f32": 4096,
+             "c2f64": 4096, "gemv": 16384, "mtx": 0}
+
+
+class HostSample:
+    """A bounded sample of a workload for the reference's CPU path: the
+    emitted C++ on its serial stub (oracle/_ref), `run(reps, threads)` ->
+    (output, seconds per rep); `region` tells the GPU arm which part of its
+    own output the sample covers."""
+
+    def __init__(self, run, work, desc, tol, region, max_threads=None):
+        self.run, self.work, self.desc, self.tol = run, work, desc, tol
+        self.region, self.max_threads = region, max_threads
+
+
+def _stencil_sample(points, n, seed, rows_sample):
+    from oracle import ref as R
+    N = n ** 3 if points == 27 else n * n
+    mid = N // 2
+    a, b = (0, N) if N <= rows_sample else (mid - rows_sample // 2, mid + rows_sample // 2)
+    rp, ci, v = S.stencil_rows(points, n, a, b, colind_dtype=np.int64)
+    x = memo(("x", points, n, seed), lambda: S.stencil_x(points, n, seed))
+    nnz = int(rp[-1])
+
+    def run(reps, threads):
+        return R.spmv_csr(rp, ci, v, x, reps=reps, threads=threads)
+
+    work = nnz * 12 + (b - a + 1) * 8 + (b - a) * 8 * 2
+    desc = (f"rows [{a}, {b}) of the same matrix ({nnz} nnz, host-generated): reference emitted "
+            "Kokkos C++ (tests/fixtures/spmv.mlir, index colind) on its serial stub")
+    return HostSample(run, work, desc, 1e-12, (a, b))
+
+
+def powerlaw_spec(n, seed, mean=10.0):
+    return memo(("spec", n, seed, mean), lambda: S.PowerLawSpec(n, mean=mean, seed=seed))
+
+
+def _spmm_sample(n, k, seed, rows_sample):
+    from oracle import ref as R
+    spec = powerlaw_spec(n, seed)
+    b = min(n, max(1, rows_sample // 40))
+    rp, ci = S.powerlaw_structure_host(spec, rows=b)
+    v = S.powerlaw_values(spec, 0, first=0, count=int(rp[-1]))
+    X = memo(("X", n, k, seed), lambda: S.spmm_dense(n, k, seed))
+    nnz = int(rp[-1])
+
+    def run(reps, threads):
+        return R.spmm_csr(rp, ci, v, X, reps=reps, threads=threads)
+
+    work = nnz * 12 + (b + 1) * 8 + b * k * 8 * 2
+    desc = (f"rows [0, {b}) of the same matrix ({nnz} nnz, host-generated): reference emitted "
+            "Kokkos C++ of oracle/ir/spmm.mlir on its serial stub")
+    return HostSample(run, work, desc, 1e-12, (0, b))
+
+
+def gcn_host_inputs(n, f, seed):
+    def make():
+        spec = powerlaw_spec(n, seed)
+        rp, ci = S.powerlaw_structure_host(spec)
+        X, W = S.gcn_features(n, f, seed)
+        return rp, ci, S.gcn_values_host(rp, ci), X, W
+    return memo(("gcn", n, f, seed), make)
+
+
+def _gcn_sample(n, f, seed, rows_sample, host=None):
+    from oracle import ref as R
+    rp_all, ci_all, v_all, X, W = host if host is not None else gcn_host_inputs(n, f, seed)
+    b = min(n, max(1, rows_sample // 80))
+    e = int(rp_all[b])
+    rp, ci, v = rp_all[:b + 1].copy(), ci_all[:e], v_all[:e]
+
+    def run(reps, threads):
+        return R.gcn(rp, ci, v, X, W, reps=reps, threads=threads)
+
+    work = e * 8 + (b + 1) * 8 + b * f * 4 * 3 + f * f * 4
+    desc = (f"rows [0, {b}) ({e} nnz): reference emitted Kokkos C++ of oracle/ir/gcn_f32.mlir "
+            "on its serial stub")
+    return HostSample(run, work, desc, 1e-5, (0, b))
+
+
+def _matmul_sample(n, dt, seed, rows_sample, threads_hint):
+    from oracle import ref as R
+    A, B = memo(("dense", n, np.dtype(dt).name, seed), lambda: S.dense_operands(n, dt, seed))
+    rows = max(threads_hint, min(n, rows_sample // 250_000))
+    Ar = np.ascontiguousarray(A[:rows])
+
+    def run(reps, threads):
+        return R.matmul(Ar, B, reps=reps, threads=threads)
+
+    tag = "f32" if dt == np.float32 else "f64"
+    desc = (f"rows [0, {rows}) of C: reference emitted Kokkos C++ of oracle/ir/matmul_{tag}.mlir "
+            "(TeamPolicy nest) on its serial stub")
+    return HostSample(run, 2.0 * rows * n * n, desc, 1e-5 if dt == np.float32 else 1e-12,
+                      (0, rows))
+
+
+def gemv_host(n):
+    def make():
+        g = np.random.default_rng(6)
+        A = g.uniform(-1.0, 1.0, (n, n))
+        x = g.uniform(-1.0, 1.0, n)
+        return A, x
+    return memo(("gemv", n), make)
+
+
+def _gemv_sample(n, rows_sample):
+    from oracle import ref as R
+    A, x = gemv_host(n)
+    rows = min(n, max(1, rows_sample // 4000))
+    Ar = np.ascontiguousarray(A[:rows])
+
+    def run(reps, threads):
+        return R.matvec(Ar, x, reps=reps)
+
+    desc = (f"rows [0, {rows}) of the same A: reference emitted Kokkos C++ of "
+            "oracle/ir/matvec_f64.mlir on its serial stub")
+    return HostSample(run, (rows * n + n + rows) * 8, desc, 1e-12, (0, rows), max_threads=1)
+
+
+def _mtx_sample(path, rows_sample):
+    from oracle import ref as R
+    import scipy.io
+    import scipy.sparse
+    A = scipy.sparse.csr_matrix(scipy.io.mmread(path))
+    A.sort_indices()
+    b = min(A.shape[0], rows_sample)
+    rp = A.indptr[:b + 1].astype(np.int64)
+    ci = A.indices[:rp[-1]].astype(np.int64)
+    v = A.data[:rp[-1]].astype(np.float64)
+    x = np.random.default_rng(7).uniform(-1.0, 1.0, A.shape[1])
+
+    def run(reps, threads):
+        return R.spmv_csr(rp, ci, v, x, reps=reps, threads=threads)
+
+    work = int(rp[-1]) * 12 + (b + 1) * 8 + b * 8 * 2
+    desc = f"rows [0, {b}) ({int(rp[-1])} nnz): reference emitted Kokkos C++ on its serial stub"
+    return HostSample(run, work, desc, 1e-12, (0, b))
+
+
+def host_sample(key, args, n, threads) -> HostSample:
+    if key == "c5":
+        return _stencil_sample(27, n, 5, args.cpu_rows)
+    if key == "c1":
+        return _stencil_sample(5, n, 1, args.cpu_rows)
+    if key == "c3":
+        return _spmm_sample(n, 64, 1, args.cpu_rows)
+    if key == "c4":
+        return _gcn_sample(n, 64, 4, args.cpu_rows)
+    if key in ("c2f32", "c2f64"):
+        dt = np.float32 if key == "c2f32" else np.float64
+        return _matmul_sample(n, dt, 3 if dt == np.float32 else 2, args.cpu_rows, threads)
+    if key == "gemv":
+        return _gemv_sample(n, args.cpu_rows)
+    if key == "mtx":
+        return _mtx_sample(args.mtx, args.cpu_rows)
+    raise KeyError(key)
+
+
+def time_cpu(sample: HostSample, threads: int, seconds: float, min_reps: int):
+    """Median seconds per rep of the sample on `threads` host threads, with
+    enough reps for about `seconds` of CPU work; returns (output, median, reps)."""
+    out, times = sample.run(min_reps, threads)
+    t = float(np.median(times))
+    reps = int(min(2000, max(min_reps, np.ceil(seconds / max(t, 1e-6)))))
+    if reps > min_reps:
+        out, times = sample.run(reps, threads)
+        t = float(np.median(times))
+    return out, t, len(times)
+
+
+def cpu_baseline(sample: HostSample, unit: str, threads: int, seconds: float, reps: int):
+    """The reference CPU path on all host cores (row blocks on std::threads,
+    bitwise identical to one thread) and on one core (the stub is
+    serial by construction)."""
+    from oracle import ref as R
+    scale = 1e9 if unit == "GB/s" else 1e12
+    cores = min(threads, sample.max_threads or threads)
+    want, t, n = time_cpu(sample, cores, seconds, reps)
+    base = {"value": round(sample.work / t / scale, 4), "unit": unit, "cores": cores,
+            "kind": "reference", "sample": f"{sample.desc}, {cores} row blocks, median of {n} reps",
+            "seconds_per_rep": t, "build": R.compile_flags()}
+    if cores > 1:
+        _, t1, n1 = time_cpu(sample, 1, seconds / 2, max(1, reps // 2))
+        base["one_core"] = {"value": round(sample.work / t1 / scale, 4), "unit": unit,
+                            "cores": 1, "seconds_per_rep": t1, "reps": n1}
+    return base, want
+
+
 # ------------------------------------------------------------------- workloads
 class Workload:
     unit = "GB/s"
@@ -179,9 +405,13 @@ class Workload:
     dtype = "f64"
     flush = None
     scaling = "strong"
+    key = ""
 
     def launches_per_step(self) -> int:
         return 1
+
+    def gpu_region(self, region):
+        raise NotImplementedError
 
 
 class StencilSpmv(Workload):
@@ -190,6 +420,7 @@ class StencilSpmv(Workload):
     def __init__(self, args, rank, world, points=27, n=585, x_seed=5):
         import paper_2509_25605_b200 as lb
         from paper_2509_25605_b200 import sharded
+        self.key = "c5" if points == 27 else "c1"
         self.lb, self.args, self.rank, self.world = lb, args, rank, world
         self.points, self.n, self.x_seed = points, n, x_seed
         self.N = n ** 3 if points == 27 else n * n
@@ -198,7 +429,7 @@ class StencilSpmv(Workload):
         self.stream = torch.cuda.current_stream()
         self.rowptr, self.colind, self.values = lb.synth_stencil(points, n, self.r0, self.r1)
         self.nnz_local = int(self.rowptr[-1].item())
-        self.x_host = np.random.default_rng(x_seed).uniform(-1.0, 1.0, self.N)
+        self.x_host = memo(("x", points, n, x_seed), lambda: S.stencil_x(points, n, x_seed))
         self.x = torch.from_numpy(self.x_host).cuda()          # indexed by global column
         self.y = torch.empty(self.r1 - self.r0, dtype=torch.float64, device="cuda")
         self.op = sharded.RowBlockSpmv(self.rowptr, self.colind, self.values, self.r0, self.r1,
@@ -223,23 +454,22 @@ class StencilSpmv(Workload):
 
     @property
     def name(self):
-        return (f"config5: CSR SpMV fp64, 3-D 27-point stencil n={self.n}" if self.points == 27
-                else f"config1: CSR SpMV fp64, 2-D 5-point Laplacian n={self.n}")
+        return WORKLOAD_NAMES[self.key].format(n=self.n)
 
     def nnz_global(self):
-        n = self.n
-        return (3 * n - 2) ** 3 if self.points == 27 else 5 * n * n - 4 * n
+        return S.stencil_nnz(self.points, self.n)
 
     def config(self):
-        return {"workload": self.name, "rows": self.N, "nnz": self.nnz_global(),
-                "index_layout": "rowptr int64, colind int32", "x": f"U(-1,1) seed {self.x_seed}",
-                "sharding": f"row blocks x{self.world}, halo exchange of x (NCCL P2P)",
-                **({"launch": self.graph_note} if self.graphs else {}),
-                "l2": ("inputs >> L2 (126 MB), no flush needed" if len(self.rot) == 1 else
-                       f"inputs < L2: steps rotate over {len(self.rot)} device copies of the "
-                       f"whole input ({len(self.rot) * self.work_local() / 1e6:.0f} MB > 3 x L2), "
-                       "no flush"),
-                "parallelism": f"rowblock{self.world}"}
+        return stencil_config(self.key, self.points, self.n, self.x_seed, self.world)
+
+    def extra_config(self):
+        d = {}
+        if self.graphs:
+            d["launch"] = self.graph_note
+        d["l2"] = ("inputs >> L2 (126 MB), no flush needed" if len(self.rot) == 1 else
+                   f"inputs < L2: steps rotate over {len(self.rot)} device copies of the whole "
+                   f"input ({len(self.rot) * self.work_local() / 1e6:.0f} MB > 3 x L2), no flush")
+        return d
 
     def work_global(self) -> float:
         # nnz*(s_v+s_i) + (N+1)*s_p + Ncols*s_v + N*s_v, int32 colind layout
@@ -364,21 +594,19 @@ class StencilSpmv(Workload):
 
         return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
 
-    def cpu_reference(self, rows_sample, threads, reps):
-        """Reference emitted spmv on rows [a, b) of the same matrix."""
-        from oracle import ref as R
-        mid = self.N // 2
-        a, b = max(0, mid - rows_sample // 2), min(self.N, mid + rows_sample // 2)
-        rp, ci, v = self.lb.synth_stencil(self.points, self.n, a, b)
-        rp, ci, v = rp.cpu().numpy(), ci.cpu().numpy().astype(np.int64), v.cpu().numpy()
-        nnz = int(rp[-1])
-        yref, times = R.spmv_csr(rp, ci, v, self.x_host, reps=reps, threads=threads)
-        work = nnz * 12 + (b - a + 1) * 8 + (b - a) * 8 * 2
-        desc = (f"rows [{a}, {b}) of the same matrix ({nnz} nnz): reference emitted Kokkos C++ "
-                f"(tests/fixtures/spmv.mlir, index colind) on its serial stub, {threads} row "
-                f"blocks on std::threads")
-        got = self.last_y[a - self.r0:b - self.r0].cpu().numpy()
-        return yref, got, times, work, desc, 1e-12
+    def gpu_region(self, region):
+        a, b = region
+        if a < self.r0 or b > self.r1:
+            return None
+        return self.last_y[a - self.r0:b - self.r0].cpu().numpy()
+
+
+def stencil_config(key, points, n, seed, world):
+    return {"workload": WORKLOAD_NAMES[key].format(n=n),
+            "rows": n ** 3 if points == 27 else n * n, "nnz": S.stencil_nnz(points, n),
+            "index_layout": "rowptr int64, colind int32", "x": f"U(-1,1) numpy seed {seed}",
+            "sharding": f"row blocks x{world}, halo exchange of x (NCCL P2P)",
+            "parallelism": f"rowblock{world}"}
 
 
 class MtxSpmv(Workload):
@@ -387,7 +615,7 @@ class MtxSpmv(Workload):
     planned once, x U(-1,1) seed 7.  N > 1: independent replicas."""
 
     scaling = "weak"
-
+    key = "mtx"
     data = "matrix market file (--mtx), x seeded"
 
     def __init__(self, args, rank, world):
@@ -410,11 +638,14 @@ class MtxSpmv(Workload):
 
     @property
     def name(self):
-        return f"matrix market SpMV fp64: {Path(self.path).name}"
+        return WORKLOAD_NAMES["mtx"].format(mtx=Path(self.path).name)
 
     def config(self):
-        return {"workload": self.name, "rows": self.N, "cols": self.ncols, "nnz": self.nnz,
-                "index_layout": "rowptr int64, colind int32", "parallelism": "replica",
+        return {"workload": self.name, "parallelism": "replica"}
+
+    def extra_config(self):
+        return {"rows": self.N, "cols": self.ncols, "nnz": self.nnz,
+                "index_layout": "rowptr int64, colind int32",
                 "l2": "L2 flushed between steps" if self.flush is not None else "inputs > L2"}
 
     def work_local(self):
@@ -442,22 +673,15 @@ class MtxSpmv(Workload):
 
         return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
 
-    def cpu_reference(self, rows_sample, threads, reps):
-        from oracle import ref as R
-        rp = self.rowptr.cpu().numpy()
-        b = min(self.N, rows_sample)
-        e0, e1 = int(rp[0]), int(rp[b])
-        ci = self.colind[e0:e1].cpu().numpy().astype(np.int64)
-        v = self.values[e0:e1].cpu().numpy()
-        yref, times = R.spmv_csr(rp[:b + 1] - e0, ci, v, self.x_host, reps=reps, threads=threads)
-        work = (e1 - e0) * 12 + (b + 1) * 8 + b * 8 * 2
-        desc = (f"rows [0, {b}) ({e1 - e0} nnz): reference emitted Kokkos C++ on its serial "
-                f"stub, {threads} row blocks")
-        return yref, self.y[:b].cpu().numpy(), times, work, desc, 1e-12
+    def gpu_region(self, region):
+        a, b = region
+        return self.y[a:b].cpu().numpy()
 
 
 class PowerLawSpmm(Workload):
-    """Config 3: CSR x dense SpMM fp64, K = 64, Chung-Lu power-law matrix.
+    """Config 3: CSR x dense SpMM fp64, K = 64, Chung-Lu power-law matrix
+    (synth_inputs.PowerLawSpec: n = 10M, seed 1 -> nnz 99,891,191, longest row
+    117,683; structure built on the device, values and X from numpy).
 
     N > 1: the SAME global matrix, row-block sharded
     (sharded.RowBlockSpmm: rank r owns rows [r*c, r*c + c), c = ceil(N / world),
@@ -466,7 +690,7 @@ class PowerLawSpmm(Workload):
     "x_replicated" variant times the local SpMM alone (features resident on
     every GPU, the GCN case)."""
 
-    name = "config3: CSR x dense SpMM fp64, K=64, power-law (Chung-Lu, Pareto 2.5) 10M rows"
+    key = "c3"
     scaling = "strong"
     variant_key = "variants"
 
@@ -476,15 +700,17 @@ class PowerLawSpmm(Workload):
         self.lb, self.args, self.world, self.rank = lb, args, world, rank
         self.N, self.k, self.seed = n, k, seed
         self.stream = torch.cuda.current_stream()
-        rowptr, colind, values = powerlaw_csr_device(n, mean, 2.5, seed)
+        spec = powerlaw_spec(n, seed, mean)
+        rowptr, colind = S.powerlaw_structure_device(spec)
         self.nnz_global_ = int(rowptr[-1].item())
-        g = torch.Generator(device="cuda").manual_seed(seed + 100)
-        X = torch.rand((n, k), generator=g, dtype=torch.float64, device="cuda") * 2 - 1
-        lens = (rowptr[1:] - rowptr[:-1])
+        values = torch.from_numpy(S.powerlaw_values(spec, self.nnz_global_)).cuda()
+        lens = rowptr[1:] - rowptr[:-1]
         self.max_len = int(lens.max().item())
         self.median_len = float(lens.double().median().item())
+        del lens
+        X_host = memo(("X", n, k, seed), lambda: S.spmm_dense(n, k, seed))
         self.r0, self.r1 = sharded.equal_row_ranges(n, world)[rank]
-        self.full = ((rowptr, colind, values, X.clone())
+        self.full = ((rowptr, colind, values, torch.from_numpy(X_host).cuda())
                      if world > 1 and n * k * 8 < (2 << 30) else None)
         if world > 1:
             a, b = int(rowptr[self.r0].item()), int(rowptr[self.r1].item())
@@ -495,23 +721,21 @@ class PowerLawSpmm(Workload):
             self.rowptr, self.colind, self.values = rowptr, colind, values
         self.nnz = int(self.rowptr[-1].item())
         self.op = sharded.RowBlockSpmm(self.rowptr, self.colind, self.values, n, k, rank, world)
-        self.op.x_local.copy_(X[self.r0:self.r1])
-        del X
+        self.op.x_local.copy_(torch.from_numpy(X_host[self.r0:self.r1]))
         self.op.gather()
         self.X = self.op.X_full[:n]
         self.Y = torch.empty((self.r1 - self.r0, k), dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
     def config(self):
-        return {"workload": self.name, "rows": self.N, "nnz": self.nnz_global_, "k": self.k,
-                "max_row": self.max_len, "median_row": self.median_len,
-                "index_layout": "rowptr int64, colind int32",
-                "generator": f"torch CUDA generator seed {self.seed} (device)",
+        return powerlaw_config("c3", self.N, self.k, self.seed, self.world)
+
+    def extra_config(self):
+        return {"nnz": self.nnz_global_, "max_row": self.max_len, "median_row": self.median_len,
                 "l2": "inputs >> L2",
-                "sharding": (f"row blocks x{self.world}, NCCL all-gather of X "
-                             f"({self.op.gather_bytes / 1e9:.2f} GB received per rank per step) "
-                             "then the local SpMM" if self.world > 1 else "none"),
-                "parallelism": f"rowblock{self.world}"}
+                **({"gather": f"NCCL all-gather of X ({self.op.gather_bytes / 1e9:.2f} GB "
+                              "received per rank per step) then the local SpMM"}
+                   if self.world > 1 else {})}
 
     def _work(self, nnz, rows):
         # nnz*(s_v+s_i) + (N+1)*s_p + Ncols*K*s_v + N*K*s_v
@@ -525,7 +749,7 @@ class PowerLawSpmm(Workload):
         return self._work(self.nnz, self.r1 - self.r0)
 
     def launches_per_step(self):
-        return 4 if self.max_len > 2048 else 1
+        return 4 if self.max_len > 2048 else 2
 
     def kernel_name(self):
         return ("spmm_batch_kernel<double> (32 rows per warp) + long rows: "
@@ -576,62 +800,68 @@ class PowerLawSpmm(Workload):
 
         return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
 
-    def cpu_reference(self, rows_sample, threads, reps):
-        from oracle import ref as R
-        a, b = 0, min(self.N, max(1, rows_sample // 40))
-        rp = self.rowptr[a:b + 1].cpu().numpy()
-        ci = self.colind[rp[0]:rp[-1]].cpu().numpy()
-        v = self.values[rp[0]:rp[-1]].cpu().numpy()
-        rp = rp - rp[0]
-        X = self.X.cpu().numpy()
-        threads = min(threads, 2)   # each thread block replicates X (5 GB) on the stub
-        self.cpu_threads_used = threads
-        Yref, times = R.spmm_csr(rp, ci, v, X, reps=reps, threads=threads)
-        nnz = int(rp[-1])
-        work = nnz * 12 + (b - a + 1) * 8 + (b - a) * self.k * 8 * 2
-        desc = (f"rows [{a}, {b}) ({nnz} nnz) of the same matrix: reference emitted Kokkos C++ "
-                f"of oracle/ir/spmm.mlir on its serial stub, {threads} row blocks")
-        got = self.Y[a:b].cpu().numpy()
-        return Yref, got, times, work, desc, 1e-12
+    def gpu_region(self, region):
+        a, b = region
+        if a < self.r0 or b > self.r1:
+            return None
+        return self.Y[a - self.r0:b - self.r0].cpu().numpy()
+
+
+def powerlaw_config(key, n, k, seed, world, extra=None):
+    d = {"workload": WORKLOAD_NAMES[key].format(n=n), "rows": n, "k": k,
+         "index_layout": "rowptr int64, colind int32",
+         "generator": f"synth_inputs.PowerLawSpec(n={n}, mean=10, seed={seed}) (numpy draws)",
+         "sharding": (f"row blocks x{world}, NCCL all-gather of the dense operand" if world > 1
+                      else "none"),
+         "parallelism": f"rowblock{world}"}
+    d.update(extra or {})
+    return d
 
 
 class DenseMatmul(Workload):
-    """Config 2: dense linalg.matmul 4096^3 (f32: 3xTF32 / exact; f64: DMMA / exact)."""
+    """Config 2: dense linalg.matmul 4096^3 (f32: 3xTF32; f64: certified
+    Ozaki on the int8 tensor cores).  N > 1: row blocks of A
+    and C (sharded.RowBlockGemm), B replicated by one broadcast when the
+    operator is built (not part of a step); strong scaling."""
 
     unit = "TFLOP/s"
     bound = "tensor"
-    scaling = "weak"
+    scaling = "strong"
 
     def __init__(self, args, rank, world, dt=torch.float32, n=4096):
         import paper_2509_25605_b200 as lb
+        from paper_2509_25605_b200 import sharded
         self.lb, self.args, self.world, self.n, self.dt = lb, args, world, n, dt
         self.dtype = "f32" if dt == torch.float32 else "f64"
+        self.key = "c2" + self.dtype
         self.stream = torch.cuda.current_stream()
-        g = torch.Generator(device="cuda").manual_seed(3 if dt == torch.float32 else 2)
-        lo = 0.0 if dt == torch.float32 else -1.0   # SURVEY 8(d): f32 U(0,1), f64 U(-1,1)
-        self.A = (torch.rand((n, n), generator=g, dtype=dt, device="cuda") * (1 - lo) + lo)
-        self.B = (torch.rand((n, n), generator=g, dtype=dt, device="cuda") * (1 - lo) + lo)
-        self.C = torch.empty((n, n), dtype=dt, device="cuda")
+        npdt = np.float32 if dt == torch.float32 else np.float64
+        seed = 3 if dt == torch.float32 else 2
+        A, B = memo(("dense", n, np.dtype(npdt).name, seed),
+                    lambda: S.dense_operands(n, npdt, seed))
+        self.r0, self.r1 = sharded.equal_row_ranges(n, world)[rank]
+        self.A = torch.from_numpy(A[self.r0:self.r1]).cuda()
+        Bd = (torch.from_numpy(B).cuda() if rank == 0 else
+              torch.empty((n, n), dtype=dt, device="cuda"))
+        self.op = sharded.RowBlockGemm(self.A, Bd, n, rank, world)
+        self.B = self.op.B
+        self.C = torch.empty((self.r1 - self.r0, n), dtype=dt, device="cuda")
         self.mode = args.gemm_mode
         if 3 * n * n * (4 if dt == torch.float32 else 8) < (256 << 20):
             self.flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
         torch.cuda.synchronize()
 
-    @property
-    def name(self):
-        return f"config2: dense linalg.matmul {self.n}^3 {self.dtype} (mode {self.mode})"
-
     def config(self):
-        return {"workload": self.name, "m": self.n, "n": self.n, "k": self.n,
-                "inputs": "U(0,1)" if self.dt == torch.float32 else "U(-1,1)",
-                "l2": "L2 flushed between steps" if self.flush is not None else "working set > L2",
-                "parallelism": "replica"}
+        return matmul_config(self.key, self.n, self.mode, self.world)
+
+    def extra_config(self):
+        return {"l2": "L2 flushed between steps" if self.flush is not None else "working set > L2"}
 
     def work_global(self):
-        return 2.0 * self.n ** 3 * self.world
+        return 2.0 * self.n ** 3
 
     def work_local(self):
-        return 2.0 * self.n ** 3
+        return 2.0 * (self.r1 - self.r0) * self.n * self.n
 
     def effective_mode(self):
         if self.mode != "auto":
@@ -655,9 +885,9 @@ class DenseMatmul(Workload):
         peak (2x the measured dense bf16 rate), counted in int8 ops."""
         if self.effective_mode() != "ozaki":
             return None
-        S = (8 if self.n * 9.0 * 2.0 ** -56 <= 0.75e-12 else 9) if self.dt == torch.float64 else 3
-        products = S * (S + 1) // 2
-        ops = products * 2.0 * self.n ** 3
+        S_ = (8 if self.n * 9.0 * 2.0 ** -56 <= 0.75e-12 else 9) if self.dt == torch.float64 else 3
+        products = S_ * (S_ + 1) // 2
+        ops = products * self.work_local()
         pk = peaks()
         peak = 2.0 * pk["bf16_tflops"]
         achieved = ops / kern_avg / 1e12
@@ -667,9 +897,19 @@ class DenseMatmul(Workload):
                 "int8_products": products, "ops_per_launch": ops}
 
     def step(self):
-        self.lb.gemm(self.A, self.B, self.C, mode=self.mode)
+        self.op.multiply(self.C, mode=self.mode, stream=self.stream)
+
+    def sharded_parity(self):
+        if self.world == 1:
+            return None
+        A, _ = _MEMO[("dense", self.n, "float32" if self.dt == torch.float32 else "float64",
+                      3 if self.dt == torch.float32 else 2)]
+        ref = self.lb.gemm(torch.from_numpy(A).cuda(), self.B, mode=self.mode)
+        return bool(torch.equal(ref[self.r0:self.r1], self.C))
 
     def e2e(self, steps, warmup):
+        """This rank's rows of A and the (replicated) B host-modified every
+        step, C's row block read back."""
         from paper_2509_25605_b200.dualview import DualView
         a = DualView.from_host(self.A.cpu(), "A", device_buffer=self.A)
         b = DualView.from_host(self.B.cpu(), "B", device_buffer=self.B)
@@ -680,167 +920,158 @@ class DenseMatmul(Workload):
             b.modify_host()
             a.sync_device(self.stream)
             b.sync_device(self.stream)
-            self.lb.gemm(a.device_view(), b.device_view(), c.device_view(), mode=self.mode)
+            self.lb.gemm(a.device_view(), b.device_view(), c.device_view(), mode=self.mode,
+                         stream=self.stream)
             c.modify_device()
             c.sync_host(self.stream)
 
         return timed_e2e(one, steps, warmup, self.world), a.nbytes + b.nbytes, c.nbytes
 
-    def cpu_reference(self, rows_sample, threads, reps):
-        from oracle import ref as R
-        rows = max(threads, min(self.n, rows_sample // 250_000))
-        A = self.A[:rows].cpu().numpy()
-        B = self.B.cpu().numpy()
-        Cref, times = R.matmul(A, B, reps=reps, threads=threads)
-        desc = (f"rows [0, {rows}) of C: reference emitted Kokkos C++ of oracle/ir/matmul_"
-                f"{self.dtype}.mlir (TeamPolicy nest) on its serial stub, {threads} row blocks")
-        got = self.C[:rows].cpu().numpy()
-        tol = 1e-5 if self.dt == torch.float32 else 1e-12
-        return Cref, got, times, 2.0 * rows * self.n * self.n, desc, tol
+    def gpu_region(self, region):
+        a, b = region
+        if a < self.r0 or b > self.r1:
+            return None
+        return self.C[a - self.r0:b - self.r0].cpu().numpy()
+
+
+def matmul_config(key, n, mode, world):
+    f32 = key.endswith("f32")
+    return {"workload": WORKLOAD_NAMES[key].format(n=n, mode=mode), "m": n, "n": n, "k": n,
+            "inputs": "U(0,1) numpy seed 3" if f32 else "U(-1,1) numpy seed 2",
+            "sharding": (f"row blocks of A and C x{world}; B replicated by one NCCL broadcast "
+                         "when the operator is built (outside the timed steps)" if world > 1
+                         else "none"),
+            "parallelism": f"rowblock{world}"}
 
 
 class GcnLayer(Workload):
     """Config 4: GCN layer H = relu((A_hat X) W), fp32, A_hat = D^-1/2 A D^-1/2 of the
-    config-3 power-law generator at 1M rows, X [N, 64] U(0,1), W [64, 64]
-    U(-1/8, 1/8) (torch Linear default bound for fan-in 64), seed 4."""
+    config-3 power-law generator at 1M rows (seed 4), X [N, 64] U(0,1), W [64, 64]
+    U(-1/8, 1/8) (torch Linear default bound for fan-in 64).  N > 1: row blocks of
+    A_hat and H, one all-gather of X per step, W broadcast once
+    (sharded.RowBlockGcn)."""
 
-    name = "config4: GCN layer relu((A_hat X) W) fp32, power-law A_hat 1M rows, 64->64"
+    key = "c4"
     dtype = "f32"
-    scaling = "weak"
+    scaling = "strong"
 
     def __init__(self, args, rank, world, n=1_000_000, f=64, seed=4):
         import paper_2509_25605_b200 as lb
-        self.lb, self.args, self.world, self.N, self.f = lb, args, world, n, f
+        from paper_2509_25605_b200 import sharded
+        self.lb, self.args, self.world, self.N, self.f, self.seed = lb, args, world, n, f, seed
         self.stream = torch.cuda.current_stream()
-        rowptr, colind, _ = powerlaw_csr_device(n, 10.0, 2.5, seed)
-        deg = (rowptr[1:] - rowptr[:-1]).clamp(min=1).to(torch.float64)
-        rows = torch.repeat_interleave(torch.arange(n, device="cuda"), rowptr[1:] - rowptr[:-1])
-        vals = (deg[rows] * deg[colind.long()]).rsqrt().to(torch.float32)
-        self.rowptr, self.colind, self.values = rowptr, colind, vals.contiguous()
-        self.nnz = int(rowptr[-1].item())
-        g = torch.Generator(device="cuda").manual_seed(seed)
-        self.X = torch.rand((n, f), generator=g, dtype=torch.float32, device="cuda")
-        self.W = (torch.rand((f, f), generator=g, dtype=torch.float32, device="cuda") * 2 - 1) / 8
-        self.H = torch.empty((n, f), dtype=torch.float32, device="cuda")
-        self.max_len = int((rowptr[1:] - rowptr[:-1]).max().item())
+        spec = powerlaw_spec(n, seed)
+        rowptr, colind = S.powerlaw_structure_device(spec)
+        rp_h, ci_h = rowptr.cpu().numpy(), colind.cpu().numpy()
+        X, W = S.gcn_features(n, f, seed)
+        vals_h = S.gcn_values_host(rp_h, ci_h)
+        _MEMO[("gcn", n, f, seed)] = (rp_h, ci_h, vals_h, X, W)
+        values = torch.from_numpy(vals_h).cuda()
+        self.nnz_global_ = int(rp_h[-1])
+        self.max_len = int(np.diff(rp_h).max())
+        self.r0, self.r1 = sharded.equal_row_ranges(n, world)[rank]
+        if world > 1:
+            a, b = int(rp_h[self.r0]), int(rp_h[self.r1])
+            self.rowptr = (rowptr[self.r0:self.r1 + 1] - a).contiguous()
+            self.colind, self.values = colind[a:b].contiguous(), values[a:b].contiguous()
+            del rowptr, colind, values
+        else:
+            self.rowptr, self.colind, self.values = rowptr, colind, values
+        self.nnz = int(self.rowptr[-1].item())
+        Wd = torch.from_numpy(W).cuda() if rank == 0 else torch.empty((f, f), device="cuda")
+        self.op = sharded.RowBlockGcn(self.rowptr, self.colind, self.values, Wd, n, rank, world)
+        self.op.x_local.copy_(torch.from_numpy(X[self.r0:self.r1]))
+        self.op.gather()
+        self.X = self.op.spmm.X_full[:n]
+        self.W = self.op.W
+        self.H = torch.empty((self.r1 - self.r0, f), dtype=torch.float32, device="cuda")
         torch.cuda.synchronize()
 
     def config(self):
-        return {"workload": self.name, "rows": self.N, "nnz": self.nnz, "features": self.f,
-                "max_row": self.max_len, "parallelism": "replica",
-                "bytes": "compulsory: A_hat + X + W + H (no A_hat X intermediate)",
-                "l2": "inputs > L2 (X 256 MB)"}
+        return powerlaw_config("c4", self.N, self.f, self.seed, self.world,
+                               {"features": self.f,
+                                "bytes": "compulsory: A_hat + X + W + H (no A_hat X intermediate)"})
+
+    def extra_config(self):
+        return {"nnz": self.nnz_global_, "max_row": self.max_len, "l2": "inputs > L2 (X 256 MB)"}
 
     def work_local(self):
         # compulsory bytes of the layer: A_hat (int32 colind + f32 values, int64
         # rowptr), X, W read once, H written once.  The A_hat X intermediate is
-        # not counted (the fused kernel never materialises it)
-        f, n = self.f, self.N
-        return self.nnz * 8 + (n + 1) * 8 + n * f * 4 + f * f * 4 + n * f * 4
+        # not counted
+        f, rows = self.f, self.r1 - self.r0
+        return self.nnz * 8 + (rows + 1) * 8 + self.N * f * 4 + f * f * 4 + rows * f * 4
 
     def work_global(self):
-        return self.work_local() * self.world
+        f, n = self.f, self.N
+        return self.nnz_global_ * 8 + (n + 1) * 8 + n * f * 4 + f * f * 4 + n * f * 4
 
     def launches_per_step(self):
-        return 4 if self.max_len > 2048 else 2
+        return 4 if self.max_len > 2048 else 3
 
     def kernel_name(self):
         return ("spmm_batch_kernel<float> + spmm_seq_long_pipe_kernel (exact-order hub rows, "
-                "16-column groups) + gemm_exact_narrow_kernel<relu> (reference order)")
+                "16-column groups) + dense stage 2 with the ReLU fused")
 
     def step(self):
-        self.lb.gcn_layer(self.rowptr, self.colind, self.values, self.X, self.W, self.H,
-                          nnz=self.nnz)
+        self.op.multiply(self.H, stream=self.stream)
+
+    def sharded_parity(self):
+        if self.world == 1:
+            return None
+        rp, ci, v, X, W = _MEMO[("gcn", self.N, self.f, self.seed)]
+        H = self.lb.gcn_layer(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(),
+                              torch.from_numpy(v).cuda(), self.X, self.W)
+        return bool(torch.equal(H[self.r0:self.r1], self.H))
 
     def e2e(self, steps, warmup):
-        """X (node features) host-modified every step, H read back."""
+        """This rank's rows of X (node features) host-modified every step (then
+        the all-gather when N > 1), H's row block read back."""
         from paper_2509_25605_b200.dualview import DualView
-        xs = DualView.from_host(self.X.cpu(), "X", device_buffer=self.X)
+        xs = DualView.from_host(self.op.x_local.cpu(), "X", device_buffer=self.op.x_local)
         hs = DualView.allocate(tuple(self.H.shape), torch.float32, "H")
 
         def one():
             xs.modify_host()
             xs.sync_device(self.stream)
-            self.lb.gcn_layer(self.rowptr, self.colind, self.values, xs.device_view(), self.W,
-                              hs.device_view(), nnz=self.nnz)
+            self.op.multiply(hs.device_view(), stream=self.stream)
             hs.modify_device()
             hs.sync_host(self.stream)
 
         return timed_e2e(one, steps, warmup, self.world), xs.nbytes, hs.nbytes
 
-    def cpu_reference(self, rows_sample, threads, reps):
-        from oracle import ref as R
-        a, b = 0, min(self.N, max(1, rows_sample // 80))
-        rp = self.rowptr[a:b + 1].cpu().numpy()
-        ci = self.colind[rp[0]:rp[-1]].cpu().numpy()
-        v = self.values[rp[0]:rp[-1]].cpu().numpy()
-        rp = rp - rp[0]
-        threads = min(threads, 4)   # each block replicates X (256 MB) on the stub
-        self.cpu_threads_used = threads
-        Href, times = R.gcn(rp, ci, v, self.X.cpu().numpy(), self.W.cpu().numpy(), reps=reps,
-                            threads=threads)
-        nnz = int(rp[-1])
-        f = self.f
-        work = nnz * 8 + (b - a + 1) * 8 + (b - a) * f * 4 * 3 + f * f * 4
-        desc = (f"rows [{a}, {b}) ({nnz} nnz): reference emitted Kokkos C++ of "
-                f"oracle/ir/gcn_f32.mlir on its serial stub, {threads} row blocks")
-        return Href, self.H[a:b].cpu().numpy(), times, work, desc, 1e-5
-
-
-def powerlaw_csr_device(n, mean, alpha, seed):
-    """Chung-Lu power-law CSR built on the device: Pareto(alpha) row
-    weights, rows and columns drawn in proportion to the weights, hubs scattered
-    by a permutation, sorted and deduplicated; int64 rowptr, int32 colind,
-    values U(-1, 1)."""
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    dev = "cuda"
-    w = (1.0 - torch.rand(n, generator=g, dtype=torch.float64, device=dev)) ** (-1.0 / (alpha - 1.0))
-    cdf = torch.cumsum(w, 0)
-    total = int(mean * n)
-    perm = torch.randperm(n, generator=g, device=dev)
-    keys = []
-    chunk = 25_000_000
-    for c0 in range(0, total, chunk):
-        m = min(chunk, total - c0)
-        r = torch.searchsorted(cdf, torch.rand(m, generator=g, dtype=torch.float64, device=dev) * cdf[-1])
-        c = torch.searchsorted(cdf, torch.rand(m, generator=g, dtype=torch.float64, device=dev) * cdf[-1])
-        r = perm[r.clamp_(max=n - 1)]
-        c = perm[c.clamp_(max=n - 1)]
-        keys.append(r.to(torch.int64) * n + c.to(torch.int64))
-        del r, c
-    key = torch.unique(torch.cat(keys))
-    del keys
-    rows = torch.div(key, n, rounding_mode="floor")
-    cols = (key - rows * n).to(torch.int32)
-    counts = torch.bincount(rows, minlength=n)
-    rowptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    rowptr[1:] = torch.cumsum(counts, 0)
-    values = torch.rand(key.numel(), generator=g, dtype=torch.float64, device=dev) * 2 - 1
-    return rowptr, cols.contiguous(), values
+    def gpu_region(self, region):
+        a, b = region
+        if a < self.r0 or b > self.r1:
+            return None
+        return self.H[a - self.r0:b - self.r0].cpu().numpy()
 
 
 class DenseMatvec(Workload):
     """linalg.matvec / LAPIS::gemv (SURVEY a10, fixture tests/fixtures/matvec_f64.mlir
-    scaled up): y = A x, A 16384 x 16384 f64 U(-1,1) seed 6 (2.1 GB > L2, no
+    scaled up): y = A x, A 16384 x 16384 f64 U(-1,1) numpy seed 6 (2.1 GB > L2, no
     flush needed), folded in the reference order (bit-identical).  N > 1:
     independent replicas."""
 
-    name = "matvec: linalg.matvec f64 16384 x 16384 (row_fold_pipe_kernel, reference order)"
+    key = "gemv"
     scaling = "weak"
 
     def __init__(self, args, rank, world, n=16384):
         import paper_2509_25605_b200 as lb
         self.lb, self.args, self.world, self.n = lb, args, world, n
         self.stream = torch.cuda.current_stream()
-        g = torch.Generator(device="cuda").manual_seed(6)
-        self.A = torch.rand((n, n), generator=g, dtype=torch.float64, device="cuda") * 2 - 1
-        self.x = torch.rand(n, generator=g, dtype=torch.float64, device="cuda") * 2 - 1
+        A, x = gemv_host(n)
+        self.A = torch.from_numpy(A).cuda()
+        self.x = torch.from_numpy(x).cuda()
         self.y = torch.empty(n, dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
     def config(self):
-        return {"workload": self.name, "rows": self.n, "cols": self.n, "l2": "A 2.1 GB >> L2",
-                "parallelism": "replica"}
+        return {"workload": WORKLOAD_NAMES["gemv"].format(n=self.n), "rows": self.n,
+                "cols": self.n, "parallelism": "replica"}
+
+    def extra_config(self):
+        return {"l2": "A 2.1 GB >> L2"}
 
     def work_local(self):
         return (self.n * self.n + 2 * self.n) * 8
@@ -849,7 +1080,7 @@ class DenseMatvec(Workload):
         return self.work_local() * self.world
 
     def kernel_name(self):
-        return "row_fold_pipe_kernel<double, DOT, 16-byte> (32 rows per CTA, 6-stage cp.async ring)"
+        return "row_fold_pipe_kernel<double, DOT, 16-byte> (32 rows per CTA, 3-stage cp.async ring)"
 
     def step(self):
         self.lb.gemv(self.A, self.x, self.y, stream=self.stream)
@@ -869,155 +1100,211 @@ class DenseMatvec(Workload):
 
         return timed_e2e(one, steps, warmup, self.world), xs.nbytes, ys.nbytes
 
-    def cpu_reference(self, rows_sample, threads, reps):
-        from oracle import ref as R
-        rows = min(self.n, max(1, rows_sample // 4000))   # 1000 rows = 131 MB
-        self.cpu_threads_used = 1
-        A = self.A[:rows].cpu().numpy()
-        yref, times = R.matvec(A, self.x.cpu().numpy(), reps=reps)
-        work = (rows * self.n + self.n + rows) * 8
-        desc = (f"rows [0, {rows}) of the same A: reference emitted Kokkos C++ of "
-                "oracle/ir/matvec_f64.mlir on its serial stub, 1 thread")
-        return yref, self.y[:rows].cpu().numpy(), times, work, desc, 1e-12
+    def gpu_region(self, region):
+        a, b = region
+        return self.y[a:b].cpu().numpy()
 
 
 WORKLOADS = {
-    "c5": lambda args, r, w: StencilSpmv(args, r, w, 27, args.n or 585, x_seed=5),
-    "c1": lambda args, r, w: StencilSpmv(args, r, w, 5, args.n or 1000, x_seed=1),
-    "c3": lambda args, r, w: PowerLawSpmm(args, r, w, args.n or 10_000_000),
-    "c2f32": lambda args, r, w: DenseMatmul(args, r, w, torch.float32, args.n or 4096),
-    "c2f64": lambda args, r, w: DenseMatmul(args, r, w, torch.float64, args.n or 4096),
-    "c4": lambda args, r, w: GcnLayer(args, r, w, args.n or 1_000_000),
-    "mtx": lambda args, r, w: MtxSpmv(args, r, w),
-    "gemv": lambda args, r, w: DenseMatvec(args, r, w, args.n or 16384),
+    "c5": lambda args, r, w, n: StencilSpmv(args, r, w, 27, n, x_seed=5),
+    "c1": lambda args, r, w, n: StencilSpmv(args, r, w, 5, n, x_seed=1),
+    "c3": lambda args, r, w, n: PowerLawSpmm(args, r, w, n),
+    "c2f32": lambda args, r, w, n: DenseMatmul(args, r, w, torch.float32, n),
+    "c2f64": lambda args, r, w, n: DenseMatmul(args, r, w, torch.float64, n),
+    "c4": lambda args, r, w, n: GcnLayer(args, r, w, n),
+    "mtx": lambda args, r, w, n: MtxSpmv(args, r, w),
+    "gemv": lambda args, r, w, n: DenseMatvec(args, r, w, n),
 }
+UNITS = {"c2f32": "TFLOP/s", "c2f64": "TFLOP/s"}
+DTYPES = {"c2f32": "f32", "c4": "f32"}
+SCALING = {"gemv": "weak", "mtx": "weak"}
 
 
-def cpu_baseline(wl, args, threads):
-    """The reference's emitted C++ on its serial stub (oracle/_ref) on a bounded
-    sample of the workload; also the parity check of that sample."""
-    from oracle import ref as R
-    if not R.available():
-        return {"unavailable": "oracle/_ref not built"}, None
-    want, got, times, work, desc, tol = wl.cpu_reference(args.cpu_rows, threads, args.cpu_reps)
-    t = float(np.median(times))
-    # about 10 s of CPU work in total (bounded sample, repeated)
-    reps = int(min(2000, max(args.cpu_reps, np.ceil(args.cpu_seconds / max(t, 1e-6)))))
-    if reps > args.cpu_reps:
-        want, got, times, work, desc, tol = wl.cpu_reference(args.cpu_rows, threads, reps)
-        t = float(np.median(times))
-    scale = 1e9 if wl.unit == "GB/s" else 1e12
-    base = {"value": round(work / t / scale, 4), "unit": wl.unit,
-            "cores": getattr(wl, "cpu_threads_used", threads),
-            "kind": "reference", "sample": desc + f", median of {len(times)} reps",
-            "seconds_per_rep": t}
-    parity = {"sample_elements": int(np.asarray(want).size), **parity_report(got, want, tol)}
-    return base, parity
+def static_config(key, args, n, world):
+    """The config object of a workload without building it (the reference arm
+    reports the same config as the B200 arm)."""
+    if key in ("c5", "c1"):
+        return stencil_config(key, 27 if key == "c5" else 5, n, 5 if key == "c5" else 1, world)
+    if key == "c3":
+        return powerlaw_config("c3", n, 64, 1, world)
+    if key == "c4":
+        return powerlaw_config("c4", n, 64, 4, world,
+                               {"features": 64,
+                                "bytes": "compulsory: A_hat + X + W + H (no A_hat X intermediate)"})
+    if key in ("c2f32", "c2f64"):
+        return matmul_config(key, n, args.gemm_mode, world)
+    if key == "gemv":
+        return {"workload": WORKLOAD_NAMES["gemv"].format(n=n), "rows": n, "cols": n,
+                "parallelism": "replica"}
+    return {"workload": WORKLOAD_NAMES["mtx"].format(mtx=Path(args.mtx).name),
+            "parallelism": "replica"}
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU path (oracle/_ref: its emitted Kokkos C++ on its
+    serial stub) on the host cores, over a bounded sample of the same workload
+    built on the host from synth_inputs — no part of the B200 backend is
+    imported or loaded.  `value` uses every host core (row blocks, bitwise
+    identical to one thread); `one_core` is the stub as shipped (serial)."""
     if rank != 0:
         return
     from oracle import ref as R
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
+    key = args.workload
+    n = args.n or DEFAULT_N[key]
     threads = os.cpu_count() or 1
-    torch.cuda.set_device(0)
-    wl = WORKLOADS[args.workload](args, 0, 1)
-    wl.step()
-    torch.cuda.synchronize()
-    _, _, times, work, desc, _ = wl.cpu_reference(args.cpu_rows, threads,
-                                                  args.warmup + args.steps)
+    sample = host_sample(key, args, n, threads)
+    cores = min(threads, sample.max_threads or threads)
+    unit = UNITS.get(key, "GB/s")
+    scale = 1e9 if unit == "GB/s" else 1e12
+    _, times = sample.run(args.warmup + args.steps, cores)
     times = times[args.warmup:]
     t = float(np.mean(times))
-    scale = 1e9 if wl.unit == "GB/s" else 1e12
-    value = work / t / scale
-    out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": wl.unit,
+    value = sample.work / t / scale
+    one = None
+    if cores > 1:
+        reps1 = max(1, min(args.steps, int(np.ceil(20.0 / max(t * cores, 1e-6)))))
+        _, t1 = sample.run(reps1 + 1, 1)
+        one = float(np.mean(t1[1:])) if len(t1) > 1 else float(t1[0])
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": unit,
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": wl.scaling,
-           "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic", "config": wl.config(),
-           "cpu_baseline": {"value": round(value, 4), "unit": wl.unit, "cores": getattr(wl, "cpu_threads_used", threads),
-                            "kind": "reference", "sample": desc},
-           "e2e": {"value": round(value, 4), "unit": wl.unit, "h2d_bytes_per_step": 0,
+           "ms_per_step": round(t * 1e3, 4), "higher_is_better": True,
+           "scaling": SCALING.get(key, "strong"), "vs_baseline": None,
+           "dtype": DTYPES.get(key, "f64"), "data": "synthetic (numpy-seeded, host-generated)",
+           "config": static_config(key, args, n, world),
+           "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": cores,
+                            "kind": "reference", "sample": f"{sample.desc}, {cores} row blocks",
+                            "build": R.compile_flags(),
+                            **({"one_core": {"value": round(sample.work / one / scale, 4),
+                                             "unit": unit, "cores": 1,
+                                             "ms_per_step": round(one * 1e3, 4)}}
+                               if one else {})},
+           "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
 
-def launch_census(wl):
-    """Kernels one step launches, counted by the CUDA activity tracer (CUPTI via
-    torch.profiler) on an untimed step after the timed region: how many of
-    OUR kernels (namespace lapis_b200 / NVRTC-generated lapis_*) run per step
-    and each one's share of the step's device time.  None when the tracer is
-    unavailable."""
+def _short_name(name: str) -> str:
+    return name.split("(")[0].replace("void ", "").replace("lapis_b200::", "")
+
+
+def graph_census(wl):
+    """Kernels of one step, read from a CUDA graph capture of that step
+    (lapis_b200_graph_kernels walks the captured graph's kernel nodes): exact
+    launch counts per kernel, no tracer involved.  None when the step cannot
+    be captured."""
+    import ctypes as C
+    from paper_2509_25605_b200 import _capi
+    side = torch.cuda.Stream()
+    old_stream, old_graphs = wl.stream, getattr(wl, "graphs", None)
+    g = torch.cuda.CUDAGraph(keep_graph=True)
     try:
+        torch.cuda.synchronize()
+        side.wait_stream(torch.cuda.current_stream())
+        wl.stream = side
+        if old_graphs is not None:
+            wl.graphs = None
+        with torch.cuda.graph(g, stream=side):
+            wl.step()
+        buf = C.create_string_buffer(1 << 16)
+        n = C.c_int64()
+        rc = _capi.lib().lapis_b200_graph_kernels(C.c_void_p(g.raw_cuda_graph()), buf, len(buf),
+                                                 C.byref(n))
+        if rc != 0:
+            return None
+        names = [x for x in buf.value.decode().split("\n") if x]
+        try:
+            dem = subprocess.run(["c++filt"], input="\n".join(names), capture_output=True,
+                                 text=True, timeout=30).stdout.split("\n")
+            names = [d or m for d, m in zip(dem, names)]
+        except (OSError, subprocess.SubprocessError):
+            pass
+        per = {}
+        for nm in names:
+            k = _short_name(nm)
+            per[k] = per.get(k, 0) + 1
+        return per
+    except Exception:
+        return None
+    finally:
+        wl.stream = old_stream
+        if old_graphs is not None:
+            wl.graphs = old_graphs
+        try:
+            g.reset()
+        except Exception:
+            pass
+        torch.cuda.synchronize()
+
+
+def profiler_census(wl):
+    """Launch counts and each kernel's share of one untimed step's device time
+    from the CUDA activity tracer (CUPTI via torch.profiler); (None, None)
+    when unavailable."""
+    try:
+        import warnings
         from torch.profiler import ProfilerActivity, profile
         torch.cuda.synchronize()
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            wl.step()
-            torch.cuda.synchronize()
-        per = {}
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                wl.step()
+                torch.cuda.synchronize()
+        cnt, per = {}, {}
         for e in prof.events():
             if getattr(e, "device_type", None) is None or "cuda" not in str(e.device_type).lower():
                 continue
-            name = e.name
-            if "lapis" not in name:
+            if "lapis" not in e.name:
                 continue
-            short = name.split("(")[0].replace("void ", "").replace("lapis_b200::", "")
-            c, t = per.get(short, (0, 0.0))
-            per[short] = (c + 1, t + float(getattr(e, "device_time", 0.0) or
-                                          getattr(e, "cuda_time", 0.0) or 0.0))
-        if not per:
-            return None
-        total = sum(t for _, t in per.values()) or 1.0
-        return {k: {"launches_per_step": c, "share": round(t / total, 4)}
-                for k, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1])}
+            k = _short_name(e.name)
+            cnt[k] = cnt.get(k, 0) + 1
+            per[k] = per.get(k, 0.0) + float(getattr(e, "device_time", 0.0) or
+                                             getattr(e, "cuda_time", 0.0) or 0.0)
+        total = sum(per.values())
+        return (cnt or None), ({k: v / total for k, v in per.items()} if total > 0 else None)
     except Exception:
-        return None
+        return None, None
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", "--problem-size", dest="n", type=int, default=0,
-                    help="problem size override")
-    ap.add_argument("--cpu-rows", type=int, default=4_000_000)
-    ap.add_argument("--cpu-reps", type=int, default=3)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="target CPU time of the cpu_baseline sample (reps are added to reach it)")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--vl", type=int, default=0,
-                    help="SpMV: time the emitted-mapping vector kernel with this vector length")
-    ap.add_argument("--mtx", default="", help="Matrix Market file for --workload mtx")
-    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "tf32x3", "dmma", "exact", "ozaki"])
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    rank, world, local = dist_setup(args)
-    if args.impl == "reference":
-        run_reference_arm(args, rank, world)
-        if world > 1:
-            dist.destroy_process_group()
-        return
-    torch.cuda.set_device(local)
-    wl = WORKLOADS[args.workload](args, rank, world)
+def launch_census(wl):
+    """How many of OUR kernels (namespace lapis_b200 / NVRTC lapis_*) one step
+    launches — from a graph capture of the step when it can be captured, else
+    from the activity tracer — and, where the tracer saw them, each one's
+    share of the step's device time."""
+    counts = graph_census(wl)
+    pcounts, shares = profiler_census(wl)
+    src = "CUDA graph capture of one untimed step (kernel nodes) x steps"
+    if counts:
+        counts = {k: c for k, c in counts.items() if "lapis" in k}
+    if not counts:
+        counts, src = pcounts, "CUDA activity trace of one untimed step x steps"
+    if not counts:
+        return None, None
+    shares = shares or {}
+    return ({k: {"launches_per_step": c,
+                 "share": round(shares[k], 4) if k in shares else None}
+             for k, c in sorted(counts.items(), key=lambda kv: -shares.get(kv[0], 0.0))}, src)
+
+
+def measure(wl, args, rank, world, local, steps, warmup, cpu_seconds, with_cpu=True):
+    """Warm-up, K timed steps (CUDA events on the launching stream, max over
+    ranks), roofline of the dominant kernel, e2e, launch census, the CPU
+    baseline and the parity sample.  Returns the JSON object of one workload."""
     stream = wl.stream
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         wl.step()
     torch.cuda.synchronize()
     if hasattr(wl, "capture_graphs"):
         wl.capture_graphs()
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             wl.step()
         torch.cuda.synchronize()
     barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(args.steps)]
+                   for _ in range(steps)]
     per_step = []
     with ClockSampler(local) as clk:
         barrier(world)
@@ -1038,7 +1325,7 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
     # with an L2 flush between steps, the step time excludes the flush
-    total = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    total = ev0.elapsed_time(ev1) / 1e3 / steps
     kern = [a.elapsed_time(b) / 1e3 for a, b in per_step] if per_step else [total]
     t_local = total if wl.flush is None else float(np.mean(kern))
     t = max_over_ranks(t_local, world)
@@ -1049,7 +1336,6 @@ def main():
     if wl.bound == "hbm":
         peak, punit, psrc = pk["hbm_gbs"], "GB/s", pk["source"] + " hbm_gbs (copy)"
     else:
-        # tensor-bound: nominal B200 dense peaks (MEASURED_PEAKS has bf16 only)
         if wl.dtype == "f32":
             # dense TF32 runs at half the bf16 rate on B200; 3xTF32 issues 3
             peak = pk["bf16_tflops"] / 2.0 / 3.0
@@ -1060,12 +1346,12 @@ def main():
     achieved = wl.work_local() / kern_avg / scale
     override = wl.roofline_override(kern_avg) if hasattr(wl, "roofline_override") else None
     traffic = None
-    tfile = ROOT / "profiles" / f"traffic_{args.workload}.json"
+    tfile = ROOT / "profiles" / f"traffic_{wl.key}.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-    exact_variant = (wl.exact_variant(max(3, args.steps // 2))
+    exact_variant = (wl.exact_variant(max(3, steps // 2))
                      if hasattr(wl, "exact_variant") and not args.vl else None)
-    census = launch_census(wl)
+    census, census_src = launch_census(wl)
     wl.step()   # the parity sample below checks the headline kernel's output
     torch.cuda.synchronize()
     sharded_parity = None
@@ -1081,11 +1367,9 @@ def main():
     e2e_dt, hb, db = wl.e2e(args.e2e_steps, 2)
     e2e_dt = max_over_ranks(e2e_dt, world)
     out = {
-        "metric": METRIC, "value": round(value, 3), "unit": wl.unit, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
-        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype,
-        "data": getattr(wl, "data", "synthetic (device-generated inputs, seeded)"),
-        "config": wl.config(),
+        "value": round(value, 3), "unit": wl.unit, "ms_per_step": round(t * 1e3, 4),
+        "steps": steps, "warmup": warmup, "scaling": wl.scaling, "dtype": wl.dtype,
+        "config": wl.config(), "workload_detail": wl.extra_config(),
         "roofline": ({**override, "traffic": traffic, "kernel": wl.kernel_name(),
                       "algorithmic_work_per_launch": wl.work_local()} if override else
                      {"bound": wl.bound, "achieved": round(achieved, 2), "peak": peak,
@@ -1098,20 +1382,95 @@ def main():
                 "path": getattr(wl, "e2e_path", "DualView lazy sync (inputs host-modified each "
                                 "step) + C-ABI kernels + result read on the host"),
                 **({"matches_device_result": wl.e2e_parity} if hasattr(wl, "e2e_parity") else {})},
-        "gpu_launches": args.steps * (sum(v["launches_per_step"] for v in census.values())
-                                      if census else wl.launches_per_step()),
-        "gpu_launches_source": ("CUDA activity trace of one untimed step x steps" if census
-                                else "static count per step x steps"),
+        "gpu_launches": steps * (sum(v["launches_per_step"] for v in census.values())
+                                 if census else wl.launches_per_step()),
+        "gpu_launches_source": census_src or "static count per step x steps",
         **({"kernels": census} if census else {}),
         **({getattr(wl, "variant_key", "exact_mode"): exact_variant} if exact_variant else {}),
         "clocks": clk.summary(),
         **({"sharded_parity": sharded_parity} if sharded_parity else {}),
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        base, parity = cpu_baseline(wl, args, os.cpu_count() or 1)
-        out["cpu_baseline"] = base
-        if parity is not None:
-            out["parity"] = parity
+    if rank == 0 and world == 1 and with_cpu and not args.no_cpu:
+        from oracle import ref as R
+        if not R.available():
+            out["cpu_baseline"] = {"unavailable": "oracle/_ref not built"}
+        else:
+            threads = os.cpu_count() or 1
+            sample = host_sample(wl.key, args, wl.n_arg, threads)
+            base, want = cpu_baseline(sample, wl.unit, threads, cpu_seconds, args.cpu_reps)
+            out["cpu_baseline"] = base
+            got = wl.gpu_region(sample.region)
+            if got is not None:
+                out["parity"] = {"sample_elements": int(np.asarray(want).size),
+                                 "sample": sample.desc.split(":")[0],
+                                 **parity_report(got, want, sample.tol)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", "--problem-size", dest="n", type=int, default=0,
+                    help="problem size override")
+    ap.add_argument("--extra", default=None,
+                    help="comma list of workloads measured in the same run after the headline "
+                         f"(N = 1 default for c5: {EXTRA_DEFAULT}; 'none' to skip)")
+    ap.add_argument("--cpu-rows", type=int, default=4_000_000)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU time of the headline cpu_baseline sample")
+    ap.add_argument("--extra-cpu-seconds", type=float, default=4.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--vl", type=int, default=0,
+                    help="SpMV: time the emitted-mapping vector kernel with this vector length")
+    ap.add_argument("--mtx", default="", help="Matrix Market file for --workload mtx")
+    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "tf32x3", "dmma", "exact", "ozaki"])
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    torch.cuda.set_device(local)
+    n = args.n or DEFAULT_N[args.workload]
+    wl = WORKLOADS[args.workload](args, rank, world, n)
+    wl.n_arg = n
+    head = measure(wl, args, rank, world, local, args.steps, args.warmup, args.cpu_seconds)
+    del wl
+    drop_memo()
+    torch.cuda.empty_cache()
+    extras = args.extra
+    if extras is None:
+        extras = EXTRA_DEFAULT if (args.workload == "c5" and world == 1 and not args.n
+                                   and not args.vl) else "none"
+    workloads = {}
+    for key in [k for k in extras.split(",") if k and k != "none"]:
+        try:
+            sub = WORKLOADS[key](args, rank, world, DEFAULT_N[key])
+            sub.n_arg = DEFAULT_N[key]
+            workloads[key] = measure(sub, args, rank, world, local, args.steps, args.warmup,
+                                     args.extra_cpu_seconds)
+            del sub
+        except Exception as e:   # one failing extra must not cost the headline line
+            workloads[key] = {"error": f"{type(e).__name__}: {e}"}
+        drop_memo()
+        torch.cuda.empty_cache()
+    out = {"metric": METRIC, "value": head.pop("value"), "unit": head.pop("unit"),
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": head.pop("ms_per_step"), "higher_is_better": True,
+           "scaling": head.pop("scaling"), "vs_baseline": None, "dtype": head.pop("dtype"),
+           "data": "synthetic (numpy-seeded inputs, synth_inputs.py; stencils generated on the "
+                   "device)",
+           **{k: v for k, v in head.items() if k not in ("steps", "warmup")}}
+    if workloads:
+        out["workloads"] = workloads
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

@@ -64,6 +64,10 @@ extern "C" {
 /* ----------------------------------------------------------------- library */
 const char* lapis_b200_last_error(void);
 int lapis_b200_version(void);
+/* Diagnostics (not a reference interface): the kernel nodes of a captured
+ * cudaGraph_t, one mangled name per line into buf (NUL-terminated, truncated
+ * to cap), their count in *nkernels — the bench's launch census of a step. */
+int lapis_b200_graph_kernels(void* graph, char* buf, int64_t cap, int64_t* nkernels);
 /* Select and warm up `device` for the calling thread (lapis_initialize,
  * golden/cpp/spmv.hpp:8-10). */
 int lapis_b200_init(int device);
@@ -206,13 +210,23 @@ int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream);
  * H = relu((A_hat X) W): config 4, the reference's one-function GCN
  * (oracle/ir/gcn_f32.mlir: loop-nest SpMM + linalg.matmul + linalg.elementwise
  * cmpf ogt / select).  X is [ncols, fin], W [fin, fout], H
- * [nrows, fout], row-major; both stages in the reference's order
- * (bit-identical).  dtype F32 or F64. */
+ * [nrows, fout], row-major.  The SpMM stage always sums in the reference's
+ * order; the dense stage (A_hat X) W + ReLU runs on the tcgen05 tensor cores
+ * (3xTF32, within the 1e-5 fp32 contract) for fp32 with fin = 64 and
+ * fout in {32, 64}, else in the reference order.  dtype F32 or F64. */
 int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz,
                          const void* rowptr, int rowptr_bytes,
                          const void* colind, int colind_bytes, const void* values,
                          const void* X, int64_t fin, const void* W, int64_t fout, void* H,
                          int dtype, void* stream);
+/* The same with the dense stage's mode: LAPIS_B200_GEMM_AUTO (as above) or
+ * LAPIS_B200_GEMM_EXACT (reference order for both stages: bit-identical to
+ * the reference interpreter). */
+int lapis_b200_gcn_layer_mode(int64_t nrows, int64_t ncols, int64_t nnz,
+                              const void* rowptr, int rowptr_bytes,
+                              const void* colind, int colind_bytes, const void* values,
+                              const void* X, int64_t fin, const void* W, int64_t fout, void* H,
+                              int mode, int dtype, void* stream);
 
 /* ------------------------------------------------------- synthetic inputs
  * Not reference interfaces: on-device generators for the benchmark matrices

@@ -33,6 +33,21 @@ REF_PKG = REF_ROOT / "pkg"
 OUT = HERE / "_ref"
 ORACLE_SO = HERE / "liblapis_oracle.so"
 REF_SO = OUT / "liblapis_ref.so"
+# the same objects built with -march=native (SURVEY 8(d) CPU recipe) plus the
+# ISA flags of the build host: oracle/ref.py loads this variant only on a host
+# whose CPU has every one of them (the GPU box's CPU may differ from this one)
+REF_SO_NATIVE = OUT / "liblapis_ref_native.so"
+NATIVE_FLAGS = OUT / "native_cpu_flags.txt"
+
+
+def cpu_flags() -> set:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("flags"):
+                return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
 
 # (header name, IR source, REF_KIND, value type, colind type, entry symbol)
 #   REF_KIND: 1 spmv, 2 spmm, 3 matmul, 4 matvec, 5 gcn
@@ -92,25 +107,29 @@ def build_reference(force: bool = False) -> Path | None:
     OUT.mkdir(exist_ok=True)
     driver = HERE / "ref_driver.cpp"
     deps = [driver, __file__, *(u[1] for u in REF_UNITS)]
-    if not force and not _stale(REF_SO, deps):
+    if not force and not _stale(REF_SO, deps) and not _stale(REF_SO_NATIVE, deps):
         return REF_SO
     runtime_hdr = OUT / "lapis_dualview_runtime.hpp"
-    objs = []
+    variants = {REF_SO: [], REF_SO_NATIVE: ["-march=native"]}
+    objs = {so: [] for so in variants}
     for name, ir, kind, vt, ct, entry in REF_UNITS:
         lowered = _lapis_cli(["opt", "--sparse-compiler-kokkos", str(ir)])
         (OUT / f"{name}.mlir").write_text(lowered)
         _lapis_cli(["translate", "--header-name", name, "--emit-runtime-header", str(runtime_hdr),
                     "-o", str(OUT / f"{name}.hpp"), str(OUT / f"{name}.mlir")])
-        obj = OUT / f"{name}.o"
-        cmd = ["g++", "-std=c++17", "-O3", "-ffp-contract=off", "-fPIC", "-pthread",
-               "-DLAPIS_USE_SERIAL_STUB", f"-I{OUT}", f"-I{REF_PKG / 'cxx_runtime/include'}",
-               f'-DREF_HEADER="{name}.hpp"', f"-DREF_KIND={kind}", f"-DREF_VT={vt}",
-               f"-DREF_CT={ct}", f"-DREF_ENTRY={entry}"]
-        if name == "spmv_ref":
-            cmd.append("-DREF_TRANSFER_PROBE")
-        _run(cmd + ["-c", str(driver), "-o", str(obj)])
-        objs.append(str(obj))
-    _run(["g++", "-shared", "-pthread", "-o", str(REF_SO), *objs])
+        for so, extra in variants.items():
+            obj = OUT / f"{name}{'_native' if extra else ''}.o"
+            cmd = ["g++", "-std=c++17", "-O3", *extra, "-ffp-contract=off", "-fPIC", "-pthread",
+                   "-DLAPIS_USE_SERIAL_STUB", f"-I{OUT}", f"-I{REF_PKG / 'cxx_runtime/include'}",
+                   f'-DREF_HEADER="{name}.hpp"', f"-DREF_KIND={kind}", f"-DREF_VT={vt}",
+                   f"-DREF_CT={ct}", f"-DREF_ENTRY={entry}"]
+            if name == "spmv_ref":
+                cmd.append("-DREF_TRANSFER_PROBE")
+            _run(cmd + ["-c", str(driver), "-o", str(obj)])
+            objs[so].append(str(obj))
+    for so in variants:
+        _run(["g++", "-shared", "-pthread", "-o", str(so), *objs[so]])
+    NATIVE_FLAGS.write_text(" ".join(sorted(cpu_flags())) + "\n")
     return REF_SO
 
 

@@ -22,6 +22,22 @@ def available() -> bool:
     return _build.REF_SO.exists()
 
 
+def variant() -> str:
+    """Which build runs: the -march=native one when this host's CPU has every
+    ISA flag of the build host, else the portable (-O3, baseline x86-64) one."""
+    so = _build.REF_SO_NATIVE
+    if so.exists() and _build.NATIVE_FLAGS.exists():
+        need = set(_build.NATIVE_FLAGS.read_text().split())
+        if need and need <= _build.cpu_flags():
+            return "native"
+    return "portable"
+
+
+def compile_flags() -> str:
+    return ("g++ -O3 -march=native (build host) -ffp-contract=off" if variant() == "native"
+            else "g++ -O3 -ffp-contract=off (portable: this CPU lacks an ISA flag of the build host)")
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
@@ -29,7 +45,8 @@ def lib() -> C.CDLL:
             _build.build_reference()
         if not _build.REF_SO.exists():
             raise RuntimeError("reference CPU path not built (needs /root/reference once)")
-        _lib = C.CDLL(str(_build.REF_SO))
+        so = _build.REF_SO_NATIVE if variant() == "native" else _build.REF_SO
+        _lib = C.CDLL(str(so))
         i64, vp, ci = C.c_int64, C.c_void_p, C.c_int
         for name in ("ref_spmv_f64_i64", "ref_spmv_f64_i32", "ref_spmm_f64_i32", "ref_gcn_f32_i32"):
             f = getattr(_lib, name)

@@ -63,6 +63,9 @@ _SIGNATURES = {
     "lapis_b200_relu": ([_I64, _VP, _VP, _INT, _VP], _INT),
     "lapis_b200_gcn_layer": ([_I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP, _I64,
                               _VP, _INT, _VP], _INT),
+    "lapis_b200_graph_kernels": ([_VP, C.c_char_p, _I64, C.POINTER(_I64)], _INT),
+    "lapis_b200_gcn_layer_mode": ([_I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP,
+                                   _I64, _VP, _INT, _INT, _VP], _INT),
     "lapis_b200_synth_stencil": ([_INT, _I64, _I64, _I64, _VP, _VP, _VP, _VP], _INT),
     "lapis_b200_csr_check": ([_I64, _VP, _INT, _VP, _INT, _I64, _I64, C.POINTER(_I64), _VP],
                              _INT),

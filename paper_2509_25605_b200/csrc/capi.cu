@@ -3,6 +3,11 @@
 // other translation units.
 #include "common.cuh"
 
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include <cstdio>
 #include <cstring>
 
@@ -42,7 +47,7 @@ int gemv(int64_t, int64_t, const void*, int64_t, const void*, void*, int, cudaSt
 int reduce_2d(int64_t, int64_t, const void*, void*, int, int, int, cudaStream_t);
 int relu(int64_t, const void*, void*, int, cudaStream_t);
 int gcn_layer(int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
-              const void*, int64_t, const void*, int64_t, void*, int, cudaStream_t);
+              const void*, int64_t, const void*, int64_t, void*, int, int, cudaStream_t);
 int synth_stencil(int, int64_t, int64_t, int64_t, int64_t*, int32_t*, double*, cudaStream_t);
 void release_workspaces();
 
@@ -57,6 +62,39 @@ extern "C" {
 const char* lapis_b200_last_error(void) { return g_last_error.c_str(); }
 
 int lapis_b200_version(void) { return 100; }
+
+int lapis_b200_graph_kernels(void* graph, char* buf, int64_t cap, int64_t* nkernels) {
+  // kernel nodes of a captured CUDA graph (one bench step), as
+  // "name\n" lines: the launch census of the step, independent of any tracer
+  if (!graph || !nkernels) return fail(LAPIS_B200_ERR_ARG, "graph_kernels: null argument");
+  cudaGraph_t g = reinterpret_cast<cudaGraph_t>(graph);
+  size_t n = 0;
+  LB_TRY(check_cuda(cudaGraphGetNodes(g, nullptr, &n), "cudaGraphGetNodes"));
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) LB_TRY(check_cuda(cudaGraphGetNodes(g, nodes.data(), &n), "cudaGraphGetNodes"));
+  std::string out;
+  int64_t k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    LB_TRY(check_cuda(cudaGraphNodeGetType(nd, &t), "cudaGraphNodeGetType"));
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams p;
+    const char* name = nullptr;
+    if (cudaGraphKernelNodeGetParams(nd, &p) == cudaSuccess && p.func)
+      cudaFuncGetName(&name, p.func);
+    cudaGetLastError();
+    out += name ? name : "?";
+    out += '\n';
+    ++k;
+  }
+  *nkernels = k;
+  if (buf && cap > 0) {
+    const size_t m = std::min<size_t>(out.size(), (size_t)cap - 1);
+    memcpy(buf, out.data(), m);
+    buf[m] = 0;
+  }
+  return LAPIS_B200_OK;
+}
 
 int lapis_b200_init(int device) {
   int n = 0;
@@ -174,7 +212,18 @@ int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz, const void* 
                          int dtype, void* stream) {
   keep_pool_memory();
   return gcn_layer(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, X, fin,
-                   W, fout, H, dtype, S(stream));
+                   W, fout, H, LAPIS_B200_GEMM_AUTO, dtype, S(stream));
+}
+
+int lapis_b200_gcn_layer_mode(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr,
+                              int rowptr_bytes, const void* colind, int colind_bytes,
+                              const void* values, const void* X, int64_t fin, const void* W,
+                              int64_t fout, void* H, int mode, int dtype, void* stream) {
+  keep_pool_memory();
+  if (mode != LAPIS_B200_GEMM_AUTO && mode != LAPIS_B200_GEMM_EXACT)
+    return fail(LAPIS_B200_ERR_ARG, "gcn: mode must be AUTO or EXACT");
+  return gcn_layer(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, X, fin,
+                   W, fout, H, mode, dtype, S(stream));
 }
 
 int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,

@@ -1,0 +1,288 @@
+// gcn_dense.cu — the GCN layer's dense stage H = relu(T W) on the tcgen05
+// tensor cores (config 4: T = A_hat X [1M x 64] fp32, W [64 x 64]).
+//
+// The reference computes it as linalg.matmul into a temporary followed by
+// linalg.elementwise ReLU (oracle/ir/gcn_f32.mlir; interp.py:711-722 and the
+// cmpf ogt + select of the elementwise op).  Its fp32 contract is 1e-5 under
+// diff_outputs, which 3xTF32 meets with margin at K = 64
+// (|error| <~ K * 2^-22 relative to sum |t||w|); the bit-identical SIMT kernel
+// (gemm_exact_narrow_kernel) stays behind the EXACT mode.
+//
+// The stage is HBM-bound (T read once, H written once: 512 MB; 8.4 GFLOP), so
+// the split into TF32 head and tail happens IN the kernel, on the tile in
+// shared memory — no split prepass over T.  One persistent CTA per SM:
+//   warp 4      TMA producer: 128 x 64 fp32 tiles of T (two 128 x 32 boxes,
+//               SWIZZLE_128B) into a 3-stage ring (full / empty mbarriers)
+//   warps 0-3   per tile: split the tile in place (head overwrites T, tail to
+//               a second buffer, same swizzled layout), one elected thread
+//               issues 3 x 8 tcgen05.mma.kind::tf32 (M = 128, N = fout, K = 8;
+//               tails first, heads last) into one of two TMEM accumulators,
+//               then — while those MMAs run — drain the PREVIOUS tile's
+//               accumulator (tcgen05.ld 32x32b, ReLU select), stage it in
+//               shared memory in the SWIZZLE_128B layout and write it with a
+//               TMA tensor store.
+// W is split once per CTA into head / tail K-major operands (W^T rows).
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+#include <algorithm>
+
+namespace lapis_b200 {
+
+constexpr int GD_BM = 128, GD_K = 64, GD_STAGES = 3, GD_THREADS = 160;
+constexpr uint32_t GD_TILE_BYTES = GD_BM * GD_K * 4;  // 32 KB: two 128 x 32 boxes
+constexpr int GD_NMAX = 64;
+constexpr uint32_t GD_B_BYTES = GD_NMAX * GD_K * 4;   // 16 KB per split half
+constexpr size_t GD_SMEM = (size_t)GD_STAGES * GD_TILE_BYTES + GD_TILE_BYTES /*tail*/ +
+                           2 * GD_B_BYTES + GD_TILE_BYTES /*H staging*/ + 1024;
+
+// instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
+__host__ __device__ constexpr uint32_t tf32_idesc_gd(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_head(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// byte offset of element (row, k) in a K-major SWIZZLE_128B operand whose K
+// extent is split into 128-byte (32-float) column sets of `rows` rows each
+__device__ __forceinline__ uint32_t sw128_off(int row, int k, int rows) {
+  const int set = k >> 5, kk = k & 31;
+  const int chunk = (kk >> 2) ^ (row & 7);
+  return (uint32_t)(set * rows * 128 + row * 128 + (chunk << 4) + ((kk & 3) << 2));
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bar_compute() {  // warps 0-3 only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <int N>
+__global__ void __launch_bounds__(GD_THREADS, 1)
+gcn_dense_tf32x3_kernel(const __grid_constant__ CUtensorMap tT, const __grid_constant__ CUtensorMap tH,
+                        const float* __restrict__ W, int64_t ldw, int ntiles) {
+  static_assert(N == 32 || N == 64, "fout must be 32 or 64");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* ring = smem;                                        // [STAGES][32 KB]
+  uint8_t* tail = ring + GD_STAGES * GD_TILE_BYTES;            // 32 KB
+  uint8_t* bhi = tail + GD_TILE_BYTES;                         // N x 64 K-major
+  uint8_t* blo = bhi + GD_B_BYTES;
+  uint8_t* stage_h = blo + GD_B_BYTES;                         // 128 x N fp32, SW128 sets
+  __shared__ uint64_t full[GD_STAGES], empty[GD_STAGES], mma_done;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tT);
+    prefetch_tmap(&tH);
+    for (int s = 0; s < GD_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&mma_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&tmem_slot)), "r"(2 * N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // W -> W^T head / tail (row n of B^T = column n of W), once per CTA
+  for (int i = threadIdx.x; i < N * GD_K; i += blockDim.x) {
+    const int n = i % N, k = i / N;   // consecutive threads read consecutive columns of a W row
+    const float w = W[(int64_t)k * ldw + n];
+    const float h = tf32_head(w);
+    const uint32_t off = sw128_off(n, k, N);
+    *reinterpret_cast<float*>(bhi + off) = h;
+    *reinterpret_cast<float*>(blo + off) = tf32_head(w - h);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* dst = ring + s * GD_TILE_BYTES;
+        mbar_arrive_expect_tx(&full[s], GD_TILE_BYTES);
+        tma_load_2d(dst, &tT, 0, t * GD_BM, &full[s]);
+        tma_load_2d(dst + GD_TILE_BYTES / 2, &tT, 32, t * GD_BM, &full[s]);
+        if (++s == GD_STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // --------------------------------------- split, MMA issue, epilogue
+    constexpr uint32_t idesc = tf32_idesc_gd(GD_BM, N);
+    const int row = warp * 32 + lane;   // the TMEM lane / tile row this thread drains
+    int s = 0;
+    uint32_t ph = 0;
+    int i = 0;
+    int prev_tile = -1;
+    auto epilogue = [&](int tile, int acc) {
+      // previous TMA store must have finished reading the staging buffer
+      if (threadIdx.x == 0) bulk_wait_read0();
+      bar_compute();
+      const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * N);
+#pragma unroll
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_x16(tbase + (uint32_t)c0, v);
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          float4 o;
+          float* op = reinterpret_cast<float*>(&o);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x = __uint_as_float(v[q + e]);
+            op[e] = (x > 0.0f) ? x : 0.0f;   // cmpf ogt + select: NaN and -0.0 map to +0
+          }
+          *reinterpret_cast<float4*>(stage_h + sw128_off(row, c0 + q, GD_BM)) = o;
+        }
+      }
+      tc_fence_before();
+      fence_async_smem();
+      bar_compute();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int set = 0; set < N / 32; ++set)
+          tma_store_2d(&tH, stage_h + set * GD_BM * 128, set * 32, tile * GD_BM);
+        bulk_commit();
+      }
+    };
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      mbar_wait(&full[s], ph);
+      if (i > 0) mbar_wait(&mma_done, (uint32_t)((i - 1) & 1));   // tail buffer free, acc ready
+      // split the tile in place: head over T, tail into `tail` (same layout)
+      uint8_t* a = ring + s * GD_TILE_BYTES;
+#pragma unroll 4
+      for (int q = threadIdx.x; q < (int)(GD_TILE_BYTES / 16); q += 128) {
+        float4 x = reinterpret_cast<float4*>(a)[q];
+        float4 h = make_float4(tf32_head(x.x), tf32_head(x.y), tf32_head(x.z), tf32_head(x.w));
+        reinterpret_cast<float4*>(a)[q] = h;
+        reinterpret_cast<float4*>(tail)[q] =
+            make_float4(tf32_head(x.x - h.x), tf32_head(x.y - h.y), tf32_head(x.z - h.z),
+                        tf32_head(x.w - h.w));
+      }
+      fence_async_smem();
+      tc_fence_before();
+      bar_compute();
+      tc_fence_after();
+      const int acc = i & 1;
+      if (warp == 0) {
+        if (elect_one()) {
+          const uint32_t d = tmem_base + (uint32_t)(acc * N);
+          bool first = true;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {   // lo*hi, hi*lo, hi*hi
+            const uint8_t* A_ = p == 0 ? tail : a;
+            const uint8_t* B_ = p == 1 ? blo : bhi;
+#pragma unroll
+            for (int set = 0; set < 2; ++set) {
+              const uint64_t ad = smem_desc_sw128(A_ + set * GD_BM * 128);
+              const uint64_t bd = smem_desc_sw128(B_ + set * N * 128);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                tc_mma_tf32(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                            first ? 0u : 1u);
+                first = false;
+              }
+            }
+          }
+          tc_commit(&empty[s]);
+          tc_commit(&mma_done);
+        }
+        __syncwarp();
+      }
+      if (prev_tile >= 0) epilogue(prev_tile, acc ^ 1);
+      prev_tile = t;
+      if (++s == GD_STAGES) { s = 0; ph ^= 1; }
+    }
+    if (prev_tile >= 0) {
+      mbar_wait(&mma_done, (uint32_t)((i - 1) & 1));
+      tc_fence_after();
+      epilogue(prev_tile, (i - 1) & 1);
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(tmem_base), "r"(2 * N));
+  }
+}
+
+static int make_rows_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols,
+                         int64_t ld) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  const cuuint32_t box[2] = {32, (cuuint32_t)GD_BM};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled failed (gcn)");
+  return LAPIS_B200_OK;
+}
+
+// Shapes the tensor-core stage takes: fin = 64, fout in {32, 64}, 16-byte row
+// pitches and bases (TMA).  Anything else goes to the reference-order kernel.
+bool gcn_dense_tc_ok(int64_t m, int64_t fout, int64_t fin, const void* T, int64_t ldt,
+                     const void* H, int64_t ldh) {
+  return m > 0 && fin == GD_K && (fout == 32 || fout == 64) && ldt % 4 == 0 && ldh % 4 == 0 &&
+         (uintptr_t)T % 16 == 0 && (uintptr_t)H % 16 == 0 && m <= (int64_t)0x7fffffff * GD_BM;
+}
+
+int gcn_dense_tf32x3(int64_t m, int64_t fout, int64_t fin, const void* T, int64_t ldt,
+                     const void* W, int64_t ldw, void* H, int64_t ldh, cudaStream_t st) {
+  if (!gcn_dense_tc_ok(m, fout, fin, T, ldt, H, ldh))
+    return fail(LAPIS_B200_ERR_ARG, "gcn dense: unsupported shape for the tensor-core stage");
+  CUtensorMap mt, mh;
+  LB_TRY(make_rows_map(&mt, (const float*)T, m, fin, ldt));
+  LB_TRY(make_rows_map(&mh, (const float*)H, m, fout, ldh));
+  const int ntiles = (int)((m + GD_BM - 1) / GD_BM);
+  const int grid = std::min(ntiles, num_sms());
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    LB_TRY(check_cuda(cudaFuncSetAttribute(gcn_dense_tf32x3_kernel<32>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GD_SMEM),
+                      "smem attr (gcn dense 32)"));
+    LB_TRY(check_cuda(cudaFuncSetAttribute(gcn_dense_tf32x3_kernel<64>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GD_SMEM),
+                      "smem attr (gcn dense 64)"));
+    configured_dev = dev;
+  }
+  if (fout == 64)
+    gcn_dense_tf32x3_kernel<64><<<grid, GD_THREADS, GD_SMEM, st>>>(mt, mh, (const float*)W, ldw, ntiles);
+  else
+    gcn_dense_tf32x3_kernel<32><<<grid, GD_THREADS, GD_SMEM, st>>>(mt, mh, (const float*)W, ldw, ntiles);
+  return check_launch("gcn_dense_tf32x3_kernel");
+}
+
+}  // namespace lapis_b200

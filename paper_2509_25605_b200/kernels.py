@@ -251,8 +251,11 @@ def relu(x, y=None, *, stream=None):
     return y
 
 
-def gcn_layer(rowptr, colind, values, X, W, H=None, *, nnz: int | None = None, stream=None):
-    """H = relu((A_hat X) W) — config 4 (oracle/ir/gcn_f32.mlir), reference order."""
+def gcn_layer(rowptr, colind, values, X, W, H=None, *, nnz: int | None = None, stream=None,
+              exact: bool = False):
+    """H = relu((A_hat X) W) — config 4 (oracle/ir/gcn_f32.mlir).  The SpMM stage
+    sums in the reference order; the dense stage runs on the tensor cores
+    (3xTF32, within 1e-5) unless ``exact`` (reference order: bit-identical)."""
     for t, nm in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (X, "X"), (W, "W")):
         _dev(t, nm)
     if X.dim() != 2 or W.dim() != 2 or X.shape[1] != W.shape[0]:
@@ -265,10 +268,11 @@ def gcn_layer(rowptr, colind, values, X, W, H=None, *, nnz: int | None = None, s
         raise BackendError("gcn: element types must match", _capi.ERR_ARG)
     if nnz is None:
         nnz = int(rowptr[-1].item() - rowptr[0].item())
-    check(_capi.lib().lapis_b200_gcn_layer(
+    check(_capi.lib().lapis_b200_gcn_layer_mode(
         nrows, X.shape[0], nnz, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"), _ptr(colind),
         _idx_bytes(colind, "colind"), _ptr(values), _ptr(X), X.shape[1], _ptr(W), W.shape[1],
-        _ptr(H), _dtype(values, "values"), _stream(stream)), "gcn_layer")
+        _ptr(H), _MODES["exact" if exact else "auto"], _dtype(values, "values"), _stream(stream)),
+        "gcn_layer")
     return H
 
 

@@ -265,6 +265,97 @@ class RowBlockSpmm:
                         nnz=self.nnz, stream=stream)
 
 
+# ------------------------------------------------------------ dense GEMM
+class RowBlockGemm:
+    """C[r0:r1, :] = A[r0:r1, :] B on rank r: the rows
+    of A and C are sharded in equal blocks (equal_row_ranges), B is replicated
+    by ONE broadcast from rank 0 when the operator is built — outside any
+    steady-state step, and stated as such in the bench line.  The step itself
+    has no collective: every C row is computed whole on one GPU, so C is
+    bit-identical to the one-GPU product for every mode (the k order of an
+    output element does not depend on the row blocking).  ``gather_c`` is the
+    optional all-gather of C (not part of the step)."""
+
+    def __init__(self, A_local: torch.Tensor, B: torch.Tensor, m_global: int, rank: int,
+                 world: int, group=None, src: int = 0):
+        self.A_local, self.B = A_local, B
+        self.m, self.rank, self.world, self.group = m_global, rank, world, group
+        self.ranges = equal_row_ranges(m_global, world)
+        self.row_begin, self.row_end = self.ranges[rank]
+        if A_local.shape[0] != self.row_end - self.row_begin:
+            raise ValueError("A_local must hold this rank's row block")
+        self.broadcast_bytes = B.numel() * B.element_size()
+        if world > 1:
+            if B.is_cuda and dist.get_backend(group) == "gloo":
+                host = B.cpu()
+                dist.broadcast(host, src, group=group)
+                B.copy_(host)
+            else:
+                dist.broadcast(B, src, group=group)
+
+    def multiply(self, C_local: torch.Tensor, mode: str = "auto", stream=None) -> torch.Tensor:
+        from .kernels import gemm
+        return gemm(self.A_local, self.B, C_local, mode=mode, stream=stream)
+
+    def gather_c(self, C_local: torch.Tensor) -> torch.Tensor:
+        c = -(-self.m // self.world)
+        full = torch.zeros((self.world * c, C_local.shape[1]), dtype=C_local.dtype,
+                           device=C_local.device)
+        slot = full[self.rank * c:self.rank * c + C_local.shape[0]]
+        slot.copy_(C_local)
+        if self.world > 1:
+            mine = full[self.rank * c:(self.rank + 1) * c]
+            if full.is_cuda and dist.get_backend(self.group) == "gloo":
+                host = full.cpu()
+                dist.all_gather_into_tensor(host, mine.cpu(), group=self.group)
+                full.copy_(host)
+            else:
+                dist.all_gather_into_tensor(full, mine, group=self.group)
+        return full[:self.m]
+
+
+# ------------------------------------------------------------- GCN layer
+class RowBlockGcn:
+    """H[r0:r1] = relu((A_hat[r0:r1, :] X) W) on rank r:
+    A_hat and H in row blocks, X row-sharded like RowBlockSpmm (one NCCL
+    all-gather of the features per step, the layer's only exchange), W
+    replicated (broadcast once from rank 0 at construction).  Each H row is
+    computed whole on one GPU (bit-identical to one GPU)."""
+
+    def __init__(self, rowptr: torch.Tensor, colind: torch.Tensor, values: torch.Tensor,
+                 W: torch.Tensor, nrows_global: int, rank: int, world: int, group=None):
+        self.spmm = RowBlockSpmm(rowptr, colind, values, nrows_global, W.shape[0], rank, world,
+                                 group)
+        self.W, self.rank, self.world, self.group = W, rank, world, group
+        self.row_begin, self.row_end = self.spmm.row_begin, self.spmm.row_end
+        if world > 1:
+            if W.is_cuda and dist.get_backend(group) == "gloo":
+                host = W.cpu()
+                dist.broadcast(host, 0, group=group)
+                W.copy_(host)
+            else:
+                dist.broadcast(W, 0, group=group)
+
+    @property
+    def x_local(self) -> torch.Tensor:
+        return self.spmm.x_local
+
+    @property
+    def gather_bytes(self) -> int:
+        return self.spmm.gather_bytes
+
+    def gather(self) -> None:
+        self.spmm.gather()
+
+    def multiply(self, H_local: torch.Tensor, stream=None, replicated: bool = False):
+        from .kernels import gcn_layer
+        if not replicated:
+            self.gather()
+        sp = self.spmm
+        return gcn_layer(sp.rowptr, sp.colind, sp.values, sp.X_full[:sp.N], self.W, H_local,
+                         nnz=sp.nnz, stream=stream)
+
+
 # ------------------------------------------------- native (C-ABI) row blocks
 class NcclComm:
     """A communicator of the backend's own (lapis_b200_nccl_comm_init): rank 0
