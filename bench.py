@@ -1190,6 +1190,9 @@ def _short_name(name: str) -> str:
     return name.split("(")[0].replace("void ", "").replace("lapis_b200::", "")
 
 
+GRAPH_CENSUS_ERR: list = []
+
+
 def graph_census(wl):
     """Kernels of one step, read from a CUDA graph capture of that step
     (lapis_b200_graph_kernels walks the captured graph's kernel nodes): exact
@@ -1226,7 +1229,8 @@ def graph_census(wl):
             k = _short_name(nm)
             per[k] = per.get(k, 0) + 1
         return per
-    except Exception:
+    except Exception as e:
+        GRAPH_CENSUS_ERR.append(f"{type(e).__name__}: {e}"[:200])
         return None
     finally:
         wl.stream = old_stream
@@ -1279,7 +1283,8 @@ def launch_census(wl):
     if counts:
         counts = {k: c for k, c in counts.items() if "lapis" in k}
     if not counts:
-        counts, src = pcounts, "CUDA activity trace of one untimed step x steps"
+        counts, src = pcounts, "CUDA activity trace of one untimed step x steps" + (
+            f" (graph capture failed: {GRAPH_CENSUS_ERR[-1]})" if GRAPH_CENSUS_ERR else "")
     if not counts:
         return None, None
     shares = shares or {}

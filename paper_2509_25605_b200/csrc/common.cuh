@@ -1,6 +1,8 @@
 // common.cuh — shared helpers for the sm_100a kernels behind include/lapis_b200.h.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <string>
@@ -137,6 +139,35 @@ inline int num_sms() {
     cached[dev] = v > 0 ? v : 148;
   }
   return cached[dev];
+}
+
+// A per-device, highest-priority, non-blocking stream for work that may run
+// concurrently with the caller's stream inside one library call (forked and
+// joined with events, so the call stays stream-ordered for the caller and is
+// graph-capturable).  nullptr when it cannot be created (the caller then
+// stays on its own stream).  LAPIS_B200_NO_SIDE_STREAM=1 disables it.
+inline cudaStream_t long_row_stream() {
+  static cudaStream_t streams[64] = {nullptr};
+  static int disabled = -1;
+  if (disabled < 0) {
+    const char* e = getenv("LAPIS_B200_NO_SIDE_STREAM");
+    disabled = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (disabled) return nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    streams[dev] = s;
+  }
+  return streams[dev];
 }
 
 }  // namespace lapis_b200

@@ -50,12 +50,14 @@ spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                 DescGuard guard = DescGuard()) {
   if (guard.skip()) return;
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * SPMM_WARPS + (threadIdx.x >> 5);
-  if (row >= nrows) return;
+  // grid-stride over rows, one warp per row (a guarded launch that is not
+  // selected costs one small grid, not one CTA per 8 rows)
+  for (int64_t row = (int64_t)blockIdx.x * SPMM_WARPS + (threadIdx.x >> 5); row < nrows;
+       row += (int64_t)gridDim.x * SPMM_WARPS) {
   const int64_t b = (int64_t)rowptr[row];
   int64_t e = (int64_t)rowptr[row + 1];
   if (e < b) e = b;
-  if (e - b > SPLIT && !guard.all_rows()) return;  // long row: kernels 2-3
+  if (e - b > SPLIT && !guard.all_rows()) continue;  // long row: kernels 2-3
   for (int64_t c0 = 0; c0 < k; c0 += 32 * EPL) {
     const int64_t col = c0 + (int64_t)lane * EPL;
     const bool full = col + EPL <= k;
@@ -103,6 +105,7 @@ spmm_row_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
 #pragma unroll
     for (int q = 0; q < EPL; ++q)
       if (col + q < k) yr[q] = acc[q];
+  }
   }
 }
 
@@ -756,9 +759,91 @@ struct SpmmOp {
       long_rows_list_kernel<RP><<<(unsigned)(g > 0 ? g : 1), 256, 0, st>>>(nrows, (const RP*)rowptr, lr);
       LB_TRY(check_launch("long_rows_list_kernel"));
     }
+    const int64_t row_grid = blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16;
     DescGuard fast, fallback;
     fast.desc = fallback.desc = lr.desc;
     fallback.mode = 1;
+    // ---- long rows (> SPLIT entries): listed above, folded (fp32: exact
+    // order) or chunked + combined on a high-priority side stream, CONCURRENT
+    // with the short-row kernels below — they write disjoint rows of Y, and a
+    // hub row's fold is a long dependent add chain (config 4: 70k entries)
+    // that would otherwise run alone on a few SMs after the batch kernel
+    T* part = nullptr;
+    cudaStream_t ls = st;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    auto join_long = [&]() -> int {
+      int jrc = LAPIS_B200_OK;
+      if (ev_join) {
+        jrc = check_cuda(cudaStreamWaitEvent(st, ev_join, 0), "join long-row stream");
+        cudaEventDestroy(ev_join);
+      }
+      if (ev_fork) cudaEventDestroy(ev_fork);
+      if (part) cudaFreeAsync(part, st);
+      return jrc;
+    };
+    if (nnz > SPLIT) {
+      cudaStream_t side = long_row_stream();
+      if (side && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventRecord(ev_fork, st) == cudaSuccess &&
+          cudaStreamWaitEvent(side, ev_fork, 0) == cudaSuccess)
+        ls = side;
+      cudaGetLastError();
+      int rc = LAPIS_B200_OK;
+      [&] {
+      // ---- long rows: fold (fp32 exact) or chunk + combine
+      if constexpr (std::is_same<T, float>::value) {
+        constexpr size_t pipe_smem = pipe_smem_bytes<CI>();
+        if (rc == LAPIS_B200_OK)
+          rc = check_cuda(cudaFuncSetAttribute(spmm_seq_long_pipe_kernel<RP, CI>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)pipe_smem), "smem attr (seq pipe)");
+        if (rc == LAPIS_B200_OK) {
+          const int64_t items = cap * ((k + PIPE_KC - 1) / PIPE_KC);
+          const int64_t g = items < (int64_t)sms * 2 ? items : (int64_t)sms * 2;
+          spmm_seq_long_pipe_kernel<RP, CI><<<(unsigned)g, 256, pipe_smem, ls>>>(
+              k, (const RP*)rowptr, (const CI*)colind, (const float*)values, (const float*)X, ldx,
+              (float*)Y, ldy, lr);
+          rc = check_launch("spmm_seq_long_pipe_kernel");
+        }
+        if (rc == LAPIS_B200_OK && W) {
+          const int64_t g = (cap + 7) / 8 < sms ? (cap + 7) / 8 : sms;
+          gcn_long_rows_epilogue_kernel<<<(unsigned)g, 256, 0, ls>>>((const float*)W, (float*)Y,
+                                                                       ldy, lr);
+          rc = check_launch("gcn_long_rows_epilogue_kernel");
+        }
+      } else {
+      if (rc == LAPIS_B200_OK) {
+        long_rows_work_kernel<RP><<<1, 1024, 0, ls>>>((const RP*)rowptr, lr);
+        rc = check_launch("long_rows_work_kernel");
+      }
+      if (rc == LAPIS_B200_OK)
+        rc = check_cuda(cudaMallocAsync((void**)&part, (size_t)wcap * k * sizeof(T), ls), "alloc(part)");
+      const size_t smem = (size_t)SPMM_WARPS * k * sizeof(T);
+      if (rc == LAPIS_B200_OK && smem > 48 * 1024) {
+        rc = check_cuda(cudaFuncSetAttribute(spmm_long_chunk_kernel<T, RP, CI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "smem attr");
+        if (rc == LAPIS_B200_OK && smem > 200 * 1024)
+          rc = fail(LAPIS_B200_ERR_UNSUPPORTED, "spmm: k too large for long-row staging");
+      }
+      if (rc == LAPIS_B200_OK) {
+        const int64_t g = wcap < (int64_t)sms * 8 ? wcap : (int64_t)sms * 8;
+        spmm_long_chunk_kernel<T, RP, CI><<<(unsigned)g, SPMM_WARPS * 32, smem, ls>>>(
+            k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, part, lr);
+        rc = check_launch("spmm_long_chunk_kernel");
+      }
+      if (rc == LAPIS_B200_OK) {
+        const int64_t g = cap < (int64_t)sms * 4 ? cap : (int64_t)sms * 4;
+        spmm_long_combine_kernel<T, RP><<<(unsigned)g, 64, 0, ls>>>(k, (const RP*)rowptr, part,
+                                                                   (T*)Y, ldy, lr);
+        rc = check_launch("spmm_long_combine_kernel");
+      }
+        }
+      }();
+      if (ls != st) cudaEventRecord(ev_join, ls);
+      if (rc != LAPIS_B200_OK) { join_long(); return rc; }
+    }
     if (batch) {
       int64_t gblocks = ((nrows + 31) / 32 + 7) / 8;
       const int64_t gcap = (int64_t)sms * 8;
@@ -814,78 +899,25 @@ struct SpmmOp {
       }
 #undef LB_GRP
     } else if (vec)
-      spmm_row_kernel<T, RP, CI, 2><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+      spmm_row_kernel<T, RP, CI, 2><<<(unsigned)row_grid, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
           (T*)Y, ldy, fast);
     else
-      spmm_row_kernel<T, RP, CI, 1><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+      spmm_row_kernel<T, RP, CI, 1><<<(unsigned)row_grid, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
           (T*)Y, ldy, fast);
     LB_TRY(check_launch("spmm_row_kernel"));
     // decreasing rowptr only: one warp per row, every row on its clamped range
     if (vec)
-      spmm_row_kernel<T, RP, CI, 2><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+      spmm_row_kernel<T, RP, CI, 2><<<(unsigned)row_grid, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
           (T*)Y, ldy, fallback);
     else
-      spmm_row_kernel<T, RP, CI, 1><<<(unsigned)blocks, SPMM_WARPS * 32, 0, st>>>(
+      spmm_row_kernel<T, RP, CI, 1><<<(unsigned)row_grid, SPMM_WARPS * 32, 0, st>>>(
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
           (T*)Y, ldy, fallback);
     LB_TRY(check_launch("spmm_row_kernel(fallback)"));
-    if (nnz <= SPLIT) return LAPIS_B200_OK;  // no row can be long
-    // ---- long rows: fold (fp32 exact) or chunk + combine
-    int rc = LAPIS_B200_OK;
-    if constexpr (std::is_same<T, float>::value) {
-      constexpr size_t pipe_smem = pipe_smem_bytes<CI>();
-      if (rc == LAPIS_B200_OK)
-        rc = check_cuda(cudaFuncSetAttribute(spmm_seq_long_pipe_kernel<RP, CI>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)pipe_smem), "smem attr (seq pipe)");
-      if (rc == LAPIS_B200_OK) {
-        const int64_t items = cap * ((k + PIPE_KC - 1) / PIPE_KC);
-        const int64_t g = items < (int64_t)sms * 2 ? items : (int64_t)sms * 2;
-        spmm_seq_long_pipe_kernel<RP, CI><<<(unsigned)g, 256, pipe_smem, st>>>(
-            k, (const RP*)rowptr, (const CI*)colind, (const float*)values, (const float*)X, ldx,
-            (float*)Y, ldy, lr);
-        rc = check_launch("spmm_seq_long_pipe_kernel");
-      }
-      if (rc == LAPIS_B200_OK && W) {
-        const int64_t g = (cap + 7) / 8 < sms ? (cap + 7) / 8 : sms;
-        gcn_long_rows_epilogue_kernel<<<(unsigned)g, 256, 0, st>>>((const float*)W, (float*)Y,
-                                                                     ldy, lr);
-        rc = check_launch("gcn_long_rows_epilogue_kernel");
-      }
-      return rc;
-    }
-    if (rc == LAPIS_B200_OK) {
-      long_rows_work_kernel<RP><<<1, 1024, 0, st>>>((const RP*)rowptr, lr);
-      rc = check_launch("long_rows_work_kernel");
-    }
-    T* part = nullptr;
-    if (rc == LAPIS_B200_OK)
-      rc = check_cuda(cudaMallocAsync((void**)&part, (size_t)wcap * k * sizeof(T), st), "alloc(part)");
-    const size_t smem = (size_t)SPMM_WARPS * k * sizeof(T);
-    if (rc == LAPIS_B200_OK && smem > 48 * 1024) {
-      rc = check_cuda(cudaFuncSetAttribute(spmm_long_chunk_kernel<T, RP, CI>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                      "smem attr");
-      if (rc == LAPIS_B200_OK && smem > 200 * 1024)
-        rc = fail(LAPIS_B200_ERR_UNSUPPORTED, "spmm: k too large for long-row staging");
-    }
-    if (rc == LAPIS_B200_OK) {
-      const int64_t g = wcap < (int64_t)sms * 8 ? wcap : (int64_t)sms * 8;
-      spmm_long_chunk_kernel<T, RP, CI><<<(unsigned)g, SPMM_WARPS * 32, smem, st>>>(
-          k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, part, lr);
-      rc = check_launch("spmm_long_chunk_kernel");
-    }
-    if (rc == LAPIS_B200_OK) {
-      const int64_t g = cap < (int64_t)sms * 4 ? cap : (int64_t)sms * 4;
-      spmm_long_combine_kernel<T, RP><<<(unsigned)g, 64, 0, st>>>(k, (const RP*)rowptr, part,
-                                                                 (T*)Y, ldy, lr);
-      rc = check_launch("spmm_long_combine_kernel");
-    }
-    if (part) cudaFreeAsync(part, st);
-    return rc;
+    return join_long();
   }
 };
 

@@ -30,7 +30,17 @@ def _device_init(t: torch.Tensor) -> None:
         _initialised.add(idx)
 
 
+def _from_dlpack(t):
+    """A DLPack producer (CuPy, JAX, numba, ... anything with __dlpack__) as a
+    zero-copy torch view of the same device memory (tensors via
+    DLPack stand in for unmanaged Kokkos Views)."""
+    if isinstance(t, torch.Tensor) or not hasattr(t, "__dlpack__"):
+        return t
+    return torch.from_dlpack(t)
+
+
 def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    t = _from_dlpack(t)
     if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
         raise BackendError(f"{name} must be a CUDA tensor (no CPU fallback)", _capi.ERR_ARG)
     if not t.is_contiguous():
@@ -70,17 +80,38 @@ def _check_values(values, x, y):
         raise BackendError("values/x/y element types must match (dialect.py:811)", _capi.ERR_ARG)
 
 
-def spmv_csr(rowptr, colind, values, x, y=None, *, vector_length: int = 0, nnz: int | None = None,
-             stream=None) -> torch.Tensor:
+def _csr_parts(A):
+    """(rowptr, colind, values) of a torch.sparse_csr_tensor, zero-copy."""
+    if not (isinstance(A, torch.Tensor) and A.layout == torch.sparse_csr):
+        raise BackendError("expected a torch.sparse_csr_tensor", _capi.ERR_ARG)
+    return A.crow_indices(), A.col_indices(), A.values()
+
+
+def _is_csr(A) -> bool:
+    return isinstance(A, torch.Tensor) and A.layout == torch.sparse_csr
+
+
+def spmv_csr(rowptr, colind=None, values=None, x=None, y=None, *, vector_length: int = 0,
+             nnz: int | None = None, stream=None) -> torch.Tensor:
     """y = A x for CSR A (sparse.spmv_csr, interp.py:798-812).  y is overwritten
     and returned (allocated when None).  ``nnz`` may be passed to avoid reading
-    rowptr[N] back from the device."""
+    rowptr[N] back from the device.
+
+    Also ``spmv_csr(A, x[, y])`` with A a CUDA ``torch.sparse_csr_tensor``
+    (crow / col / values used in place, the ``torch.mv(A_csr, x)`` of
+    PAPER.md:298-313).  Any argument may be a DLPack producer."""
+    if _is_csr(rowptr):
+        A, x, y = rowptr, colind, values
+        rowptr, colind, values = _csr_parts(A)
+        if nnz is None:
+            nnz = A.values().numel()
+    rowptr, colind, values, x, y = (_from_dlpack(t) for t in (rowptr, colind, values, x, y))
     for t, n in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (x, "x")):
         _dev(t, n)
     nrows = rowptr.numel() - 1
     if y is None:
         y = torch.empty(max(nrows, 0), dtype=values.dtype, device=values.device)
-    _dev(y, "y")
+    y = _dev(y, "y")
     _check_values(values, x, y)
     if nrows < 0:
         raise BackendError("rowptr must have at least one entry", _capi.ERR_ARG)
@@ -101,7 +132,9 @@ class CsrPlan:
 
     def __init__(self, rowptr: torch.Tensor, nnz: int | None = None, stream=None,
                  exact: bool | None = None):
-        _dev(rowptr, "rowptr")
+        if _is_csr(rowptr):
+            rowptr = rowptr.crow_indices()
+        rowptr = _dev(rowptr, "rowptr")
         self.nrows = rowptr.numel() - 1
         self.nnz = int(rowptr[-1].item() - rowptr[0].item()) if nnz is None else int(nnz)
         self.rowptr = rowptr
@@ -128,11 +161,12 @@ class CsrPlan:
                 "warpblock": wb, "ntiles": int(out[2]), "kernel": kernel}
 
     def spmv(self, colind, values, x, y=None, *, stream=None) -> torch.Tensor:
+        colind, values, x, y = (_from_dlpack(t) for t in (colind, values, x, y))
         for t, n in ((colind, "colind"), (values, "values"), (x, "x")):
             _dev(t, n)
         if y is None:
             y = torch.empty(self.nrows, dtype=values.dtype, device=values.device)
-        _dev(y, "y")
+        y = _dev(y, "y")
         _check_values(values, x, y)
         check(_capi.lib().lapis_b200_spmv_csr_plan(
             self._handle, _ptr(self.rowptr), _idx_bytes(self.rowptr, "rowptr"), _ptr(colind),
@@ -152,8 +186,17 @@ class CsrPlan:
             pass
 
 
-def spmm_csr(rowptr, colind, values, X, Y=None, *, nnz: int | None = None, stream=None):
-    """Y = A X for CSR A and row-major dense X [ncols, k] (oracle/ir/spmm.mlir)."""
+def spmm_csr(rowptr, colind=None, values=None, X=None, Y=None, *, nnz: int | None = None,
+             stream=None):
+    """Y = A X for CSR A and row-major dense X [ncols, k] (oracle/ir/spmm.mlir).
+    Also ``spmm_csr(A, X[, Y])`` with A a CUDA ``torch.sparse_csr_tensor``
+    (``torch.sparse.mm(A, X)``); any argument may be a DLPack producer."""
+    if _is_csr(rowptr):
+        A, X, Y = rowptr, colind, values
+        rowptr, colind, values = _csr_parts(A)
+        if nnz is None:
+            nnz = A.values().numel()
+    rowptr, colind, values, X, Y = (_from_dlpack(t) for t in (rowptr, colind, values, X, Y))
     for t, n in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (X, "X")):
         _dev(t, n)
     if X.dim() != 2:
@@ -162,7 +205,7 @@ def spmm_csr(rowptr, colind, values, X, Y=None, *, nnz: int | None = None, strea
     k = X.shape[1]
     if Y is None:
         Y = torch.empty((nrows, k), dtype=values.dtype, device=values.device)
-    _dev(Y, "Y")
+    Y = _dev(Y, "Y")
     _check_values(values, X, Y)
     if tuple(Y.shape) != (nrows, k):
         raise BackendError(f"Y has shape {tuple(Y.shape)}, expected {(nrows, k)}", _capi.ERR_ARG)
@@ -177,7 +220,7 @@ def spmm_csr(rowptr, colind, values, X, Y=None, *, nnz: int | None = None, strea
 
 def gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
     """C = A B (LAPIS::gemm, runtime_header.py:249-266; linalg.matmul)."""
-    _dev(A, "A"); _dev(B, "B")
+    A = _dev(A, "A"); B = _dev(B, "B")
     if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0]:
         raise BackendError(f"matmul shape mismatch {tuple(A.shape)} x {tuple(B.shape)}",
                            _capi.ERR_ARG)
@@ -187,7 +230,7 @@ def gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
     n = B.shape[1]
     if C_out is None:
         C_out = torch.empty((m, n), dtype=A.dtype, device=A.device)
-    _dev(C_out, "C")
+    C_out = _dev(C_out, "C")
     if tuple(C_out.shape) != (m, n) or C_out.dtype != A.dtype:
         raise BackendError("C has the wrong shape or dtype", _capi.ERR_ARG)
     check(_capi.lib().lapis_b200_gemm(m, n, k, _ptr(A), k, _ptr(B), n, _ptr(C_out), n,
@@ -197,14 +240,14 @@ def gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
 
 def batch_gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
     """C[b] = A[b] B[b] (linalg.batch_matmul, interp.py:746-763)."""
-    _dev(A, "A"); _dev(B, "B")
+    A = _dev(A, "A"); B = _dev(B, "B")
     if A.dim() != 3 or B.dim() != 3 or A.shape[0] != B.shape[0] or A.shape[2] != B.shape[1]:
         raise BackendError("batch_matmul shape mismatch", _capi.ERR_ARG)
     nb, m, k = A.shape
     n = B.shape[2]
     if C_out is None:
         C_out = torch.empty((nb, m, n), dtype=A.dtype, device=A.device)
-    _dev(C_out, "C")
+    C_out = _dev(C_out, "C")
     check(_capi.lib().lapis_b200_batch_gemm(nb, m, n, k, _ptr(A), _ptr(B), _ptr(C_out),
                                             _dtype(A, "A"), _MODES[mode], _stream(stream)),
           "batch_gemm")
@@ -213,13 +256,13 @@ def batch_gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
 
 def gemv(A, x, y=None, *, stream=None):
     """y = A x (LAPIS::gemv, runtime_header.py:268-282; linalg.matvec)."""
-    _dev(A, "A"); _dev(x, "x")
+    A = _dev(A, "A"); x = _dev(x, "x")
     if A.dim() != 2 or x.dim() != 1 or A.shape[1] != x.shape[0]:
         raise BackendError("matvec shape mismatch", _capi.ERR_ARG)
     m, n = A.shape
     if y is None:
         y = torch.empty(m, dtype=A.dtype, device=A.device)
-    _dev(y, "y")
+    y = _dev(y, "y")
     check(_capi.lib().lapis_b200_gemv(m, n, _ptr(A), n, _ptr(x), _ptr(y), _dtype(A, "A"),
                                       _stream(stream)), "gemv")
     return y
@@ -227,13 +270,13 @@ def gemv(A, x, y=None, *, stream=None):
 
 def reduce2d(src, axis: int, combiner: str = "add", out=None, *, stream=None):
     """linalg.reduce over one axis of a rank-2 array (interp.py:779-795)."""
-    _dev(src, "src")
+    src = _dev(src, "src")
     if src.dim() != 2:
         raise BackendError("reduce2d expects a rank-2 source", _capi.ERR_ARG)
     rows, cols = src.shape
     if out is None:
         out = torch.empty(rows if axis == 1 else cols, dtype=src.dtype, device=src.device)
-    _dev(out, "out")
+    out = _dev(out, "out")
     check(_capi.lib().lapis_b200_reduce_2d(rows, cols, _ptr(src), _ptr(out), axis,
                                            _COMBINERS[combiner], _dtype(src, "src"),
                                            _stream(stream)), "reduce_2d")
@@ -242,10 +285,10 @@ def reduce2d(src, axis: int, combiner: str = "add", out=None, *, stream=None):
 
 def relu(x, y=None, *, stream=None):
     """y = (x > 0) ? x : 0 (linalg.elementwise cmpf ogt + select)."""
-    _dev(x, "x")
+    x = _dev(x, "x")
     if y is None:
         y = torch.empty_like(x)
-    _dev(y, "y")
+    y = _dev(y, "y")
     check(_capi.lib().lapis_b200_relu(x.numel(), _ptr(x), _ptr(y), _dtype(x, "x"),
                                       _stream(stream)), "relu")
     return y
@@ -255,7 +298,14 @@ def gcn_layer(rowptr, colind, values, X, W, H=None, *, nnz: int | None = None, s
               exact: bool = False):
     """H = relu((A_hat X) W) — config 4 (oracle/ir/gcn_f32.mlir).  The SpMM stage
     sums in the reference order; the dense stage runs on the tensor cores
-    (3xTF32, within 1e-5) unless ``exact`` (reference order: bit-identical)."""
+    (3xTF32, within 1e-5) unless ``exact`` (reference order: bit-identical).
+    A torch.sparse_csr_tensor may be passed for rowptr with colind = values =
+    None; any argument may be a DLPack producer."""
+    if _is_csr(rowptr):
+        rowptr, colind, values = _csr_parts(rowptr)
+        if nnz is None:
+            nnz = values.numel()
+    rowptr, colind, values, X, W, H = (_from_dlpack(t) for t in (rowptr, colind, values, X, W, H))
     for t, nm in ((rowptr, "rowptr"), (colind, "colind"), (values, "values"), (X, "X"), (W, "W")):
         _dev(t, nm)
     if X.dim() != 2 or W.dim() != 2 or X.shape[1] != W.shape[0]:
@@ -263,7 +313,7 @@ def gcn_layer(rowptr, colind, values, X, W, H=None, *, nnz: int | None = None, s
     nrows = rowptr.numel() - 1
     if H is None:
         H = torch.empty((nrows, W.shape[1]), dtype=values.dtype, device=values.device)
-    _dev(H, "H")
+    H = _dev(H, "H")
     if not (values.dtype == X.dtype == W.dtype == H.dtype):
         raise BackendError("gcn: element types must match", _capi.ERR_ARG)
     if nnz is None:
@@ -284,7 +334,7 @@ def synth_stencil(points: int, n: int, row_begin: int = 0, row_end: int | None =
     row_end = N if row_end is None else row_end
     rows = row_end - row_begin
     rowptr = torch.empty(rows + 1, dtype=torch.int64, device=device)
-    _dev(rowptr, "rowptr")
+    rowptr = _dev(rowptr, "rowptr")
     check(_capi.lib().lapis_b200_synth_stencil(points, n, row_begin, row_end, _ptr(rowptr), None,
                                                None, _stream(stream)), "synth_stencil(rowptr)")
     nnz = int(rowptr[-1].item())
