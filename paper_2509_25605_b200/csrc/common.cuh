@@ -232,6 +232,39 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// Ordered read-only loads: asm volatile statements keep their program order,
+// so a batch of these is ISSUED in the order written (all index loads of a
+// batch, then all gathers) instead of being interleaved by the scheduler with
+// the loads that depend on them; a predicated-off load returns 0.
+template <class T> __device__ __forceinline__ T ld_ord(const T* p, bool pred);
+template <> __device__ __forceinline__ double ld_ord<double>(const double* p, bool pred) {
+  double v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
+               "@q ld.global.nc.f64 %0, [%1];\n\t}" : "=d"(v) : "l"(p), "r"((int)pred));
+  return v;
+}
+template <> __device__ __forceinline__ float ld_ord<float>(const float* p, bool pred) {
+  float v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f32 %0, 0f00000000;\n\t"
+               "@q ld.global.nc.f32 %0, [%1];\n\t}" : "=f"(v) : "l"(p), "r"((int)pred));
+  return v;
+}
+template <> __device__ __forceinline__ long long ld_ord<long long>(const long long* p, bool pred) {
+  long long v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b64 %0, 0;\n\t"
+               "@q ld.global.nc.b64 %0, [%1];\n\t}" : "=l"(v) : "l"(p), "r"((int)pred));
+  return v;
+}
+template <> __device__ __forceinline__ long ld_ord<long>(const long* p, bool pred) {
+  return (long)ld_ord<long long>(reinterpret_cast<const long long*>(p), pred);
+}
+template <> __device__ __forceinline__ int ld_ord<int>(const int* p, bool pred) {
+  int v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t"
+               "@q ld.global.nc.b32 %0, [%1];\n\t}" : "=r"(v) : "l"(p), "r"((int)pred));
+  return v;
+}
+
 template <class T> __device__ __forceinline__ T ld_hint(const T* p, uint64_t pol);
 template <> __device__ __forceinline__ double ld_hint<double>(const double* p, uint64_t pol) {
   double v;

@@ -29,7 +29,7 @@
 
 namespace lapis_b200 {
 
-constexpr int GD_BM = 128, GD_K = 64, GD_STAGES = 3, GD_THREADS = 160;
+constexpr int GD_BM = 128, GD_K = 64, GD_STAGES = 3, GD_COMPUTE = 256, GD_THREADS = GD_COMPUTE + 32;
 constexpr uint32_t GD_TILE_BYTES = GD_BM * GD_K * 4;  // 32 KB: two 128 x 32 boxes
 constexpr int GD_NMAX = 64;
 constexpr uint32_t GD_B_BYTES = GD_NMAX * GD_K * 4;   // 16 KB per split half
@@ -69,8 +69,30 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void bar_compute() {  // warps 0-3 only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void bar_compute() {  // warps 0-7 only
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void tmem_ld_x16_nowait(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 template <int N>
@@ -79,8 +101,7 @@ gcn_dense_tf32x3_kernel(const __grid_constant__ CUtensorMap tT, const __grid_con
                         const float* __restrict__ W, int64_t ldw, int ntiles) {
   static_assert(N == 32 || N == 64, "fout must be 32 or 64");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring = smem;                                        // [STAGES][32 KB]
   uint8_t* tail = ring + GD_STAGES * GD_TILE_BYTES;            // 32 KB
   uint8_t* bhi = tail + GD_TILE_BYTES;                         // N x 64 K-major
@@ -117,7 +138,7 @@ gcn_dense_tf32x3_kernel(const __grid_constant__ CUtensorMap tT, const __grid_con
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
 
-  if (warp == 4) {
+  if (warp == GD_COMPUTE / 32) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int s = 0;
@@ -134,7 +155,10 @@ gcn_dense_tf32x3_kernel(const __grid_constant__ CUtensorMap tT, const __grid_con
   } else {
     // --------------------------------------- split, MMA issue, epilogue
     constexpr uint32_t idesc = tf32_idesc_gd(GD_BM, N);
-    const int row = warp * 32 + lane;   // the TMEM lane / tile row this thread drains
+    const int lq = warp & 3, half = warp >> 2;
+    const int row = lq * 32 + lane;     // the TMEM lane / tile row this thread drains
+    const uint32_t stage_u = smem_u32(stage_h);
+    const uint32_t tail_u = smem_u32(tail);
     int s = 0;
     uint32_t ph = 0;
     int i = 0;
@@ -143,21 +167,25 @@ gcn_dense_tf32x3_kernel(const __grid_constant__ CUtensorMap tT, const __grid_con
       // previous TMA store must have finished reading the staging buffer
       if (threadIdx.x == 0) bulk_wait_read0();
       bar_compute();
-      const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * N);
+      // warp w drains TMEM lanes 32*(w%4).. (its row quarter), columns of half w/4
+      constexpr int NH = N / 2;
+      const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + (uint32_t)(acc * N + half * NH);
+      uint32_t v[NH / 16][16];
 #pragma unroll
-      for (int c0 = 0; c0 < N; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_x16(tbase + (uint32_t)c0, v);
+      for (int c = 0; c < NH / 16; ++c) tmem_ld_x16_nowait(tbase + (uint32_t)(c * 16), v[c]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < NH / 16; ++c) {
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
           float4 o;
           float* op = reinterpret_cast<float*>(&o);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float x = __uint_as_float(v[q + e]);
+            const float x = __uint_as_float(v[c][q + e]);
             op[e] = (x > 0.0f) ? x : 0.0f;   // cmpf ogt + select: NaN and -0.0 map to +0
           }
-          *reinterpret_cast<float4*>(stage_h + sw128_off(row, c0 + q, GD_BM)) = o;
+          sts128(stage_u + sw128_off(row, half * NH + c * 16 + q, GD_BM), o);
         }
       }
       tc_fence_before();
@@ -175,14 +203,14 @@ gcn_dense_tf32x3_kernel(const __grid_constant__ CUtensorMap tT, const __grid_con
       if (i > 0) mbar_wait(&mma_done, (uint32_t)((i - 1) & 1));   // tail buffer free, acc ready
       // split the tile in place: head over T, tail into `tail` (same layout)
       uint8_t* a = ring + s * GD_TILE_BYTES;
-#pragma unroll 4
-      for (int q = threadIdx.x; q < (int)(GD_TILE_BYTES / 16); q += 128) {
-        float4 x = reinterpret_cast<float4*>(a)[q];
-        float4 h = make_float4(tf32_head(x.x), tf32_head(x.y), tf32_head(x.z), tf32_head(x.w));
-        reinterpret_cast<float4*>(a)[q] = h;
-        reinterpret_cast<float4*>(tail)[q] =
-            make_float4(tf32_head(x.x - h.x), tf32_head(x.y - h.y), tf32_head(x.z - h.z),
-                        tf32_head(x.w - h.w));
+      const uint32_t a_u = smem_u32(a);
+#pragma unroll
+      for (int q = threadIdx.x; q < (int)(GD_TILE_BYTES / 16); q += GD_COMPUTE) {
+        const float4 x = lds128(a_u + q * 16);
+        const float4 h = make_float4(tf32_head(x.x), tf32_head(x.y), tf32_head(x.z), tf32_head(x.w));
+        sts128(a_u + q * 16, h);
+        sts128(tail_u + q * 16, make_float4(tf32_head(x.x - h.x), tf32_head(x.y - h.y),
+                                            tf32_head(x.z - h.z), tf32_head(x.w - h.w)));
       }
       fence_async_smem();
       tc_fence_before();
