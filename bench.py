@@ -720,7 +720,10 @@ class PowerLawSpmm(Workload):
         else:
             self.rowptr, self.colind, self.values = rowptr, colind, values
         self.nnz = int(self.rowptr[-1].item())
-        self.op = sharded.RowBlockSpmm(self.rowptr, self.colind, self.values, n, k, rank, world)
+        # an SpMM plan pins the most referenced X rows in L2 (LAPIS_BENCH_SPMM_PLAN=0: off)
+        self.use_plan = os.environ.get("LAPIS_BENCH_SPMM_PLAN", "1") == "1"
+        self.op = sharded.RowBlockSpmm(self.rowptr, self.colind, self.values, n, k, rank, world,
+                                       plan=self.use_plan)
         self.op.x_local.copy_(torch.from_numpy(X_host[self.r0:self.r1]))
         self.op.gather()
         self.X = self.op.X_full[:n]
@@ -733,6 +736,7 @@ class PowerLawSpmm(Workload):
     def extra_config(self):
         return {"nnz": self.nnz_global_, "max_row": self.max_len, "median_row": self.median_len,
                 "l2": "inputs >> L2",
+                "spmm_plan": self.op.plan.info() if self.op.plan is not None else None,
                 **({"gather": f"NCCL all-gather of X ({self.op.gather_bytes / 1e9:.2f} GB "
                               "received per rank per step) then the local SpMM"}
                    if self.world > 1 else {})}

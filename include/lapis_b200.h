@@ -206,6 +206,29 @@ int lapis_b200_reduce_2d(int64_t rows, int64_t cols, const void* src, void* out,
  * interp.py:520-545, 766-776). */
 int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream);
 
+/* ------------------------------------------------------------- SpMM plans
+ * Structure-only analysis for repeated Y = A X on one CSR structure with a new
+ * dense X every call (config 3, the GCN's features).  The plan counts how
+ * often each X row is referenced, keeps a remapped private copy of colind and
+ * a buffer for the most referenced rows (hot_bytes: 0 = 64 MB, capped by the
+ * device's persisting-L2 limit); every lapis_b200_spmm_csr_plan call copies
+ * those rows of X into the buffer, pins it in L2 (persisting access-policy
+ * window on the stream for the call) and runs the SpMM with hot rows read from
+ * it.  Same results as lapis_b200_spmm_csr (per-row order unchanged).  The
+ * caller's rowptr / colind must stay as they were at plan creation. */
+typedef void* lapis_b200_spmm_plan;
+int lapis_b200_spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k,
+                                const void* rowptr, int rowptr_bytes, const void* colind,
+                                int colind_bytes, int dtype, int64_t hot_bytes, void* stream,
+                                lapis_b200_spmm_plan* out);
+/* out4 = {hot rows, entries reading a hot row, persisting bytes granted, nnz} */
+int lapis_b200_spmm_plan_info(lapis_b200_spmm_plan plan, int64_t* out4);
+int lapis_b200_spmm_plan_destroy(lapis_b200_spmm_plan plan);
+int lapis_b200_spmm_csr_plan(lapis_b200_spmm_plan plan, const void* rowptr, int rowptr_bytes,
+                             const void* colind, int colind_bytes, const void* values,
+                             const void* X, int64_t ldx, void* Y, int64_t ldy, int dtype,
+                             void* stream);
+
 /* ---------------------------------------------------------------- GCN layer
  * H = relu((A_hat X) W): config 4, the reference's one-function GCN
  * (oracle/ir/gcn_f32.mlir: loop-nest SpMM + linalg.matmul + linalg.elementwise

@@ -13,8 +13,8 @@ There is no CPU fallback: without the built library or a CUDA device every
 call raises ``BackendError``.
 """
 from ._capi import BackendError, library_path
-from .kernels import (CsrPlan, batch_gemm, csr_vector_length, gcn_layer, gemm, gemv, reduce2d,
+from .kernels import (CsrPlan, SpmmPlan, batch_gemm, csr_vector_length, gcn_layer, gemm, gemv, reduce2d,
                       relu, spmm_csr, spmv_csr, synth_stencil)
 
-__all__ = ["BackendError", "CsrPlan", "batch_gemm", "csr_vector_length", "gcn_layer", "gemm", "gemv",
+__all__ = ["BackendError", "CsrPlan", "SpmmPlan", "batch_gemm", "csr_vector_length", "gcn_layer", "gemm", "gemv",
            "library_path", "reduce2d", "relu", "spmm_csr", "spmv_csr", "synth_stencil"]

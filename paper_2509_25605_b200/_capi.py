@@ -63,6 +63,12 @@ _SIGNATURES = {
     "lapis_b200_relu": ([_I64, _VP, _VP, _INT, _VP], _INT),
     "lapis_b200_gcn_layer": ([_I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP, _I64,
                               _VP, _INT, _VP], _INT),
+    "lapis_b200_spmm_plan_create": ([_I64, _I64, _I64, _I64, _VP, _INT, _VP, _INT, _INT, _I64, _VP,
+                                     C.POINTER(_VP)], _INT),
+    "lapis_b200_spmm_plan_info": ([_VP, C.POINTER(_I64)], _INT),
+    "lapis_b200_spmm_plan_destroy": ([_VP], _INT),
+    "lapis_b200_spmm_csr_plan": ([_VP, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP, _I64, _INT, _VP],
+                                 _INT),
     "lapis_b200_graph_kernels": ([_VP, C.c_char_p, _I64, C.POINTER(_I64)], _INT),
     "lapis_b200_gcn_layer_mode": ([_I64, _I64, _I64, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP,
                                    _I64, _VP, _INT, _INT, _VP], _INT),

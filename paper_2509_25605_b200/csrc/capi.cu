@@ -49,6 +49,12 @@ int relu(int64_t, const void*, void*, int, cudaStream_t);
 int gcn_layer(int64_t, int64_t, int64_t, const void*, int, const void*, int, const void*,
               const void*, int64_t, const void*, int64_t, void*, int, int, cudaStream_t);
 int synth_stencil(int, int64_t, int64_t, int64_t, int64_t*, int32_t*, double*, cudaStream_t);
+int spmm_plan_create(int64_t, int64_t, int64_t, int64_t, const void*, int, const void*, int, int,
+                     int64_t, cudaStream_t, void**);
+int spmm_plan_info(void*, int64_t*);
+int spmm_plan_destroy(void*);
+int spmm_csr_plan(void*, const void*, int, const void*, int, const void*, const void*, int64_t,
+                  void*, int64_t, int, cudaStream_t);
 void release_workspaces();
 
 }  // namespace lapis_b200
@@ -131,6 +137,7 @@ int lapis_b200_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* r
                         int rowptr_bytes, const void* colind, int colind_bytes,
                         const void* values, const void* x, void* y, int dtype,
                         int vector_length, void* stream) {
+  LB_RANGE("lapis_b200_spmv_csr");
   keep_pool_memory();
   return spmv_csr(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, x, y,
                   dtype, vector_length, S(stream));
@@ -138,6 +145,7 @@ int lapis_b200_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* r
 
 int lapis_b200_csr_plan_create(int64_t nrows, int64_t nnz, const void* rowptr, int rowptr_bytes,
                                void* stream, lapis_b200_csr_plan* out_plan) {
+  LB_RANGE("lapis_b200_csr_plan_create");
   keep_pool_memory();
   return csr_plan_create(nrows, nnz, rowptr, rowptr_bytes, S(stream),
                          reinterpret_cast<void**>(out_plan));
@@ -156,6 +164,7 @@ int lapis_b200_csr_plan_set_exact(lapis_b200_csr_plan plan, int exact) {
 int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int rowptr_bytes,
                              const void* colind, int colind_bytes, const void* values,
                              const void* x, void* y, int dtype, void* stream) {
+  LB_RANGE("lapis_b200_spmv_csr_plan");
   return spmv_csr_plan(plan, rowptr, rowptr_bytes, colind, colind_bytes, values, x, y, dtype,
                        S(stream));
 }
@@ -164,19 +173,47 @@ int lapis_b200_spmm_csr(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, co
                         int rowptr_bytes, const void* colind, int colind_bytes,
                         const void* values, const void* X, int64_t ldx, void* Y, int64_t ldy,
                         int dtype, void* stream) {
+  LB_RANGE("lapis_b200_spmm_csr");
   keep_pool_memory();
   return spmm_csr(nrows, ncols, nnz, k, rowptr, rowptr_bytes, colind, colind_bytes, values, X,
                   ldx, Y, ldy, dtype, S(stream));
 }
 
+int lapis_b200_spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k,
+                                 const void* rowptr, int rowptr_bytes, const void* colind,
+                                 int colind_bytes, int dtype, int64_t hot_bytes, void* stream,
+                                 lapis_b200_spmm_plan* out) {
+  LB_RANGE("lapis_b200_spmm_plan_create");
+  keep_pool_memory();
+  return spmm_plan_create(nrows, ncols, nnz, k, rowptr, rowptr_bytes, colind, colind_bytes, dtype,
+                          hot_bytes, S(stream), out);
+}
+
+int lapis_b200_spmm_plan_info(lapis_b200_spmm_plan plan, int64_t* out4) {
+  return spmm_plan_info(plan, out4);
+}
+
+int lapis_b200_spmm_plan_destroy(lapis_b200_spmm_plan plan) { return spmm_plan_destroy(plan); }
+
+int lapis_b200_spmm_csr_plan(lapis_b200_spmm_plan plan, const void* rowptr, int rowptr_bytes,
+                             const void* colind, int colind_bytes, const void* values,
+                             const void* X, int64_t ldx, void* Y, int64_t ldy, int dtype,
+                             void* stream) {
+  LB_RANGE("lapis_b200_spmm_csr_plan");
+  return spmm_csr_plan(plan, rowptr, rowptr_bytes, colind, colind_bytes, values, X, ldx, Y, ldy,
+                       dtype, S(stream));
+}
+
 int lapis_b200_gemm(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
                     int64_t ldb, void* C, int64_t ldc, int dtype, int mode, void* stream) {
+  LB_RANGE("lapis_b200_gemm");
   keep_pool_memory();
   return gemm_dispatch(1, m, n, k, A, lda, B, ldb, C, ldc, 0, 0, 0, dtype, mode, S(stream));
 }
 
 int lapis_b200_gemv(int64_t m, int64_t n, const void* A, int64_t lda, const void* x, void* y,
                     int dtype, void* stream) {
+  LB_RANGE("lapis_b200_gemv");
   if (m < 0 || n < 0 || lda < n) return fail(LAPIS_B200_ERR_ARG, "gemv: bad extents");
   if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "gemv: unsupported dtype");
   if (m > 0 && (!y || (n > 0 && (!A || !x)))) return fail(LAPIS_B200_ERR_ARG, "gemv: null operand");
@@ -185,6 +222,7 @@ int lapis_b200_gemv(int64_t m, int64_t n, const void* A, int64_t lda, const void
 
 int lapis_b200_batch_gemm(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A,
                           const void* B, void* C, int dtype, int mode, void* stream) {
+  LB_RANGE("lapis_b200_batch_gemm");
   keep_pool_memory();
   if (batch < 0) return fail(LAPIS_B200_ERR_ARG, "batch_gemm: negative batch");
   return gemm_dispatch(batch, m, n, k, A, k, B, n, C, n, m * k, k * n, m * n, dtype, mode,
@@ -193,6 +231,7 @@ int lapis_b200_batch_gemm(int64_t batch, int64_t m, int64_t n, int64_t k, const 
 
 int lapis_b200_reduce_2d(int64_t rows, int64_t cols, const void* src, void* out, int axis,
                          int combiner, int dtype, void* stream) {
+  LB_RANGE("lapis_b200_reduce_2d");
   if (rows < 0 || cols < 0) return fail(LAPIS_B200_ERR_ARG, "reduce: negative extent");
   if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "reduce: unsupported dtype");
   if ((rows > 0 && cols > 0 && !src) || ((axis == 1 ? rows : cols) > 0 && !out))
@@ -201,6 +240,7 @@ int lapis_b200_reduce_2d(int64_t rows, int64_t cols, const void* src, void* out,
 }
 
 int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream) {
+  LB_RANGE("lapis_b200_relu");
   if (n < 0) return fail(LAPIS_B200_ERR_ARG, "relu: negative extent");
   if (n > 0 && (!x || !y)) return fail(LAPIS_B200_ERR_ARG, "relu: null operand");
   return relu(n, x, y, dtype, S(stream));
@@ -210,6 +250,7 @@ int lapis_b200_gcn_layer(int64_t nrows, int64_t ncols, int64_t nnz, const void* 
                          int rowptr_bytes, const void* colind, int colind_bytes, const void* values,
                          const void* X, int64_t fin, const void* W, int64_t fout, void* H,
                          int dtype, void* stream) {
+  LB_RANGE("lapis_b200_gcn_layer");
   keep_pool_memory();
   return gcn_layer(nrows, ncols, nnz, rowptr, rowptr_bytes, colind, colind_bytes, values, X, fin,
                    W, fout, H, LAPIS_B200_GEMM_AUTO, dtype, S(stream));
@@ -219,6 +260,7 @@ int lapis_b200_gcn_layer_mode(int64_t nrows, int64_t ncols, int64_t nnz, const v
                               int rowptr_bytes, const void* colind, int colind_bytes,
                               const void* values, const void* X, int64_t fin, const void* W,
                               int64_t fout, void* H, int mode, int dtype, void* stream) {
+  LB_RANGE("lapis_b200_gcn_layer_mode");
   keep_pool_memory();
   if (mode != LAPIS_B200_GEMM_AUTO && mode != LAPIS_B200_GEMM_EXACT)
     return fail(LAPIS_B200_ERR_ARG, "gcn: mode must be AUTO or EXACT");
@@ -228,6 +270,7 @@ int lapis_b200_gcn_layer_mode(int64_t nrows, int64_t ncols, int64_t nnz, const v
 
 int lapis_b200_synth_stencil(int points, int64_t n, int64_t row_begin, int64_t row_end,
                              int64_t* rowptr, int32_t* colind, double* values, void* stream) {
+  LB_RANGE("lapis_b200_synth_stencil");
   keep_pool_memory();
   return synth_stencil(points, n, row_begin, row_end, rowptr, colind, values, S(stream));
 }

@@ -1,6 +1,8 @@
 // common.cuh — shared helpers for the sm_100a kernels behind include/lapis_b200.h.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdlib>
 
 #include <cuda_runtime.h>
@@ -10,6 +12,16 @@
 #include "../../include/lapis_b200.h"
 
 namespace lapis_b200 {
+
+// NVTX range around each C-ABI entry point (visible in nsys / ncu --nvtx;
+// header-only NVTX v3: a no-op unless a tool injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define LB_RANGE(name) ::lapis_b200::NvtxRange lb_nvtx_range_(name)
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string& msg);

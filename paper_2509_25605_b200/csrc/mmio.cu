@@ -220,6 +220,7 @@ int lapis_b200_mm_info(const char* path, int64_t* out4) {
 // file order (Matrix Market files do not repeat coordinates).
 int lapis_b200_mm_read_csr(const char* path, int64_t* rowptr, void* colind, int colind_bytes,
                            double* values) {
+  LB_RANGE("lapis_b200_mm_read_csr");
   if (!path || !rowptr || !colind) return fail(LAPIS_B200_ERR_ARG, "mm_read_csr: null argument");
   if (colind_bytes != 4 && colind_bytes != 8)
     return fail(LAPIS_B200_ERR_ARG, "mm_read_csr: colind_bytes must be 4 or 8");

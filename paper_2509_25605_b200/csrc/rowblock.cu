@@ -310,6 +310,7 @@ int lapis_b200_rowblock_create(void* comm, int rank, int world, const int64_t* r
                                const void* rowptr, int rowptr_bytes, const void* colind,
                                int colind_bytes, int64_t nnz, int exact, void* stream,
                                lapis_b200_rowblock* out) {
+  LB_RANGE("lapis_b200_rowblock_create");
   if (!out) return fail(LAPIS_B200_ERR_ARG, "rowblock_create: null out");
   *out = nullptr;
   if (world < 1 || world > RB_MAX_WORLD || rank < 0 || rank >= world || !row_begins || !rowptr ||
@@ -395,6 +396,7 @@ int lapis_b200_rowblock_info(lapis_b200_rowblock handle, int64_t* out) {
 int lapis_b200_spmv_csr_rowblock(lapis_b200_rowblock handle, const void* rowptr, int rowptr_bytes,
                                  const void* colind, int colind_bytes, const void* values,
                                  void* x_full, void* y_local, int dtype, void* stream) {
+  LB_RANGE("lapis_b200_spmv_csr_rowblock");
   auto* h = reinterpret_cast<RowBlockImpl*>(handle);
   if (!h) return fail(LAPIS_B200_ERR_ARG, "spmv_rowblock: null handle");
   if (!valid_dtype(dtype)) return fail(LAPIS_B200_ERR_ARG, "spmv_rowblock: unsupported dtype");

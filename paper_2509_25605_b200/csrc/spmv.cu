@@ -357,37 +357,24 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
       int64_t e = (int64_t)rowptr[row + 1];
       if (e < b) e = b;  // interp.py:808 range(begin, max(begin, end))
       if constexpr (EXACT) {
-        // batches of MS steps: all MS colind loads, then all MS x gathers, are
-        // issued before the first fold, so a short row costs two memory round
-        // trips instead of one per two steps; the fold then adds the batch's
-        // products in ascending j (in-group shuffles)
-        constexpr int MS = VL >= 8 ? 4 : 8;
-        for (int64_t j0 = b; j0 < e; j0 += (int64_t)MS * VL) {
-          CI cc[MS];
-          T vv[MS], xv[MS];
+        int64_t j0 = b;
+        for (; j0 + VL < e; j0 += 2 * VL) {
+          const int64_t ja = j0 + lane, jb = j0 + VL + lane;
+          const T pa = Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja]));
+          const T pb = jb < e ? Arith<T>::mul(values[jb], __ldg(x + (int64_t)colind[jb])) : T(0);
 #pragma unroll
-          for (int s2 = 0; s2 < MS; ++s2) {
-            const int64_t j = j0 + s2 * VL + lane;
-            cc[s2] = ld_ord(colind + j, j < e);
-          }
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
 #pragma unroll
-          for (int s2 = 0; s2 < MS; ++s2) {
-            const int64_t j = j0 + s2 * VL + lane;
-            vv[s2] = ld_ord(values + j, j < e);
-          }
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pb : __shfl_sync(gmask, pb, s2, VL));
+        }
+        if (j0 < e) {
+          const int64_t ja = j0 + lane;
+          const T pa = ja < e ? Arith<T>::mul(values[ja], __ldg(x + (int64_t)colind[ja])) : T(0);
 #pragma unroll
-          for (int s2 = 0; s2 < MS; ++s2)
-            xv[s2] = ld_ord(x + (int64_t)cc[s2], j0 + s2 * VL + lane < e);
-          T pr[MS];
-#pragma unroll
-          for (int s2 = 0; s2 < MS; ++s2) pr[s2] = Arith<T>::mul(vv[s2], xv[s2]);
-#pragma unroll
-          for (int s2 = 0; s2 < MS; ++s2) {
-            if (j0 + s2 * VL >= e) break;   // uniform within the VL group
-#pragma unroll
-            for (int q = 0; q < VL; ++q)
-              acc = Arith<T>::add(acc, VL == 1 ? pr[s2] : __shfl_sync(gmask, pr[s2], q, VL));
-          }
+          for (int s2 = 0; s2 < VL; ++s2)
+            acc = Arith<T>::add(acc, VL == 1 ? pa : __shfl_sync(gmask, pa, s2, VL));
         }
       } else {
         for (int64_t j = b + lane; j < e; j += VL)

@@ -218,6 +218,61 @@ def spmm_csr(rowptr, colind=None, values=None, X=None, Y=None, *, nnz: int | Non
     return Y
 
 
+class SpmmPlan:
+    """Structure-only analysis for repeated Y = A X on one CSR structure
+    (lapis_b200_spmm_plan_*): the most referenced rows of X are copied every
+    multiply into a compact buffer pinned in L2 (persisting access-policy
+    window) and read there through a remapped private colind.  Same results
+    as spmm_csr.  ``hot_bytes`` 0 = 64 MB (capped by the device's persisting
+    L2 limit)."""
+
+    def __init__(self, rowptr, colind, ncols: int, k: int, dtype=torch.float64, *,
+                 nnz: int | None = None, hot_bytes: int = 0, stream=None):
+        rowptr, colind = _dev(_from_dlpack(rowptr), "rowptr"), _dev(_from_dlpack(colind), "colind")
+        self.nrows = rowptr.numel() - 1
+        self.nnz = int(rowptr[-1].item() - rowptr[0].item()) if nnz is None else int(nnz)
+        self.k, self.dtype = int(k), dtype
+        self.rowptr, self.colind = rowptr, colind
+        handle = C.c_void_p()
+        check(_capi.lib().lapis_b200_spmm_plan_create(
+            self.nrows, int(ncols), self.nnz, self.k, _ptr(rowptr), _idx_bytes(rowptr, "rowptr"),
+            _ptr(colind), _idx_bytes(colind, "colind"), _DTYPES[dtype], int(hot_bytes),
+            _stream(stream), C.byref(handle)), "spmm_plan_create")
+        self._handle = handle
+
+    def info(self) -> dict:
+        out = (C.c_int64 * 4)()
+        check(_capi.lib().lapis_b200_spmm_plan_info(self._handle, out), "spmm_plan_info")
+        return {"hot_rows": int(out[0]), "hot_entries": int(out[1]),
+                "persisting_bytes": int(out[2]), "nnz": int(out[3])}
+
+    def spmm(self, values, X, Y=None, *, stream=None) -> torch.Tensor:
+        values, X, Y = (_from_dlpack(t) for t in (values, X, Y))
+        values, X = _dev(values, "values"), _dev(X, "X")
+        if X.dim() != 2 or X.shape[1] != self.k:
+            raise BackendError(f"X must be [ncols, {self.k}]", _capi.ERR_ARG)
+        if Y is None:
+            Y = torch.empty((self.nrows, self.k), dtype=values.dtype, device=values.device)
+        Y = _dev(Y, "Y")
+        _check_values(values, X, Y)
+        check(_capi.lib().lapis_b200_spmm_csr_plan(
+            self._handle, _ptr(self.rowptr), _idx_bytes(self.rowptr, "rowptr"), _ptr(self.colind),
+            _idx_bytes(self.colind, "colind"), _ptr(values), _ptr(X), X.shape[1], _ptr(Y),
+            Y.shape[1], _dtype(values, "values"), _stream(stream)), "spmm_csr_plan")
+        return Y
+
+    def close(self) -> None:
+        if getattr(self, "_handle", None) is not None and self._handle.value:
+            _capi.lib().lapis_b200_spmm_plan_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def gemm(A, B, C_out=None, *, mode: str = "auto", stream=None):
     """C = A B (LAPIS::gemm, runtime_header.py:249-266; linalg.matmul)."""
     A = _dev(A, "A"); B = _dev(B, "B")

@@ -225,7 +225,7 @@ class RowBlockSpmm:
     one GPU)."""
 
     def __init__(self, rowptr: torch.Tensor, colind: torch.Tensor, values: torch.Tensor,
-                 nrows_global: int, k: int, rank: int, world: int, group=None):
+                 nrows_global: int, k: int, rank: int, world: int, group=None, plan: bool = False):
         self.rowptr, self.colind, self.values = rowptr, colind, values
         self.N, self.k, self.rank, self.world, self.group = nrows_global, k, rank, world, group
         self.ranges = equal_row_ranges(nrows_global, world)
@@ -234,6 +234,10 @@ class RowBlockSpmm:
         self.nnz = int(rowptr[-1].item() - rowptr[0].item())
         self.X_full = torch.zeros((world * self.chunk, k), dtype=values.dtype,
                                   device=values.device)
+        self.plan = None
+        if plan and values.is_cuda:
+            from .kernels import SpmmPlan
+            self.plan = SpmmPlan(rowptr, colind, nrows_global, k, values.dtype, nnz=self.nnz)
 
     @property
     def x_local(self) -> torch.Tensor:
@@ -261,6 +265,8 @@ class RowBlockSpmm:
         from .kernels import spmm_csr
         if not replicated:
             self.gather()
+        if self.plan is not None:
+            return self.plan.spmm(self.values, self.X_full[:self.N], Y_local, stream=stream)
         return spmm_csr(self.rowptr, self.colind, self.values, self.X_full[:self.N], Y_local,
                         nnz=self.nnz, stream=stream)
 

@@ -94,3 +94,29 @@ def test_decreasing_rowptr(cuda_device, k, dtype):
     got = Yd[:4000].cpu().numpy()
     assert bits_equal(got, want)
     assert bool((Yd[4000:] == 7.0).all()), "write past Y"
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("hot_mb", [0, 1])
+def test_spmm_plan_hot_rows_bitexact(cuda_device, dtype, hot_mb):
+    """SpmmPlan (hot X rows pinned in L2, remapped colind) gives spmm_csr's bits."""
+    import synth_inputs as S
+    spec = S.PowerLawSpec(60_000, mean=10.0, seed=3)
+    rowptr, colind = S.powerlaw_structure_host(spec)
+    values = S.powerlaw_values(spec, int(rowptr[-1])).astype(dtype)
+    X = np.random.default_rng(4).uniform(-1, 1, (60_000, 64)).astype(dtype)
+    plan = lb.SpmmPlan(cu(rowptr), cu(colind), 60_000, 64,
+                       torch.float64 if dtype == np.float64 else torch.float32,
+                       hot_bytes=hot_mb << 20)
+    info = plan.info()
+    assert info["hot_rows"] > 0 and info["hot_entries"] > 0
+    Xd = cu(X)
+    got = plan.spmm(cu(values), Xd).cpu().numpy()
+    want = lb.spmm_csr(cu(rowptr), cu(colind), cu(values), Xd).cpu().numpy()
+    assert bits_equal(got, want)
+    X2 = np.random.default_rng(5).uniform(-1, 1, (60_000, 64)).astype(dtype)   # new X, same plan
+    got2 = plan.spmm(cu(values), cu(X2)).cpu().numpy()
+    ok, msg = O.diff_outputs([got2], [O.spmm_csr(rowptr, colind, values, X2)],
+                             1e-12 if dtype == np.float64 else 1e-5)
+    assert ok, msg
+    plan.close()
