@@ -534,6 +534,32 @@ class StencilSpmv(Workload):
         y = plan.spmv(ci, v, self.x)
         return bool(torch.equal(y[self.r0:self.r1], self.last_y))
 
+    def launch_floor(self, steps):
+        """Per-step cost of an EMPTY step with the same launch mechanism (one
+        captured CUDA graph holding one of our kernels on 1 element, replayed
+        back to back): the fixed launch / ramp cost inside a ~20 us config-1
+        step.  None unless the steps replay graphs."""
+        if not self.graphs:
+            return None
+        tiny_x = torch.zeros(1, dtype=torch.float64, device="cuda")
+        tiny_y = torch.empty_like(tiny_x)
+        side = torch.cuda.Stream()
+        side.wait_stream(self.stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self.lb.relu(tiny_x, tiny_y, stream=side)
+        self.stream.wait_stream(side)
+        for _ in range(3):
+            g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(self.stream)
+        for _ in range(steps):
+            g.replay()
+        b.record(self.stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / steps
+
     def exact_variant(self, steps):
         """The same multiply with every row folded in the reference order (plan
         exact mode, bit-identical); device-resident throughput."""
@@ -723,7 +749,8 @@ class PowerLawSpmm(Workload):
         # an SpMM plan pins the most referenced X rows in L2 (LAPIS_BENCH_SPMM_PLAN=0: off)
         self.use_plan = os.environ.get("LAPIS_BENCH_SPMM_PLAN", "1") == "1"
         self.op = sharded.RowBlockSpmm(self.rowptr, self.colind, self.values, n, k, rank, world,
-                                       plan=self.use_plan)
+                                       plan=self.use_plan,
+                                       hot_bytes=int(os.environ.get("LAPIS_BENCH_SPMM_HOT_MB", "0")) << 20)
         self.op.x_local.copy_(torch.from_numpy(X_host[self.r0:self.r1]))
         self.op.gather()
         self.X = self.op.X_full[:n]
@@ -1358,6 +1385,7 @@ def measure(wl, args, rank, world, local, steps, warmup, cpu_seconds, with_cpu=T
     tfile = ROOT / "profiles" / f"traffic_{wl.key}.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    floor = wl.launch_floor(steps) if hasattr(wl, "launch_floor") else None
     exact_variant = (wl.exact_variant(max(3, steps // 2))
                      if hasattr(wl, "exact_variant") and not args.vl else None)
     census, census_src = launch_census(wl)
@@ -1384,7 +1412,11 @@ def measure(wl, args, rank, world, local, steps, warmup, cpu_seconds, with_cpu=T
                      {"bound": wl.bound, "achieved": round(achieved, 2), "peak": peak,
                       "unit": punit, "frac": round(achieved / peak, 4), "traffic": traffic,
                       "peak_source": psrc, "kernel": wl.kernel_name(),
-                      "algorithmic_work_per_launch": wl.work_local()}),
+                      "algorithmic_work_per_launch": wl.work_local(),
+                      **({"launch_floor_us": round(floor * 1e6, 3),
+                          "frac_floor_corrected": round(wl.work_local() / max(kern_avg - floor, 1e-9)
+                                                        / scale / peak, 4)}
+                         if floor else {})}),
         "e2e": {"value": round(wl.work_global() / e2e_dt / scale, 3), "unit": wl.unit,
                 "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
                 "ms_per_step": round(e2e_dt * 1e3, 3),

@@ -210,7 +210,7 @@ int lapis_b200_relu(int64_t n, const void* x, void* y, int dtype, void* stream);
  * Structure-only analysis for repeated Y = A X on one CSR structure with a new
  * dense X every call (config 3, the GCN's features).  The plan counts how
  * often each X row is referenced, keeps a remapped private copy of colind and
- * a buffer for the most referenced rows (hot_bytes: 0 = 64 MB, capped by the
+ * a buffer for the most referenced rows (hot_bytes: 0 = 16 MB, capped by the
  * device's persisting-L2 limit); every lapis_b200_spmm_csr_plan call copies
  * those rows of X into the buffer, pins it in L2 (persisting access-policy
  * window on the stream for the call) and runs the SpMM with hot rows read from

@@ -32,11 +32,12 @@ REF_ROOT = Path(os.environ.get("LAPIS_REFERENCE", "/root/reference"))
 REF_PKG = REF_ROOT / "pkg"
 OUT = HERE / "_ref"
 ORACLE_SO = HERE / "liblapis_oracle.so"
-REF_SO = OUT / "liblapis_ref.so"
-# the same objects built with -march=native (SURVEY 8(d) CPU recipe) plus the
-# ISA flags of the build host: oracle/ref.py loads this variant only on a host
-# whose CPU has every one of them (the GPU box's CPU may differ from this one)
-REF_SO_NATIVE = OUT / "liblapis_ref_native.so"
+# -march=native (SURVEY 8(d) CPU recipe) build, recorded with the ISA flags of
+# the build host: oracle/ref.py loads it only on a host whose CPU has every one
+# of them (the GPU box's CPU may differ from this one), else the portable
+# build of the same objects
+REF_SO_NATIVE = OUT / "liblapis_ref.so"
+REF_SO = OUT / "liblapis_ref_portable.so"
 NATIVE_FLAGS = OUT / "native_cpu_flags.txt"
 
 
@@ -108,9 +109,9 @@ def build_reference(force: bool = False) -> Path | None:
     driver = HERE / "ref_driver.cpp"
     deps = [driver, __file__, *(u[1] for u in REF_UNITS)]
     if not force and not _stale(REF_SO, deps) and not _stale(REF_SO_NATIVE, deps):
-        return REF_SO
+        return REF_SO_NATIVE
     runtime_hdr = OUT / "lapis_dualview_runtime.hpp"
-    variants = {REF_SO: [], REF_SO_NATIVE: ["-march=native"]}
+    variants = {REF_SO: [], REF_SO_NATIVE: ["-march=native"]}   # portable, native
     objs = {so: [] for so in variants}
     for name, ir, kind, vt, ct, entry in REF_UNITS:
         lowered = _lapis_cli(["opt", "--sparse-compiler-kokkos", str(ir)])
@@ -130,7 +131,7 @@ def build_reference(force: bool = False) -> Path | None:
     for so in variants:
         _run(["g++", "-shared", "-pthread", "-o", str(so), *objs[so]])
     NATIVE_FLAGS.write_text(" ".join(sorted(cpu_flags())) + "\n")
-    return REF_SO
+    return REF_SO_NATIVE
 
 
 EMITTED = OUT / "emitted"

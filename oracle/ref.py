@@ -19,7 +19,7 @@ _lib = None
 
 
 def available() -> bool:
-    return _build.REF_SO.exists()
+    return _build.REF_SO.exists() or _build.REF_SO_NATIVE.exists()
 
 
 def variant() -> str:
@@ -41,9 +41,9 @@ def compile_flags() -> str:
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
-        if not _build.REF_SO.exists():
+        if not available():
             _build.build_reference()
-        if not _build.REF_SO.exists():
+        if not available():
             raise RuntimeError("reference CPU path not built (needs /root/reference once)")
         so = _build.REF_SO_NATIVE if variant() == "native" else _build.REF_SO
         _lib = C.CDLL(str(so))

@@ -440,6 +440,12 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
     const int64_t my_len = lane < nr ? s_rp[lane + 1] - s_rp[lane] : 0;
     const unsigned long_mask = __ballot_sync(0xffffffffu, my_len > SPLIT);
     for (int64_t c0 = (int64_t)lane * CPL; c0 - (int64_t)lane * CPL < k; c0 += 32 * CPL) {
+      // X rows are addressed as base + col * pitch with one 32x32->64-bit
+      // multiply-add (column index and pitch in bytes both < 2^32)
+      const char* xbase = reinterpret_cast<const char*>(X + c0);
+      const uint32_t ldxb = (uint32_t)(ldx * (int64_t)sizeof(T));
+      const char* hbase = HOT ? reinterpret_cast<const char*>(Xh + c0) : nullptr;
+      const uint32_t ldhb = (uint32_t)(ldh * (int64_t)sizeof(T));
       int ra = 0;
       while (ra < nr) {
         if ((long_mask >> ra) & 1u) { ++ra; continue; }
@@ -448,6 +454,7 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
         const int64_t jb = s_rp[ra], je = s_rp[rb];
         int cur = ra;
         int64_t nxt = s_rp[ra + 1];
+        T* yrow = Y + (r0 + ra) * ldy + c0;
         T acc[CPL];
 #pragma unroll
         for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
@@ -464,30 +471,31 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
               const int pe = t0 + U * PF + (lane % U);
               const CI pa = __shfl_sync(0xffffffffu, my_col, pe & 31);
               const CI pb = __shfl_sync(0xffffffffu, nx_col, pe & 31);
-              const int64_t pc = (int64_t)(pe < 32 ? pa : pb);
+              const CI pc = pe < 32 ? pa : pb;
               const int line = lane / U;
               if (j0 + pe < je && line * (128 / (int)sizeof(T)) < 32 * CPL && (!HOT || pc >= 0))
                 asm volatile("prefetch.global.L2 [%0];" ::
-                             "l"(X + pc * ldx + c0 - lane * CPL + line * (128 / sizeof(T))));
+                             "l"(xbase + (uint64_t)(uint32_t)pc * ldxb +
+                                 (line * 128 - lane * CPL * (int)sizeof(T))));
             }
             CI cols[U];
             T vals[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               cols[u] = __shfl_sync(0xffffffffu, my_col, (t0 + u) & 31);
-              vals[u] = __shfl_sync(0xffffffffu, my_val, (t0 + u) & 31);
+              vals[u] = __shfl_sync(0xffffffffu, my_val, (t0 + u) & 31);   // 0 past the run
             }
             T xv[U][CPL];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               if (t0 + u < cnt) {
-                const T* xr;
+                const char* xr;
                 if constexpr (HOT)
-                  xr = cols[u] >= 0 ? X + (int64_t)cols[u] * ldx + c0
-                                    : Xh + (int64_t)(~cols[u]) * ldh + c0;
+                  xr = cols[u] >= 0 ? xbase + (uint64_t)(uint32_t)cols[u] * ldxb
+                                    : hbase + (uint64_t)(uint32_t)(~cols[u]) * ldhb;
                 else
-                  xr = X + (int64_t)cols[u] * ldx + c0;
-                ldx_row<T, CPL>(xr, xv[u]);
+                  xr = xbase + (uint64_t)(uint32_t)cols[u] * ldxb;
+                ldx_row<T, CPL>(reinterpret_cast<const T*>(xr), xv[u]);
               } else {
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) xv[u][q] = T(0);
@@ -495,25 +503,28 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              if (t0 + u < cnt) {
-                const int64_t j = j0 + t0 + u;
-                while (j == nxt) {   // rows that end here (empty rows included)
-                  sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
+              // past the run: value 0 and X 0, the add of +0.0 leaves the sum
+              // unchanged (a running sum from +0.0 is never -0.0)
+              if (t0 + u < cnt && j0 + t0 + u == nxt) {
+                do {   // rows that end here (empty rows included)
+                  sty_row<T, CPL>(yrow, acc);
 #pragma unroll
                   for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
+                  yrow += ldy;
                   ++cur;
                   nxt = s_rp[cur + 1];
-                }
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(vals[u], xv[u][q]));
+                } while (j0 + t0 + u == nxt);
               }
+#pragma unroll
+              for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(vals[u], xv[u][q]));
             }
           }
           my_col = nx_col;
           my_val = nx_val;
         }
         for (; cur < rb; ++cur) {
-          sty_row<T, CPL>(Y + (r0 + cur) * ldy + c0, acc);
+          sty_row<T, CPL>(yrow, acc);
+          yrow += ldy;
 #pragma unroll
           for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
         }
@@ -1212,7 +1223,9 @@ int spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const
   cudaGetDevice(&p->device);
   const int64_t row_bytes = k * elem_bytes(dtype);
   if (hot_bytes < 0) hot_bytes = 0;
-  if (hot_bytes == 0) hot_bytes = 64ll << 20;
+  // 16 MB measured best on config 3 (8.83 ms vs 9.40 without a plan, 8.99 at 32 MB,
+  // 10.84 at 64 MB: a larger persisting set starves the streamed rest of L2)
+  if (hot_bytes == 0) hot_bytes = 16ll << 20;
   int max_persist = 0;
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, p->device);
   cudaGetLastError();
@@ -1294,7 +1307,8 @@ int spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const
   for (int v = (int)tau; v < NB && tau < (unsigned)NB; ++v) p->hot_entries += (int64_t)h[v] * v;
   // persisting L2 for the hot rows (process-wide limit; never lowered here)
   const size_t want = (size_t)p->nhot * row_bytes;
-  if (want > 0 && max_persist > 0) {
+  const char* wenv = getenv("LAPIS_B200_SPMM_WINDOW");   // A/B runs: 0 = no persisting window
+  if (want > 0 && max_persist > 0 && !(wenv && wenv[0] == '0')) {
     size_t cur = 0;
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
     if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(want, max_persist));

@@ -223,7 +223,7 @@ class SpmmPlan:
     (lapis_b200_spmm_plan_*): the most referenced rows of X are copied every
     multiply into a compact buffer pinned in L2 (persisting access-policy
     window) and read there through a remapped private colind.  Same results
-    as spmm_csr.  ``hot_bytes`` 0 = 64 MB (capped by the device's persisting
+    as spmm_csr.  ``hot_bytes`` 0 = 16 MB (capped by the device's persisting
     L2 limit)."""
 
     def __init__(self, rowptr, colind, ncols: int, k: int, dtype=torch.float64, *,

@@ -225,7 +225,8 @@ class RowBlockSpmm:
     one GPU)."""
 
     def __init__(self, rowptr: torch.Tensor, colind: torch.Tensor, values: torch.Tensor,
-                 nrows_global: int, k: int, rank: int, world: int, group=None, plan: bool = False):
+                 nrows_global: int, k: int, rank: int, world: int, group=None, plan: bool = False,
+                 hot_bytes: int = 0):
         self.rowptr, self.colind, self.values = rowptr, colind, values
         self.N, self.k, self.rank, self.world, self.group = nrows_global, k, rank, world, group
         self.ranges = equal_row_ranges(nrows_global, world)
@@ -237,7 +238,8 @@ class RowBlockSpmm:
         self.plan = None
         if plan and values.is_cuda:
             from .kernels import SpmmPlan
-            self.plan = SpmmPlan(rowptr, colind, nrows_global, k, values.dtype, nnz=self.nnz)
+            self.plan = SpmmPlan(rowptr, colind, nrows_global, k, values.dtype, nnz=self.nnz,
+                                 hot_bytes=hot_bytes)
 
     @property
     def x_local(self) -> torch.Tensor:
