@@ -483,6 +483,137 @@ spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
   }
 }
 
+// ------------------------------------------------------- row-stream kernel
+// Exact (reference-order) SpMV for regular structures, one row per thread.
+// A tile is NT consecutive rows; their contiguous entry range is brought into
+// a ST-deep shared-memory ring by the TMA engine (cp.async.bulk of colind and
+// values, one mbarrier per stage), so no thread waits on the structure stream
+// and every DRAM byte of it moves in 16-byte-aligned bulk transfers.  Thread
+// i folds row r0+i sequentially — colind from shared memory, the x gather
+// (lanes hold consecutive rows: for stencils the 32 gathers of one
+// instruction are consecutive x entries), the product, the ordered add — in
+// chunks of MC entries whose gathers are all issued before the chunk's adds.
+// Small tiles (NT = 64: 21.5 KB per stage for 27-point rows) give five
+// independent CTA pipelines per SM, each with a tile in flight while the
+// previous one folds.  The row sum is the reference's sequential sum bit for
+// bit (interp.py:808-811) whatever the row lengths.  A tile whose entries
+// exceed the stage (irregular rows), or the unaligned tail of the last tile,
+// is read from global memory directly; so is a row whose range lies outside
+// its tile's stream (a decreasing rowptr), clamped to range(begin,
+// max(begin, end)) (interp.py:808).  Shared-memory reads: lane i reads entry
+// b_i + u, b_i = i * len — conflict-free for odd row lengths (27-point).
+template <class T, class CI, int CAP, int ST>
+struct RowStreamSmem {
+  static constexpr int CA = 16 / sizeof(CI), VA = 16 / sizeof(T);
+  static constexpr size_t CI_BYTES = ((CAP + CA) * sizeof(CI) + 127) / 128 * 128;
+  static constexpr size_t V_BYTES = ((CAP + VA) * sizeof(T) + 127) / 128 * 128;
+  static constexpr size_t STAGE_BYTES = CI_BYTES + V_BYTES;
+  static constexpr size_t TOTAL = ST * STAGE_BYTES;
+};
+
+// one row's ordered sum: chunks of MC entries, each chunk's gathers issued
+// before its adds; cp / vp point at the row's first entry (shared or global)
+template <class T, class CI, int MC>
+__device__ __forceinline__ T row_fold(const CI* __restrict__ cp, const T* __restrict__ vp, int n,
+                                      const T* __restrict__ x) {
+  T acc = Arith<T>::zero();
+  for (int q = 0; q < n; q += MC) {
+    int64_t c[MC];
+#pragma unroll
+    for (int u = 0; u < MC; ++u) c[u] = q + u < n ? (int64_t)cp[q + u] : 0;
+    T xv[MC];
+#pragma unroll
+    for (int u = 0; u < MC; ++u) xv[u] = ld_ord<T>(x + c[u], q + u < n);
+#pragma unroll
+    for (int u = 0; u < MC; ++u)
+      if (q + u < n) acc = Arith<T>::add(acc, Arith<T>::mul(vp[q + u], xv[u]));
+  }
+  return acc;
+}
+
+template <class T, class RP, class CI, int NT, int CAP, int ST, int MC>
+__global__ void __launch_bounds__(NT)
+spmv_rowstream_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
+                      const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
+                      int tma_ok, RowGuard guard = RowGuard()) {
+  if (row_guard_skip(guard)) return;
+  constexpr int ROWS = NT;
+  using L = RowStreamSmem<T, CI, CAP, ST>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[ST];
+  __shared__ int64_t meta[ST][2];  // first staged entry of colind / values (aligned down); -1: direct
+  const int tid = threadIdx.x;
+  const int gi = tid;
+  const int64_t ntiles = (nrows + ROWS - 1) / ROWS;
+  auto sci = [&](int st) { return reinterpret_cast<CI*>(smem + st * L::STAGE_BYTES); };
+  auto sv = [&](int st) { return reinterpret_cast<T*>(smem + st * L::STAGE_BYTES + L::CI_BYTES); };
+  const int64_t nnz_end = tid == 0 ? (int64_t)rowptr[nrows] : 0;
+  auto issue = [&](int st, int64_t t) {
+    const int64_t r0 = t * ROWS, r1 = min(nrows, r0 + ROWS);
+    const int64_t s = (int64_t)rowptr[r0], e = (int64_t)rowptr[r1];
+    const int64_t sc = s & ~(int64_t)(L::CA - 1), ec = (e + L::CA - 1) & ~(int64_t)(L::CA - 1);
+    const int64_t sv0 = s & ~(int64_t)(L::VA - 1), ev = (e + L::VA - 1) & ~(int64_t)(L::VA - 1);
+    const bool direct = !tma_ok || e <= s || e - s > CAP || ec > nnz_end || ev > nnz_end;
+    meta[st][0] = direct ? -1 : sc;
+    meta[st][1] = sv0;
+    if (direct) {
+      mbar_arrive(&full[st]);
+    } else {
+      const uint32_t bc = (uint32_t)((ec - sc) * sizeof(CI)), bv = (uint32_t)((ev - sv0) * sizeof(T));
+      mbar_arrive_expect_tx(&full[st], bc + bv);
+      bulk_g2s(sci(st), colind + sc, bc, &full[st]);
+      bulk_g2s(sv(st), values + sv0, bv, &full[st]);
+    }
+  };
+  if (tid == 0) {
+    for (int st = 0; st < ST; ++st) mbar_init(&full[st], 1);
+    fence_barrier_init();
+    for (int st = 0; st < ST; ++st) {
+      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
+      if (t < ntiles) issue(st, t);
+    }
+  }
+  __syncthreads();
+  int64_t t = blockIdx.x;
+  int64_t b = 0, e = 0;
+  if (t < ntiles && t * ROWS + gi < nrows) {
+    b = (int64_t)rowptr[t * ROWS + gi];
+    e = (int64_t)rowptr[t * ROWS + gi + 1];
+  }
+  for (int64_t it = 0; t < ntiles; ++it, t += gridDim.x) {
+    const int st = (int)(it % ST);
+    const int64_t row = t * ROWS + gi;
+    const int64_t tn = t + gridDim.x;
+    int64_t bn = 0, en = 0;
+    if (tn < ntiles && tn * ROWS + gi < nrows) {
+      bn = (int64_t)rowptr[tn * ROWS + gi];
+      en = (int64_t)rowptr[tn * ROWS + gi + 1];
+    }
+    if (e < b) e = b;
+    mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+    const int64_t sc = meta[st][0], sv0 = meta[st][1];
+    const int64_t tile_s = (int64_t)rowptr[t * ROWS];
+    const int64_t tile_e = (int64_t)rowptr[min(nrows, t * ROWS + ROWS)];
+    const bool staged = sc >= 0 && b >= tile_s && e <= tile_e;
+    T acc;
+    if (__all_sync(0xffffffffu, staged || row >= nrows))
+      acc = row_fold<T, CI, MC>(sci(st) + (b - sc), sv(st) + (b - sv0), (int)(e - b), x);
+    else
+      acc = row_fold<T, CI, MC>(colind + b, values + b, (int)(e - b), x);
+    if (row < nrows) y[row] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t tr = t + (int64_t)ST * gridDim.x;
+      if (tr < ntiles) {
+        fence_proxy_async();
+        issue(st, tr);
+      }
+    }
+    b = bn;
+    e = en;
+  }
+}
+
 // structure analysis for the plan: longest row, and whether rowptr is monotone
 // (stats[1] != 0 when some row has rowptr[r+1] < rowptr[r])
 template <class RP>
@@ -515,6 +646,8 @@ struct CsrPlanImpl {
   int exact_vl = 0;             // > 0: regular structure -> vector kernel with this VL
   int exact = 0;                // 1: fp64 / int rows folded in the reference order too
   int warpblock = 0;            // 1: warp-block kernel (irregular monotone structures)
+  int rowstream = 0;            // > 0: row-stream kernel for the reference-order fold (staged entries per row)
+  int rowstream_all = 0;        // 1: row-stream kernel in tree mode too (LAPIS_B200_SPMV_KERNEL=rs)
 };
 
 static int64_t ntiles_for(int64_t nrows, int64_t nnz) {
@@ -586,6 +719,75 @@ static int launch_tile_t(int64_t ntiles, const void* rowptr, const void* colind,
     default: return launch_tile_cfg<T, RP, CI, 256, 4>(ntiles, rowptr, colind, values, x, y, tile_row, st, g);
   }
 }
+
+template <class T, class RP, class CI, int NT, int PER, int ST, int MC>
+static int launch_rowstream_cfg(int64_t nrows, const void* rowptr, const void* colind,
+                                const void* values, const void* x, void* y, cudaStream_t st,
+                                RowGuard guard) {
+  constexpr int ROWS = NT, CAP = ROWS * PER;
+  using L = RowStreamSmem<T, CI, CAP, ST>;
+  auto kern = spmv_rowstream_kernel<T, RP, CI, NT, CAP, ST, MC>;
+  static int configured[64] = {0};
+  static int ctas_per_sm[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!configured[dev]) {
+    LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)L::TOTAL), "smem attr (spmv_rowstream_kernel)"));
+    int c = 0;
+    LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kern, NT, L::TOTAL),
+                      "occupancy"));
+    ctas_per_sm[dev] = c < 1 ? 1 : c;
+    configured[dev] = 1;
+  }
+  const int tma_ok = ((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0);
+  const int64_t ntiles = (nrows + ROWS - 1) / ROWS;
+  int64_t grid = (int64_t)num_sms() * ctas_per_sm[dev];
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
+  // static tile split: CTA b takes tiles b, b + G, ...  (a dynamic counter
+  // with a ring of prefetched tile ids measured slower: 5.11 vs 5.77 TB/s)
+  kern<<<(unsigned)grid, NT, L::TOTAL, st>>>(nrows, (const RP*)rowptr, (const CI*)colind,
+                                             (const T*)values, (const T*)x, (T*)y, tma_ok, guard);
+  return check_launch("spmv_rowstream_kernel");
+}
+
+// staged entries per row class of the row-stream kernel; 0 = not used
+// (rows of <= 14 entries stay on the exact vector kernel: C1's 5-point rows
+// measured 20 us there against 20-88 us for row-stream shapes)
+static int rowstream_per(double mean) {
+  if (mean > 14.0 && mean <= 28.0) return 32;
+  return 0;
+}
+// LAPIS_B200_RS_CFG selects a shape variant for tuning runs (0 = default)
+static int rowstream_cfg() {
+  static int cfg = [] {
+    const char* e = getenv("LAPIS_B200_RS_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return cfg;
+}
+
+template <class T, class RP, class CI>
+struct RowStreamOp {
+  static int run(int per, int64_t nrows, const void* rp, const void* ci, const void* v,
+                 const void* x, void* y, cudaStream_t st, RowGuard g) {
+    // (NT threads = rows per tile, PER staged entries per row, ST stages, MC).
+    // Measured on a 24M-row 27-point stencil (exact): NT = 64, 2 stages
+    // (five CTAs per SM) 5.77 TB/s; NT = 96 5.53; NT = 128 5.09; NT = 256
+    // 4.92; NT = 32 5.2; NT = 64 with 3 stages 3.6, with MC = 8 5.24 (the
+    // vector kernel: tree 5.59, exact 4.72).  Full config 5 (200M rows):
+    // 5.14 TB/s exact vs 4.37 for the exact vector kernel.
+    switch (rowstream_cfg()) {
+      case 1: return launch_rowstream_cfg<T, RP, CI, 32, 28, 2, 16>(nrows, rp, ci, v, x, y, st, g);
+      case 2: return launch_rowstream_cfg<T, RP, CI, 128, 28, 2, 16>(nrows, rp, ci, v, x, y, st, g);
+      default: break;
+    }
+    (void)per;
+    return launch_rowstream_cfg<T, RP, CI, 64, 28, 2, 16>(nrows, rp, ci, v, x, y, st, g);
+  }
+};
 
 template <class T, class RP, class CI, int VL, bool EXACT>
 static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind,
@@ -768,7 +970,13 @@ int spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const void* rowptr, int 
   greg.want = 1;  // regular: exact vector kernel
   gwb.want = 2;   // monotone irregular: warp-block kernel (the plan's choice)
   girr.want = 3;  // decreasing rowptr: exact vector kernel, one row per lane
-  if (rc == LAPIS_B200_OK)
+  // regular: the row-stream kernel (reference order, structure streamed by the
+  // TMA engine) when the mean row fits its stage, else the exact vector kernel
+  const int per = rowstream_per(mean);
+  if (rc == LAPIS_B200_OK && per > 0)
+    rc = dispatch_types<RowStreamOp>(dtype, rp_bytes, ci_bytes, per, nrows, rowptr, colind, values,
+                                     x, y, st, greg);
+  else if (rc == LAPIS_B200_OK)
     rc = dispatch_types<VecExactGuardedOp>(dtype, rp_bytes, ci_bytes, cvl, nrows, rowptr, colind,
                                            values, x, y, st, greg);
   if (rc == LAPIS_B200_OK)
@@ -824,8 +1032,14 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
   const char* kf = getenv("LAPIS_B200_SPMV_KERNEL");
   bool wb = monotone && !force && (!regular || mean < WARPBLOCK_MAX_MEAN);
   if (kf && !strcmp(kf, "wb")) wb = monotone;
-  if (kf && (!strcmp(kf, "vec") || !strcmp(kf, "tile"))) wb = false;
+  if (kf && (!strcmp(kf, "vec") || !strcmp(kf, "tile") || !strcmp(kf, "rs"))) wb = false;
   p->warpblock = wb ? 1 : 0;
+  // row-stream kernel: the reference-order fold of regular monotone structures
+  // (C1, C5 exact, fp32); LAPIS_B200_SPMV_KERNEL = vec keeps the vector kernel
+  const bool vec_forced = kf && !strcmp(kf, "vec");
+  p->rowstream = (monotone && regular && !wb && !vec_forced && !force) ? rowstream_per(mean) : 0;
+  if (kf && !strcmp(kf, "rs") && monotone) p->rowstream = rowstream_per(mean) ? rowstream_per(mean) : 32;
+  p->rowstream_all = (kf && !strcmp(kf, "rs")) ? 1 : 0;
   return LAPIS_B200_OK;
 }
 
@@ -861,7 +1075,7 @@ int csr_plan_info(void* plan, int64_t* out4) {
   out4[0] = p->max_len;
   out4[1] = p->exact_vl;
   out4[2] = p->ntiles;
-  out4[3] = p->exact | (p->warpblock << 1);
+  out4[3] = p->exact | (p->warpblock << 1) | ((p->rowstream > 0) << 2);
   return LAPIS_B200_OK;
 }
 
@@ -890,13 +1104,17 @@ int spmv_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
     return dispatch_types<WarpBlockOp>(dtype, rp_bytes, ci_bytes, p->nrows, rowptr, colind,
                                        values, x, y,
                                        (p->exact || dtype == LAPIS_B200_F32) ? 1 : 0, st);
+  const bool ordered = p->exact || dtype == LAPIS_B200_F32 || p->exact_vl == 1;
+  if (p->rowstream > 0 && (ordered || p->rowstream_all))
+    return dispatch_types<RowStreamOp>(dtype, rp_bytes, ci_bytes, p->rowstream, p->nrows, rowptr,
+                                       colind, values, x, y, st, RowGuard());
   if (p->exact_vl > 0) {
     // fp32 always folds in the reference order (its 1e-5 contract cannot absorb
     // reassociation on long rows); fp64 / ints take the emitted-mapping tree
     // (ThreadVectorRange reduce) unless exact mode was requested
     // (VL = 1: both are the sequential row sum; the exact kernel's two-entry
     // unroll keeps more loads in flight — C1 21.5 vs 26 us measured)
-    if (p->exact || dtype == LAPIS_B200_F32 || p->exact_vl == 1)
+    if (ordered)
       return dispatch_types<VecExactOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,
                                         colind, values, x, y, st);
     return dispatch_types<VecOp>(dtype, rp_bytes, ci_bytes, p->exact_vl, p->nrows, rowptr,

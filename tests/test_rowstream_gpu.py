@@ -1,0 +1,94 @@
+"""The row-stream SpMV kernel (csrc/spmv.cu spmv_rowstream_kernel): the
+reference-order fold of regular structures with the entry stream staged by the
+TMA engine.  Every case is bit-identical to the oracle's sequential row sums
+(interp.py:808-811): stencils (the plan's and the no-plan call's choice),
+forced on ragged rows (tiles larger than a stage fall back to global loads),
+unaligned operands (no bulk copies), an offset rowptr and every value type."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2509_25605_b200 as lb
+from conftest import bits_equal
+from matrices import ragged_csr, stencil_csr
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def _x(rng, n, dtype):
+    if np.issubdtype(dtype, np.integer):
+        return rng.integers(-9, 9, n).astype(dtype)
+    return rng.uniform(-1, 1, n).astype(dtype)
+
+
+@pytest.mark.parametrize("points,n", [(27, 5), (27, 23), (27, 41)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int64, np.int32])
+def test_stencil_plan_exact(cuda_device, points, n, dtype):
+    rowptr, colind, values = stencil_csr(points, n)
+    values = values.astype(dtype)
+    rng = np.random.default_rng(points * 1000 + n)
+    x = _x(rng, rowptr.size - 1, dtype)
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
+    info = plan.info()
+    assert info["rowstream"] and "rowstream" in info["kernel"], info
+    want = O.spmv_csr(rowptr, colind, values, x)
+    assert bits_equal(host(plan.spmv(cu(colind), cu(values), cu(x))), want)
+    # the no-plan call (the emitted C++'s LAPIS::spmv_csr) takes it too
+    assert bits_equal(host(lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x))), want)
+
+
+@pytest.mark.parametrize("nrows", [1, 255, 257, 5000])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_forced_on_ragged_rows(cuda_device, monkeypatch, nrows, dtype):
+    # long rows push a tile past its stage (global-load fallback for that tile)
+    monkeypatch.setenv("LAPIS_B200_SPMV_KERNEL", "rs")
+    rng = np.random.default_rng(nrows)
+    longs = {0: 2400, nrows - 1: 9000} if nrows > 2 else {}
+    rowptr, colind, values = ragged_csr(rng, nrows, 12000, max_len=60, empty_every=7,
+                                        long_rows=longs, dtype=dtype)
+    x = _x(rng, 12000, dtype)
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
+    assert plan.info()["rowstream"], plan.info()
+    want = O.spmv_csr(rowptr, colind, values, x)
+    assert bits_equal(host(plan.spmv(cu(colind), cu(values), cu(x))), want)
+    # forced in tree mode too: still the sequential sum
+    assert bits_equal(host(lb.CsrPlan(cu(rowptr)).spmv(cu(colind), cu(values), cu(x))), want)
+
+
+def test_unaligned_operands_and_offset_rowptr(cuda_device):
+    rowptr, colind, values = stencil_csr(27, 13)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, rowptr.size - 1)
+    want = O.spmv_csr(rowptr, colind, values, x)
+    # colind / values one element into their allocations: no 16-byte alignment
+    ci = torch.cat([torch.zeros(1, dtype=torch.int32), torch.from_numpy(colind)]).cuda()[1:]
+    va = torch.cat([torch.zeros(1, dtype=torch.float64), torch.from_numpy(values)]).cuda()[1:]
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
+    assert bits_equal(host(plan.spmv(ci, va, cu(x))), want)
+    # rowptr starting at 7: the entry stream begins 7 entries into the arrays
+    off = 7
+    rp7 = rowptr + off
+    ci7 = np.concatenate([np.full(off, -1, np.int32), colind])
+    va7 = np.concatenate([np.full(off, np.nan), values])
+    plan7 = lb.CsrPlan(cu(rp7), exact=True)
+    assert bits_equal(host(plan7.spmv(cu(ci7), cu(va7), cu(x))), want)
+
+
+def test_large_stencil_matches_oracle(cuda_device):
+    # a multi-tile, multi-wave 27-point case (1.7M rows) on the device generator
+    n = 120
+    rp, ci, v = lb.synth_stencil(27, n)
+    x = np.random.default_rng(9).uniform(-1, 1, n ** 3)
+    plan = lb.CsrPlan(rp, exact=True)
+    assert plan.info()["rowstream"]
+    y = host(plan.spmv(ci, v, cu(x)))
+    assert bits_equal(y, O.spmv_csr(host(rp), host(ci), host(v), x))
