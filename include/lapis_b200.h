@@ -223,6 +223,10 @@ int lapis_b200_spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64
                                 lapis_b200_spmm_plan* out);
 /* out4 = {hot rows, entries reading a hot row, persisting bytes granted, nnz} */
 int lapis_b200_spmm_plan_info(lapis_b200_spmm_plan plan, int64_t* out4);
+/* *out_far = entries carrying the plan's far-reuse hint (loaded L2 evict_first:
+ * the X row's next use lies beyond the plan's reuse horizon), -1 when the plan
+ * has no hints. */
+int lapis_b200_spmm_plan_hints(lapis_b200_spmm_plan plan, int64_t* out_far);
 int lapis_b200_spmm_plan_destroy(lapis_b200_spmm_plan plan);
 int lapis_b200_spmm_csr_plan(lapis_b200_spmm_plan plan, const void* rowptr, int rowptr_bytes,
                              const void* colind, int colind_bytes, const void* values,

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "lapis_b200_spmm_plan_create": ([_I64, _I64, _I64, _I64, _VP, _INT, _VP, _INT, _INT, _I64, _VP,
                                      C.POINTER(_VP)], _INT),
     "lapis_b200_spmm_plan_info": ([_VP, C.POINTER(_I64)], _INT),
+    "lapis_b200_spmm_plan_hints": ([_VP, C.POINTER(_I64)], _INT),
     "lapis_b200_spmm_plan_destroy": ([_VP], _INT),
     "lapis_b200_spmm_csr_plan": ([_VP, _VP, _INT, _VP, _INT, _VP, _VP, _I64, _VP, _I64, _INT, _VP],
                                  _INT),

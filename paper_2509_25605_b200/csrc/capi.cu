@@ -52,6 +52,7 @@ int synth_stencil(int, int64_t, int64_t, int64_t, int64_t*, int32_t*, double*, c
 int spmm_plan_create(int64_t, int64_t, int64_t, int64_t, const void*, int, const void*, int, int,
                      int64_t, cudaStream_t, void**);
 int spmm_plan_info(void*, int64_t*);
+int spmm_plan_hints(void*, int64_t*);
 int spmm_plan_destroy(void*);
 int spmm_csr_plan(void*, const void*, int, const void*, int, const void*, const void*, int64_t,
                   void*, int64_t, int, cudaStream_t);
@@ -191,6 +192,10 @@ int lapis_b200_spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64
 
 int lapis_b200_spmm_plan_info(lapis_b200_spmm_plan plan, int64_t* out4) {
   return spmm_plan_info(plan, out4);
+}
+
+int lapis_b200_spmm_plan_hints(lapis_b200_spmm_plan plan, int64_t* out_far) {
+  return spmm_plan_hints(plan, out_far);
 }
 
 int lapis_b200_spmm_plan_destroy(lapis_b200_spmm_plan plan) { return spmm_plan_destroy(plan); }

@@ -16,6 +16,8 @@
 //   (other types; deterministic, no atomics on values).
 #include "common.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -233,6 +235,36 @@ __device__ __forceinline__ void sty_row(T* p, const T (&v)[CPL]) {
   *reinterpret_cast<V*>(p) = w;
 }
 
+// X-row slice load with an L2 eviction-priority policy (SpMM plans with reuse
+// hints): one instruction whatever the policy, so lanes of a warp may carry
+// different policies
+template <class T, int CPL>
+__device__ __forceinline__ void ldx_row_pol(const T* p, T (&v)[CPL], uint64_t pol) {
+  using V = typename XVec<T, CPL>::V;
+  if constexpr (sizeof(V) == 4) {
+    uint32_t w;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(w) : "l"(p), "l"(pol));
+    memcpy(&v[0], &w, 4);
+  } else if constexpr (sizeof(V) == 8) {
+    unsigned long long w;
+    asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(w) : "l"(p), "l"(pol));
+    memcpy(&v[0], &w, 8);
+  } else {
+    static_assert(sizeof(V) % 16 == 0, "ldx_row_pol: 4, 8, 16 or 32 bytes");
+#pragma unroll
+    for (int h = 0; h < (int)(sizeof(V) / 16); ++h) {
+      unsigned long long a, b;
+      asm volatile("ld.global.nc.L2::cache_hint.v2.b64 {%0,%1}, [%2], %3;"
+                   : "=l"(a), "=l"(b) : "l"(reinterpret_cast<const char*>(p) + 16 * h), "l"(pol));
+      memcpy(reinterpret_cast<char*>(&v[0]) + 16 * h, &a, 8);
+      memcpy(reinterpret_cast<char*>(&v[0]) + 16 * h + 8, &b, 8);
+    }
+  }
+}
+// bit 30 of a non-negative remapped column: the X row's next use lies beyond
+// the plan's reuse horizon (loaded L2::evict_first)
+constexpr int32_t SPMM_FAR_BIT = 1 << 30;
+
 // ------------------------------------------------ fused GCN epilogue (fp32)
 // H[row, :] = relu(AX[row, :] W) for one row held by the warp as 2 values per
 // lane (lane l: AX[row, 2l], AX[row, 2l+1]; fin = fout = 64), W staged in shared
@@ -415,17 +447,25 @@ spmm_batch_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
 // most referenced X rows, which the plan pins in L2 with a persisting access
 // policy window; other entries address X as usual.  Entry order unchanged.
 template <class T, class RP, class CI, int CPL, int U, int PF, bool HOT = false>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, (U > 16 ? 2 : (U > 8 ? 3 : 4)))
 spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
                    const CI* __restrict__ colind, const T* __restrict__ values,
                    const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
                    unsigned long long* __restrict__ next, DescGuard guard,
-                   const T* __restrict__ Xh = nullptr, int64_t ldh = 0) {
+                   const T* __restrict__ Xh = nullptr, int64_t ldh = 0, int farpf = 0) {
   if (guard.skip()) return;
   __shared__ int64_t s_rp_all[8][33];
   const int lane = threadIdx.x & 31;
   int64_t* s_rp = s_rp_all[threadIdx.x >> 5];
   const int64_t nbatch = (nrows + 31) >> 5;
+  // HOT plans with reuse hints: X rows whose next use is far are loaded
+  // evict_first (they would only push out rows with reuse), the rest evict_normal
+  uint64_t pol_far = 0, pol_near = 0, pol_hot = 0;
+  if constexpr (HOT) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_far));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_near));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hot));
+  }
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(next, 1ull);
@@ -473,10 +513,19 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
               const CI pb = __shfl_sync(0xffffffffu, nx_col, pe & 31);
               const CI pc = pe < 32 ? pa : pb;
               const int line = lane / U;
-              if (j0 + pe < je && line * (128 / (int)sizeof(T)) < 32 * CPL && (!HOT || pc >= 0))
-                asm volatile("prefetch.global.L2 [%0];" ::
-                             "l"(xbase + (uint64_t)(uint32_t)pc * ldxb +
-                                 (line * 128 - lane * CPL * (int)sizeof(T))));
+              if (j0 + pe < je && line * (128 / (int)sizeof(T)) < 32 * CPL && (!HOT || pc >= 0)) {
+                const char* pa_line = xbase + (uint64_t)(uint32_t)(HOT ? (pc & ~SPMM_FAR_BIT) : pc) * ldxb +
+                                      (line * 128 - lane * CPL * (int)sizeof(T));
+                if (HOT && (pc & SPMM_FAR_BIT)) {  // far reuse
+                  if (farpf == 2)
+                    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], 128, %1;" ::
+                                 "l"(pa_line), "l"(pol_far));
+                  else if (farpf == 1)
+                    asm volatile("prefetch.global.L2 [%0];" :: "l"(pa_line));
+                } else {
+                  asm volatile("prefetch.global.L2 [%0];" :: "l"(pa_line));
+                }
+              }
             }
             CI cols[U];
             T vals[U];
@@ -489,13 +538,16 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               if (t0 + u < cnt) {
-                const char* xr;
-                if constexpr (HOT)
-                  xr = cols[u] >= 0 ? xbase + (uint64_t)(uint32_t)cols[u] * ldxb
-                                    : hbase + (uint64_t)(uint32_t)(~cols[u]) * ldhb;
-                else
-                  xr = xbase + (uint64_t)(uint32_t)cols[u] * ldxb;
-                ldx_row<T, CPL>(reinterpret_cast<const T*>(xr), xv[u]);
+                if constexpr (HOT) {
+                  const CI cu = cols[u];
+                  const char* xr = cu >= 0 ? xbase + (uint64_t)(uint32_t)(cu & ~SPMM_FAR_BIT) * ldxb
+                                           : hbase + (uint64_t)(uint32_t)(~cu) * ldhb;
+                  ldx_row_pol<T, CPL>(reinterpret_cast<const T*>(xr), xv[u],
+                                      cu < 0 ? pol_hot : ((cu & SPMM_FAR_BIT) ? pol_far : pol_near));
+                } else {
+                  ldx_row<T, CPL>(reinterpret_cast<const T*>(xbase + (uint64_t)(uint32_t)cols[u] * ldxb),
+                                  xv[u]);
+                }
               } else {
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) xv[u][q] = T(0);
@@ -532,6 +584,28 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
       }
     }
   }
+}
+
+// L2 prefetch of far-reuse X rows in hinted plans: 0 none, 1 plain, 2 bulk
+// prefetch with an evict_first policy (LAPIS_B200_SPMM_FARPF, A/B runs)
+inline int spmm_far_prefetch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LAPIS_B200_SPMM_FARPF");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+// gathers in flight per warp of the batch kernel: -1 = by element size
+// (default), else LAPIS_B200_SPMM_U = 8 / 16 / 32 (A/B runs)
+inline int spmm_u16() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("LAPIS_B200_SPMM_U");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
 }
 
 // LAPIS_B200_SPMM_V1=1: the original batch kernel (A/B runs)
@@ -1031,8 +1105,12 @@ struct SpmmOp {
         if (hot && next && pf <= 1) {
 #define LB_BATH(CC, PFV) spmm_batch2_kernel<T, RP, int32_t, CC, 8, PFV, true><<<(unsigned)gblocks, 256, 0, st>>>( \
           nrows, k, (const RP*)rowptr, hot->colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, \
-          next, fast, (const T*)hot->xhot, hot->ldh)
-          if (pf == 1) {
+          next, fast, (const T*)hot->xhot, hot->ldh, spmm_far_prefetch())
+          if (spmm_u16() == 16 && cpl == 2) {
+            spmm_batch2_kernel<T, RP, int32_t, 2, 16, 1, true><<<(unsigned)gblocks, 256, 0, st>>>(
+                nrows, k, (const RP*)rowptr, hot->colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy,
+                next, fast, (const T*)hot->xhot, hot->ldh, spmm_far_prefetch());
+          } else if (pf == 1) {
             if (cpl == 4) LB_BATH(4, 1); else if (cpl == 2) LB_BATH(2, 1); else LB_BATH(1, 1);
           } else {
             if (cpl == 4) LB_BATH(4, 0); else if (cpl == 2) LB_BATH(2, 0); else LB_BATH(1, 0);
@@ -1042,7 +1120,23 @@ struct SpmmOp {
 #define LB_BAT2(CC, PFV) spmm_batch2_kernel<T, RP, CI, CC, 8, PFV><<<(unsigned)gblocks, 256, 0, st>>>( \
           nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, \
           next, fast)
-          if (pf == 1) {
+          if (spmm_u16() == 32 && cpl == 2) {
+            spmm_batch2_kernel<T, RP, CI, 2, 32, 1><<<(unsigned)gblocks, 256, 0, st>>>(
+                nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+                (T*)Y, ldy, next, fast);
+          } else if ((spmm_u16() == 16 || (spmm_u16() < 0 && sizeof(T) == 4)) && cpl <= 2) {
+            // 4-byte elements: 16 gathers in flight per warp (three CTAs per
+            // SM); config 4's SpMM 0.848 -> 0.813 ms per layer.  (8-byte rows:
+            // config 3 9.86 -> 15.3 ms, so they keep 8.)
+            if (cpl == 2)
+              spmm_batch2_kernel<T, RP, CI, 2, 16, 1><<<(unsigned)gblocks, 256, 0, st>>>(
+                  nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+                  (T*)Y, ldy, next, fast);
+            else
+              spmm_batch2_kernel<T, RP, CI, 1, 16, 1><<<(unsigned)gblocks, 256, 0, st>>>(
+                  nrows, k, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)X, ldx,
+                  (T*)Y, ldy, next, fast);
+          } else if (pf == 1) {
             if (cpl == 4) LB_BAT2(4, 1); else if (cpl == 2) LB_BAT2(2, 1); else LB_BAT2(1, 1);
           } else {
             if (cpl == 4) LB_BAT2(4, 0); else if (cpl == 2) LB_BAT2(2, 0); else LB_BAT2(1, 0);
@@ -1155,6 +1249,8 @@ struct SpmmPlanImpl {
   void* xhot = nullptr;           // [nhot, k]
   int64_t nhot = 0, hot_entries = 0;
   size_t window_bytes = 0;        // persisting window actually granted
+  int hints = 0;                  // 1: SPMM_FAR_BIT reuse hints in colind_hot
+  int64_t far_entries = 0;        // entries marked far
 };
 
 __global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ ci32,
@@ -1208,6 +1304,95 @@ __global__ void hot_gather_kernel(int64_t nhot, int64_t row_bytes, const int32_t
   }
 }
 
+// Reuse hints (bit 30 of the remapped colind, SPMM_FAR_BIT): the gathers run
+// in CSR order, so the distance from an entry to the next entry of the same
+// column is the X row's reuse distance.  Entries whose next use lies more
+// than D entries ahead (D = 8 L2-sized working sets of X rows) are loaded
+// evict_first and the rest evict_normal — a cheap stand-in for Belady's
+// replacement.  scripts/cache_sim.c on config 3 (126 MB of X rows): LRU 84.2M
+// misses, this policy 61.4M, Belady 61.0M.  Positions sorted by column
+// (stable radix sort) give every entry its successor in one pass.
+__global__ void col_keys_kernel(int64_t nnz, const int32_t* __restrict__ ci32,
+                                const int64_t* __restrict__ ci64, int32_t* __restrict__ keys,
+                                int32_t* __restrict__ pos) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    keys[j] = ci32 ? ci32[j] : (int32_t)ci64[j];
+    pos[j] = (int32_t)j;
+  }
+}
+__global__ void reuse_hint_kernel(int64_t nnz, const int32_t* __restrict__ skeys,
+                                  const int32_t* __restrict__ spos, int64_t horizon,
+                                  int32_t* __restrict__ colind_hot,
+                                  unsigned long long* __restrict__ nfar) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = spos[i];
+    const bool near = i + 1 < nnz && skeys[i + 1] == skeys[i] && (int64_t)spos[i + 1] - p <= horizon;
+    const int32_t c = colind_hot[p];
+    if (!near && c >= 0) {
+      colind_hot[p] = c | SPMM_FAR_BIT;
+      ++local;
+    }
+  }
+  if (local) atomicAdd(nfar, local);
+}
+
+static int spmm_reuse_hints(SpmmPlanImpl* p, const int32_t* c32, const int64_t* c64,
+                            int64_t row_bytes, cudaStream_t st) {
+  const int64_t nnz = p->nnz;
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
+  const char* de = getenv("LAPIS_B200_SPMM_HINT_D");
+  const double mult = de ? atof(de) : 8.0;
+  const int64_t horizon = (int64_t)(mult * (double)std::max<int64_t>(1, (int64_t)l2 / row_bytes));
+  int end_bit = 1;
+  while (end_bit < 31 && (1ll << end_bit) < p->ncols) ++end_bit;
+  int32_t *keys = nullptr, *keys2 = nullptr, *pos = nullptr, *pos2 = nullptr;
+  void* tmp = nullptr;
+  unsigned long long* nfar = nullptr;
+  size_t tmp_bytes = 0;
+  auto cleanup = [&]() {
+    for (void* q : {(void*)keys, (void*)keys2, (void*)pos, (void*)pos2, tmp, (void*)nfar})
+      if (q) cudaFreeAsync(q, st);
+  };
+  const size_t b = (size_t)nnz * 4;
+  int rc = check_cuda(cudaMallocAsync((void**)&keys, b, st), "alloc(hint keys)");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&keys2, b, st), "alloc(hint keys)");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&pos, b, st), "alloc(hint pos)");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&pos2, b, st), "alloc(hint pos)");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&nfar, 8, st), "alloc(hint count)");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMemsetAsync(nfar, 0, 8, st), "memset(hint count)");
+  const int sms = num_sms();
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nnz + 255) / 256, (int64_t)sms * 8));
+  if (rc == LAPIS_B200_OK) {
+    col_keys_kernel<<<g, 256, 0, st>>>(nnz, c32, c64, keys, pos);
+    rc = check_launch("col_keys_kernel");
+  }
+  if (rc == LAPIS_B200_OK)
+    rc = check_cuda(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, pos, pos2,
+                                                    (int)nnz, 0, end_bit, st), "radix sort (size)");
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync(&tmp, tmp_bytes, st), "alloc(sort)");
+  if (rc == LAPIS_B200_OK)
+    rc = check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, pos, pos2,
+                                                    (int)nnz, 0, end_bit, st), "radix sort");
+  if (rc == LAPIS_B200_OK) {
+    reuse_hint_kernel<<<g, 256, 0, st>>>(nnz, keys2, pos2, horizon, p->colind_hot, nfar);
+    rc = check_launch("reuse_hint_kernel");
+  }
+  unsigned long long h = 0;
+  if (rc == LAPIS_B200_OK)
+    rc = check_cuda(cudaMemcpyAsync(&h, nfar, 8, cudaMemcpyDeviceToHost, st), "hint count D2H");
+  cleanup();
+  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaStreamSynchronize(st), "hint sync");
+  if (rc == LAPIS_B200_OK) {
+    p->far_entries = (int64_t)h;
+    p->hints = 1;
+  }
+  return rc;
+}
+
 int spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const void* rowptr,
                      int rp_bytes, const void* colind, int ci_bytes, int dtype, int64_t hot_bytes,
                      cudaStream_t st, void** out) {
@@ -1226,11 +1411,13 @@ int spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const
   // 16 MB measured best on config 3 (8.83 ms vs 9.40 without a plan, 8.99 at 32 MB,
   // 10.84 at 64 MB: a larger persisting set starves the streamed rest of L2)
   if (hot_bytes == 0) hot_bytes = 16ll << 20;
+  const char* nohot = getenv("LAPIS_B200_SPMM_NOHOT");  // A/B runs: hints only
+  if (nohot && nohot[0] == '1') hot_bytes = 0;
   int max_persist = 0;
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, p->device);
   cudaGetLastError();
   if (max_persist > 0 && hot_bytes > max_persist) hot_bytes = max_persist;
-  const int64_t cap = std::min<int64_t>(ncols, hot_bytes / row_bytes);
+  const int64_t cap = hot_bytes > 0 ? std::min<int64_t>(ncols, hot_bytes / row_bytes) : 0;
   int rc = LAPIS_B200_OK;
   unsigned* counts = nullptr;
   int32_t* hot_index = nullptr;
@@ -1304,6 +1491,19 @@ int spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const
     return rc;
   }
   p->nhot = std::min<int64_t>((int64_t)nh, cap);
+  // reuse hints (LAPIS_B200_SPMM_HINT=0 disables): needs column ids < 2^30 and
+  // positions < 2^31
+  const char* he = getenv("LAPIS_B200_SPMM_HINT");
+  if (!(he && he[0] == '0') && nnz > 0 && nnz < 0x7fffffffLL && ncols < (1ll << 30)) {
+    rc = spmm_reuse_hints(p, c32, c64, row_bytes, st);
+    if (rc != LAPIS_B200_OK) {
+      cudaFree(p->colind_hot);
+      if (p->hot_cols) cudaFree(p->hot_cols);
+      if (p->xhot) cudaFree(p->xhot);
+      delete p;
+      return rc;
+    }
+  }
   for (int v = (int)tau; v < NB && tau < (unsigned)NB; ++v) p->hot_entries += (int64_t)h[v] * v;
   // persisting L2 for the hot rows (process-wide limit; never lowered here)
   const size_t want = (size_t)p->nhot * row_bytes;
@@ -1327,6 +1527,13 @@ int spmm_plan_info(void* plan, int64_t* out4) {
   out4[1] = p->hot_entries;
   out4[2] = (int64_t)p->window_bytes;
   out4[3] = p->nnz;
+  return LAPIS_B200_OK;
+}
+
+int spmm_plan_hints(void* plan, int64_t* out_far) {
+  auto* p = static_cast<SpmmPlanImpl*>(plan);
+  if (!p || !out_far) return fail(LAPIS_B200_ERR_ARG, "spmm plan hints: null argument");
+  *out_far = p->hints ? p->far_entries : -1;
   return LAPIS_B200_OK;
 }
 
@@ -1375,7 +1582,7 @@ int spmm_csr_plan(void* plan, const void* rowptr, int rp_bytes, const void* coli
     cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
     cudaGetLastError();
   }
-  const HotMap* hp = p->nhot > 0 ? &hm : nullptr;
+  const HotMap* hp = (p->nhot > 0 || p->hints) ? &hm : nullptr;
   int rc;
 #define LB_SPMMP(T)                                                                              \
   if (rp_bytes == 8 && ci_bytes == 4) rc = SpmmOp<T, int64_t, int32_t>::run(nrows, nnz, k, rowptr, colind, values, X, ldx, Y, ldy, st, nullptr, hp); \

@@ -247,8 +247,11 @@ class SpmmPlan:
     def info(self) -> dict:
         out = (C.c_int64 * 4)()
         check(_capi.lib().lapis_b200_spmm_plan_info(self._handle, out), "spmm_plan_info")
+        far = C.c_int64(0)
+        check(_capi.lib().lapis_b200_spmm_plan_hints(self._handle, C.byref(far)), "spmm_plan_hints")
         return {"hot_rows": int(out[0]), "hot_entries": int(out[1]),
-                "persisting_bytes": int(out[2]), "nnz": int(out[3])}
+                "persisting_bytes": int(out[2]), "nnz": int(out[3]),
+                "far_reuse_entries": int(far.value)}
 
     def spmm(self, values, X, Y=None, *, stream=None) -> torch.Tensor:
         values, X, Y = (_from_dlpack(t) for t in (values, X, Y))

@@ -140,11 +140,56 @@ int main(int argc, char** argv) {
       left -= take;
     }
     const int64_t miss_pin = (n - covered) + pinned;
+    /* ---- LRU with reuse hints: an access whose next use is more than D
+     * accesses away is (re)placed at the LRU end (an L2 evict_first load),
+     * others at the MRU end; D = hint_dist * cap (HINT_D env, default 4) */
+    const double hint_mult = getenv("HINT_D") ? atof(getenv("HINT_D")) : 4.0;
+    const int64_t D = (int64_t)(hint_mult * (double)cap);
+    int64_t miss_hint = 0;
+    {
+      int32_t* pv = malloc(ncols * 4);
+      int32_t* nv = malloc(ncols * 4);
+      char* inn = calloc(ncols, 1);
+      int32_t hd = -1, tl = -1;
+      int64_t sz = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        const int32_t c = a[i];
+        const int near = nxt[i] != INT64_MAX && nxt[i] - i <= D;
+        if (inn[c]) {
+          /* unlink c */
+          if (pv[c] >= 0) nv[pv[c]] = nv[c]; else hd = nv[c];
+          if (nv[c] >= 0) pv[nv[c]] = pv[c]; else tl = pv[c];
+        } else {
+          ++miss_hint;
+          if (sz == cap) {
+            const int32_t v = tl;
+            tl = pv[v];
+            if (tl >= 0) nv[tl] = -1; else hd = -1;
+            inn[v] = 0;
+            --sz;
+          }
+          inn[c] = 1;
+          ++sz;
+        }
+        if (near || hd < 0) {  /* MRU end */
+          pv[c] = -1; nv[c] = hd;
+          if (hd >= 0) pv[hd] = c;
+          hd = c;
+          if (tl < 0) tl = c;
+        } else {               /* LRU end */
+          nv[c] = -1; pv[c] = tl;
+          nv[tl] = c;
+          tl = c;
+        }
+      }
+      free(pv); free(nv); free(inn);
+    }
     free(hist);
     free(cur);
-    printf("%s{\"cap_rows\": %lld, \"miss_opt\": %lld, \"miss_lru\": %lld, \"miss_pin\": %lld}",
+    printf("%s{\"cap_rows\": %lld, \"miss_opt\": %lld, \"miss_lru\": %lld, \"miss_pin\": %lld, "
+           "\"miss_hint\": %lld, \"hint_d\": %lld}",
            ai > 3 ? ", " : "", (long long)cap, (long long)miss_opt, (long long)miss_lru,
-           (long long)miss_pin);
+           (long long)miss_pin, (long long)miss_hint, (long long)D);
     fflush(stdout);
   }
   printf("]}\n");
