@@ -214,11 +214,25 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+__device__ __forceinline__ float tf32_trunc(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+// head / tail of the split: rawhi = 1 keeps the fp32 value as the head (the
+// tensor core reads only its TF32 bits) and the tail is a - trunc(a)
+__device__ __forceinline__ void tf32_split(float a, int rawhi, float& h, float& l) {
+  if (rawhi) {
+    h = a;
+    l = tf32_rna(a - tf32_trunc(a));
+  } else {
+    h = tf32_rna(a);
+    l = tf32_rna(a - h);
+  }
+}
 
 // A [m, k] (lda) -> hi, lo [m, kp], zero padded for k <= j < kp
 __global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float* __restrict__ A,
                                   int64_t lda, float* __restrict__ hi, float* __restrict__ lo,
-                                  Guard guard) {
+                                  Guard guard, int rawhi) {
   if (guard_skip(guard)) return;
   // a CTA per row (grid-stride), 4 consecutive elements per thread: 16-byte
   // loads when the row pitch allows, 16-byte stores (kp % 4 == 0), no
@@ -239,10 +253,13 @@ __global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float*
         a.z = j + 2 < k ? ar[j + 2] : 0.0f;
         a.w = j + 3 < k ? ar[j + 3] : 0.0f;
       }
-      const float4 h = make_float4(tf32_rna(a.x), tf32_rna(a.y), tf32_rna(a.z), tf32_rna(a.w));
+      float4 h, l;
+      tf32_split(a.x, rawhi, h.x, l.x);
+      tf32_split(a.y, rawhi, h.y, l.y);
+      tf32_split(a.z, rawhi, h.z, l.z);
+      tf32_split(a.w, rawhi, h.w, l.w);
       hr[j4] = h;
-      lr[j4] = make_float4(tf32_rna(a.x - h.x), tf32_rna(a.y - h.y), tf32_rna(a.z - h.z),
-                           tf32_rna(a.w - h.w));
+      lr[j4] = l;
     }
   }
 }
@@ -250,7 +267,7 @@ __global__ void split_rows_kernel(int64_t m, int64_t k, int64_t kp, const float*
 // B [k, n] (ldb) -> hi, lo [n, kp] (transposed: K-major), zero padded
 __global__ void split_transpose_kernel(int64_t k, int64_t n, int64_t kp, const float* __restrict__ B,
                                        int64_t ldb, float* __restrict__ hi, float* __restrict__ lo,
-                                       Guard guard) {
+                                       Guard guard, int rawhi) {
   if (guard_skip(guard)) return;
   // 64 (k) x 64 (n) tile, 256 threads: coalesced 128-byte row loads, 8-byte
   // stores of consecutive k pairs (kp is a multiple of 4)
@@ -271,9 +288,37 @@ __global__ void split_transpose_kernel(int64_t k, int64_t n, int64_t kp, const f
     const int64_t nn = n0 + r;
     if (nn < n && kk < kp) {
       const float a0 = tile[2 * tx][r], a1 = tile[2 * tx + 1][r];
-      const float h0 = tf32_rna(a0), h1 = tf32_rna(a1);
+      float h0, h1, l0, l1;
+      tf32_split(a0, rawhi, h0, l0);
+      tf32_split(a1, rawhi, h1, l1);
       *reinterpret_cast<float2*>(hi + nn * kp + kk) = make_float2(h0, h1);
-      *reinterpret_cast<float2*>(lo + nn * kp + kk) = make_float2(tf32_rna(a0 - h0), tf32_rna(a1 - h1));
+      *reinterpret_cast<float2*>(lo + nn * kp + kk) = make_float2(l0, l1);
+    }
+  }
+}
+
+// tails only (RAW kernel): lo[i, j] = rna_tf32(a - trunc_tf32(a)) for
+// j < cols, 0 for cols <= j < ldo; rows x cols with pitch lda -> pitch ldo
+__global__ void tf32_tail_kernel(int64_t rows, int64_t cols, int64_t ldo, const float* __restrict__ A,
+                                 int64_t lda, float* __restrict__ lo, Guard guard) {
+  if (guard_skip(guard)) return;
+  const bool vec = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0);
+  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+    const float* ar = A + i * lda;
+    float4* lr = reinterpret_cast<float4*>(lo + i * ldo);
+    for (int64_t j4 = threadIdx.x; j4 < ldo / 4; j4 += blockDim.x) {
+      const int64_t j = 4 * j4;
+      float4 a;
+      if (vec && j + 3 < cols) {
+        a = *reinterpret_cast<const float4*>(ar + j);
+      } else {
+        a.x = j < cols ? ar[j] : 0.0f;
+        a.y = j + 1 < cols ? ar[j + 1] : 0.0f;
+        a.z = j + 2 < cols ? ar[j + 2] : 0.0f;
+        a.w = j + 3 < cols ? ar[j + 3] : 0.0f;
+      }
+      lr[j4] = make_float4(tf32_rna(a.x - tf32_trunc(a.x)), tf32_rna(a.y - tf32_trunc(a.y)),
+                           tf32_rna(a.z - tf32_trunc(a.z)), tf32_rna(a.w - tf32_trunc(a.w)));
     }
   }
 }
@@ -293,6 +338,36 @@ static int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, in
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return LAPIS_B200_OK;
+}
+
+// rows x cols fp32 row-major (pitch ld elements), box = box_inner x box_rows
+static int make_rowmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols,
+                             int64_t ld, uint32_t box_inner, uint32_t box_rows,
+                             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  const cuuint32_t box[2] = {box_inner, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LAPIS_B200_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return LAPIS_B200_OK;
+}
+
+// raw-head path: A 16-byte aligned with a 16-byte row pitch.  (Reading B
+// MN-major straight from the caller's row-major B — TMA 128-B / 32-B-atom
+// swizzle, UMMA layout type 1 — was measured too: correct, but the kernel
+// ran 0.633 vs 0.57 ms at 4096^3, more than the transpose it saves.)
+static bool tf32_raw_ok(const void* A, int64_t lda, int64_t sA, int64_t batch) {
+  static const int off = [] {
+    const char* e = getenv("LAPIS_B200_TF32_RAW");
+    return (e && e[0] == '0') ? 1 : 0;
+  }();
+  if (off) return false;
+  return (uintptr_t)A % 16 == 0 && lda % 4 == 0 && (batch <= 1 || sA % 4 == 0);
 }
 
 int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
@@ -317,6 +392,48 @@ int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, i
                       "smem attr (gemm_tf32x3_kernel)"));
     configured_dev = dev;
   }
+  if (tf32_raw_ok(A, lda, sA, batch)) {
+    // the head of A is A itself (read K-major straight from the caller's
+    // row-major A); workspace: A's tail [m, kp], B's head and tail transposed
+    float* ws = nullptr;
+    const size_t a_elems = (size_t)m * kp, b_elems = (size_t)n * kp;
+    LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, (a_elems + 2 * b_elems) * sizeof(float), st),
+                      "alloc(tf32x3 workspace)"));
+    float* al = ws;
+    float* bh = al + a_elems;
+    float* bl = bh + b_elems;
+    int rc = LAPIS_B200_OK;
+    for (int64_t b = 0; b < batch && rc == LAPIS_B200_OK; ++b) {
+      const float* Ab = (const float*)A + b * sA;
+      const float* Bb = (const float*)B + b * sB;
+      float* Cb = (float*)C + b * sC;
+      const int64_t ga = std::min<int64_t>(m, (int64_t)num_sms() * 16);
+      tf32_tail_kernel<<<(unsigned)ga, 256, 0, st>>>(m, k, kp, Ab, lda, al, guard);
+      dim3 tg((unsigned)((n + 63) / 64), (unsigned)((kp + 63) / 64));
+      split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl, guard, 1);
+      rc = check_launch("tf32 split (raw A head)");
+      CUtensorMap mah, mal, mbh, mbl;
+      if (rc == LAPIS_B200_OK) rc = make_rowmajor_map(&mah, Ab, m, k, lda, TG_BK, TG_BM);
+      if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mal, al, m, kp, TG_BM);
+      if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mbh, bh, n, kp, TG_BN);
+      if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mbl, bl, n, kp, TG_BN);
+      if (rc != LAPIS_B200_OK) break;
+      Tf32Params prm;
+      prm.m = (int)m;
+      prm.n = (int)n;
+      prm.nk = (int)((kp + TG_BK - 1) / TG_BK);
+      prm.num_m = (int)((m + TG_BM - 1) / TG_BM);
+      prm.num_n = (int)((n + TG_BN - 1) / TG_BN);
+      prm.C = Cb;
+      prm.ldc = ldc;
+      const int tiles = prm.num_m * prm.num_n;
+      const int grid = std::min(tiles, num_sms());
+      gemm_tf32x3_kernel<<<grid, TG_THREADS_V2, TG_SMEM, st>>>(mah, mal, mbh, mbl, prm, guard);
+      rc = check_launch("gemm_tf32x3_kernel");
+    }
+    cudaFreeAsync(ws, st);
+    return rc;
+  }
   float* ws = nullptr;
   const size_t a_elems = (size_t)m * kp, b_elems = (size_t)n * kp;
   LB_TRY(check_cuda(cudaMallocAsync((void**)&ws, 2 * (a_elems + b_elems) * sizeof(float), st),
@@ -331,9 +448,13 @@ int gemm_tf32x3(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, i
     const float* Bb = (const float*)B + b * sB;
     float* Cb = (float*)C + b * sC;
     const int64_t sblocks = std::min<int64_t>(m, (int64_t)num_sms() * 16);
-    split_rows_kernel<<<(unsigned)sblocks, 256, 0, st>>>(m, k, kp, Ab, lda, ah, al, guard);
+    static const int rawhi = [] {
+      const char* e = getenv("LAPIS_B200_TF32_RAWHI");
+      return (e && e[0] == '1') ? 1 : 0;
+    }();
+    split_rows_kernel<<<(unsigned)sblocks, 256, 0, st>>>(m, k, kp, Ab, lda, ah, al, guard, rawhi);
     dim3 tg((unsigned)((n + 63) / 64), (unsigned)((kp + 63) / 64));
-    split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl, guard);
+    split_transpose_kernel<<<tg, 256, 0, st>>>(k, n, kp, Bb, ldb, bh, bl, guard, rawhi);
     rc = check_launch("tf32 split");
     CUtensorMap mah, mal, mbh, mbl;
     if (rc == LAPIS_B200_OK) rc = make_kmajor_map(&mah, ah, m, kp, TG_BM);
