@@ -401,12 +401,39 @@ spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __res
 // load instruction reads 32 consecutive entries.  Short regular rows (C1: 5
 // per row) are the case the vector kernel serves worst: one row per lane there
 // reads 5 strided entries with about 2 loads in flight per thread.
-template <class T, class RP, class CI, int U, bool EXACT>
+// Schedulable (non-volatile) read-only load with an L2 eviction policy.
+template <class T> __device__ __forceinline__ T ld_pol(const T* p, uint64_t pol);
+template <> __device__ __forceinline__ double ld_pol<double>(const double* p, uint64_t pol) {
+  double v; asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol)); return v;
+}
+template <> __device__ __forceinline__ float ld_pol<float>(const float* p, uint64_t pol) {
+  float v; asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol)); return v;
+}
+template <> __device__ __forceinline__ long long ld_pol<long long>(const long long* p, uint64_t pol) {
+  long long v; asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol)); return v;
+}
+template <> __device__ __forceinline__ long ld_pol<long>(const long* p, uint64_t pol) {
+  long v; asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol)); return v;
+}
+template <> __device__ __forceinline__ int ld_pol<int>(const int* p, uint64_t pol) {
+  int v; asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
+}
+
+// POL: the structure stream (each 128-B line consumed whole by one coalesced
+// warp load) is read L2::evict_first and the x gathers L2::evict_last, so x
+// (80 MB for config 3's 10M rows) stays in the 126 MB L2 instead of being
+// pushed out by the 1.2 GB entry stream.
+template <class T, class RP, class CI, int U, bool EXACT, bool POL = false>
 __global__ void __launch_bounds__(256)
 spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                       const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
                       unsigned long long* __restrict__ next, RowGuard guard = RowGuard()) {
   if (row_guard_skip(guard)) return;
+  uint64_t pol_first = 0, pol_last = 0;
+  if constexpr (POL) {
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+  }
   constexpr int CAP = 32 * U;
   __shared__ T win[8][CAP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -439,14 +466,22 @@ spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t j = base + u * 32 + lane;
-        c[u] = j < hi ? colind[j] : CI(0);
-        v[u] = j < hi ? values[j] : T(0);
+        if constexpr (POL) {
+          c[u] = j < hi ? ld_pol<CI>(colind + j, pol_first) : CI(0);
+          v[u] = j < hi ? ld_pol<T>(values + j, pol_first) : T(0);
+        } else {
+          c[u] = j < hi ? colind[j] : CI(0);
+          v[u] = j < hi ? values[j] : T(0);
+        }
       }
       T p[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t j = base + u * 32 + lane;
-        p[u] = j < hi ? __ldg(x + (int64_t)c[u]) : T(0);
+        if constexpr (POL)
+          p[u] = j < hi ? ld_pol<T>(x + (int64_t)c[u], pol_last) : T(0);
+        else
+          p[u] = j < hi ? __ldg(x + (int64_t)c[u]) : T(0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) my[u * 32 + lane] = Arith<T>::mul(v[u], p[u]);
@@ -816,8 +851,24 @@ template <class T, class RP, class CI>
 static int launch_warpblock_t(int64_t nrows, const void* rowptr, const void* colind,
                               const void* values, const void* x, void* y, int exact,
                               unsigned long long* next, cudaStream_t st, RowGuard guard) {
-  auto kern = exact ? spmv_warpblock_kernel<T, RP, CI, 8, true>
-                    : spmv_warpblock_kernel<T, RP, CI, 8, false>;
+  static const bool pol = [] {
+    const char* e = getenv("LAPIS_B200_SPMV_WB_POLICY");  // A/B runs: 0 = plain loads
+    return !(e && e[0] == '0');
+  }();
+  static const int wbu = [] {
+    const char* e = getenv("LAPIS_B200_SPMV_WB_U");  // A/B runs: entries per lane per window
+    return e ? atoi(e) : 16;
+  }();
+  auto kern = exact ? (pol ? spmv_warpblock_kernel<T, RP, CI, 8, true, true>
+                           : spmv_warpblock_kernel<T, RP, CI, 8, true, false>)
+                    : (pol ? spmv_warpblock_kernel<T, RP, CI, 8, false, true>
+                           : spmv_warpblock_kernel<T, RP, CI, 8, false, false>);
+  if (wbu == 16 && pol)
+    kern = exact ? spmv_warpblock_kernel<T, RP, CI, 16, true, true>
+                 : spmv_warpblock_kernel<T, RP, CI, 16, false, true>;
+  if (wbu == 24 && pol)
+    kern = exact ? spmv_warpblock_kernel<T, RP, CI, 24, true, true>
+                 : spmv_warpblock_kernel<T, RP, CI, 24, false, true>;
   static thread_local int configured_dev = -1;
   static thread_local int ctas_per_sm[2] = {0, 0};
   int dev = 0;
