@@ -17,7 +17,14 @@
  *   - return 0 on success, a LAPIS_B200_ERR_* code otherwise, with a
  *     thread-local message in lapis_b200_last_error(); the host process is
  *     never aborted (the reference stub calls exit(1),
- *     lapis_serial_stub.hpp:29-32).
+ *     lapis_serial_stub.hpp:29-32);
+ *   - threads: any number of host threads may call concurrently, each on its
+ *     own stream (per-call scratch comes from stream-ordered cudaMallocAsync;
+ *     plans are read-only after creation); tests/test_threads_gpu.py;
+ *   - scratch memory: the first call on a device raises the release threshold
+ *     of that device's DEFAULT memory pool so per-call workspaces stay cached
+ *     in the pool (a process-wide setting other cudaMallocAsync users share);
+ *     LAPIS_B200_KEEP_POOL=0 leaves the pool as the caller configured it.
  */
 #ifndef LAPIS_B200_H
 #define LAPIS_B200_H

@@ -99,6 +99,11 @@ __device__ __forceinline__ longlong2 ld_stream(const longlong2* p) {
 // turns every per-call workspace into a fresh mapping).
 inline void keep_pool_memory() {
   static bool done[64] = {false};
+  static const bool off = [] {
+    const char* e = getenv("LAPIS_B200_KEEP_POOL");
+    return e && e[0] == '0';
+  }();
+  if (off) return;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || done[dev]) return;
