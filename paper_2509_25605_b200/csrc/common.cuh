@@ -283,28 +283,6 @@ template <> __device__ __forceinline__ int ld_ord<int>(const int* p, bool pred) 
   return v;
 }
 
-// shared-memory counterpart of ld_ord (8- or 4-byte element, generic pointer
-// into shared memory): issued in program order with the other ordered loads
-template <class T> __device__ __forceinline__ T ld_shared_ord(const T* p, bool pred) {
-  static_assert(sizeof(T) == 8 || sizeof(T) == 4, "ld_shared_ord: 4- or 8-byte elements");
-  const uint32_t a = smem_u32(p);
-  if constexpr (sizeof(T) == 8) {
-    unsigned long long v;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b64 %0, 0;\n\t"
-                 "@q ld.shared.b64 %0, [%1];\n\t}" : "=l"(v) : "r"(a), "r"((int)pred));
-    T r;
-    memcpy(&r, &v, 8);
-    return r;
-  } else {
-    unsigned v;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t"
-                 "@q ld.shared.b32 %0, [%1];\n\t}" : "=r"(v) : "r"(a), "r"((int)pred));
-    T r;
-    memcpy(&r, &v, 4);
-    return r;
-  }
-}
-
 template <class T> __device__ __forceinline__ T ld_hint(const T* p, uint64_t pol);
 template <> __device__ __forceinline__ double ld_hint<double>(const double* p, uint64_t pol) {
   double v;
