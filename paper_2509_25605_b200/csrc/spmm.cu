@@ -597,168 +597,6 @@ inline int spmm_far_prefetch() {
   return v;
 }
 
-// ------------------------------------------------ kernel 1b (ring, async copies)
-// The batch kernel's row walk with the X-row gathers moved off the register
-// file: every lane copies its 16-byte (8-byte) slice of an X row straight into
-// a per-warp shared-memory ring with cp.async (no register is held while the
-// copy is in flight), RING = 32 rows in flight per warp at all times.  The
-// entry stream is cut into groups of 8; the ring holds 4 groups, so the group
-// being folded always has the next 3 in flight and the one issued after it
-// lies exactly one 32-entry colind window ahead (`nx_col`).  Same fold, same
-// order as the batch kernel (bit-identical).  HOT plans: negative columns
-// address the hot buffer, far-reuse columns copy with an L2::evict_first hint.
-constexpr int RING_G = 8, RING_NG = 4, RING_ROWS = RING_G * RING_NG;  // 32
-constexpr int RING_WARPS = 4;
-
-template <int BYTES>
-__device__ __forceinline__ void cp_async_slice(uint32_t dst, const void* src, uint64_t pol, bool hint) {
-  static_assert(BYTES == 8 || BYTES == 16, "ring slices are 8 or 16 bytes");
-  if constexpr (BYTES == 16) {
-    if (hint)
-      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "l"(pol) : "memory");
-    else
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
-  } else {
-    if (hint)
-      asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" :: "r"(dst), "l"(src), "l"(pol) : "memory");
-    else
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
-  }
-}
-
-template <class T, class RP, class CI, int CPL, bool HOT>
-__global__ void __launch_bounds__(RING_WARPS * 32)
-spmm_ring_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
-                 const CI* __restrict__ colind, const T* __restrict__ values,
-                 const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy,
-                 unsigned long long* __restrict__ next, DescGuard guard,
-                 const T* __restrict__ Xh = nullptr, int64_t ldh = 0) {
-  if (guard.skip()) return;
-  constexpr int SLICE = CPL * (int)sizeof(T);
-  extern __shared__ __align__(128) unsigned char ring_smem[];
-  __shared__ int64_t s_rp_all[RING_WARPS][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t* s_rp = s_rp_all[warp];
-  unsigned char* ring = ring_smem + (size_t)warp * RING_ROWS * 32 * SLICE;
-  const uint32_t ring_s = smem_u32(ring) + (uint32_t)(lane * SLICE);
-  uint64_t pol_far = 0;
-  if constexpr (HOT) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_far));
-  const int64_t nbatch = (nrows + 31) >> 5;
-  for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(next, 1ull);
-    const int64_t bt = (int64_t)__shfl_sync(0xffffffffu, t, 0);
-    if (bt >= nbatch) break;
-    const int64_t r0 = bt << 5;
-    const int nr = (int)((nrows - r0) < 32 ? (nrows - r0) : 32);
-    __syncwarp();
-    if (lane <= nr) s_rp[lane] = (int64_t)rowptr[r0 + lane];
-    if (nr == 32 && lane == 0) s_rp[32] = (int64_t)rowptr[r0 + 32];
-    __syncwarp();
-    const int64_t my_len = lane < nr ? s_rp[lane + 1] - s_rp[lane] : 0;
-    const unsigned long_mask = __ballot_sync(0xffffffffu, my_len > SPLIT);
-    for (int64_t c0 = (int64_t)lane * CPL; c0 - (int64_t)lane * CPL < k; c0 += 32 * CPL) {
-      const char* xbase = reinterpret_cast<const char*>(X + c0);
-      const uint32_t ldxb = (uint32_t)(ldx * (int64_t)sizeof(T));
-      const char* hbase = HOT ? reinterpret_cast<const char*>(Xh + c0) : nullptr;
-      const uint32_t ldhb = (uint32_t)(ldh * (int64_t)sizeof(T));
-      int ra = 0;
-      while (ra < nr) {
-        if ((long_mask >> ra) & 1u) { ++ra; continue; }
-        const unsigned above = long_mask & ~((2u << ra) - 1u);
-        const int rb = above ? (__ffs(above) - 1) : nr;
-        const int64_t jb = s_rp[ra], je = s_rp[rb];
-        int cur = ra;
-        int64_t nxt = s_rp[ra + 1];
-        T* yrow = Y + (r0 + ra) * ldy + c0;
-        T acc[CPL];
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
-        // colind / values windows: my_* = the consumer's window, nx_* = the next
-        CI my_col = 0, nx_col = 0;
-        T my_val = T(0), nx_val = T(0);
-        if (jb + lane < je) { my_col = colind[jb + lane]; my_val = values[jb + lane]; }
-        if (jb + 32 + lane < je) { nx_col = colind[jb + 32 + lane]; nx_val = values[jb + 32 + lane]; }
-        const int64_t ngroups = (je - jb + RING_G - 1) / RING_G;
-        // group g's copies (entries jb + 8g .. +8), window col source w
-        auto issue = [&](int64_t g, CI wcol) {
-#pragma unroll
-          for (int i = 0; i < RING_G; ++i) {
-            const int64_t e = g * RING_G + i;  // relative entry
-            const CI col = __shfl_sync(0xffffffffu, wcol, (int)(e & 31));
-            if (jb + e < je) {
-              const uint32_t dst = ring_s + (uint32_t)(((e & (RING_ROWS - 1)) * 32) * SLICE);
-              if constexpr (HOT) {
-                const char* src = col >= 0 ? xbase + (uint64_t)(uint32_t)(col & ~SPMM_FAR_BIT) * ldxb
-                                           : hbase + (uint64_t)(uint32_t)(~col) * ldhb;
-                cp_async_slice<SLICE>(dst, src, pol_far, col >= 0 && (col & SPMM_FAR_BIT));
-              } else {
-                cp_async_slice<SLICE>(dst, xbase + (uint64_t)(uint32_t)col * ldxb, 0, false);
-              }
-            }
-          }
-          asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-#pragma unroll
-        for (int g = 0; g < RING_NG; ++g) issue(g, my_col);
-        for (int64_t g = 0; g < ngroups; ++g) {
-          if (g > 0 && (g & (RING_NG - 1)) == 0) {  // next 32-entry window
-            my_col = nx_col;
-            my_val = nx_val;
-            const int64_t w = jb + (g / RING_NG + 1) * 32 + lane;
-            nx_col = w < je ? colind[w] : CI(0);
-            nx_val = w < je ? values[w] : T(0);
-          }
-          asm volatile("cp.async.wait_group %0;" :: "n"(RING_NG - 1) : "memory");
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < RING_G; ++i) {
-            const int64_t e = g * RING_G + i;
-            const T v = __shfl_sync(0xffffffffu, my_val, (int)(e & 31));
-            if (jb + e < je) {
-              T xv[CPL];
-              const unsigned char* sp = ring + ((e & (RING_ROWS - 1)) * 32 + lane) * SLICE;
-              memcpy(xv, sp, SLICE);
-              while (jb + e == nxt) {  // rows that end here (empty rows included)
-                sty_row<T, CPL>(yrow, acc);
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
-                yrow += ldy;
-                ++cur;
-                nxt = s_rp[cur + 1];
-              }
-#pragma unroll
-              for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::add(acc[q], Arith<T>::mul(v, xv[q]));
-            }
-          }
-          __syncwarp();   // the group's slots are refilled below
-          issue(g + RING_NG, nx_col);
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        for (; cur < rb; ++cur) {
-          sty_row<T, CPL>(yrow, acc);
-          yrow += ldy;
-#pragma unroll
-          for (int q = 0; q < CPL; ++q) acc[q] = Arith<T>::zero();
-        }
-        ra = rb;
-      }
-    }
-  }
-}
-
-// LAPIS_B200_SPMM_RING=1: the ring kernel (cp.async X-row slices) for 8- and
-// 16-byte slices (A/B runs)
-inline bool spmm_ring() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LAPIS_B200_SPMM_RING");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 // gathers in flight per warp of the batch kernel: -1 = by element size
 // (default), else LAPIS_B200_SPMM_U = 8 / 16 / 32 (A/B runs)
 inline int spmm_u16() {
@@ -1264,44 +1102,7 @@ struct SpmmOp {
       }
       if (!fused) {
         if (W) return fail(LAPIS_B200_ERR_ARG, "gcn fused: fp32 only");
-        if (spmm_ring() && next && (cpl * (int)sizeof(T) == 8 || cpl * (int)sizeof(T) == 16)) {
-          auto launch_ring = [&](auto kern) -> int {
-            const int smem = RING_WARPS * RING_ROWS * 32 * cpl * (int)sizeof(T);
-            static int ctas[64] = {0};
-            int dev = 0;
-            cudaGetDevice(&dev);
-            if (dev < 0 || dev >= 64) dev = 0;
-            if (!ctas[dev]) {
-              LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                                "smem attr (spmm_ring_kernel)"));
-              int c = 0;
-              LB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kern, RING_WARPS * 32, smem),
-                                "occupancy"));
-              ctas[dev] = c < 1 ? 1 : c;
-            }
-            const int64_t g = std::min<int64_t>((int64_t)sms * ctas[dev], ((nrows + 31) / 32 + RING_WARPS - 1) / RING_WARPS);
-            kern<<<(unsigned)std::max<int64_t>(g, 1), RING_WARPS * 32, smem, st>>>(
-                nrows, k, (const RP*)rowptr, hot ? (const CI*)hot->colind : (const CI*)colind,
-                (const T*)values, (const T*)X, ldx, (T*)Y, ldy, next, fast,
-                hot ? (const T*)hot->xhot : nullptr, hot ? hot->ldh : 0);
-            return check_launch("spmm_ring_kernel");
-          };
-          // slices of 8 or 16 bytes: cpl 2 (both widths), 4 (4-byte), 1 (8-byte)
-          int rrc = fail(LAPIS_B200_ERR_ARG, "spmm ring: unsupported slice");
-          constexpr bool four = sizeof(T) == 4;
-          if (hot) {
-            if constexpr (std::is_same<CI, int32_t>::value) {
-              if (cpl == 2) rrc = launch_ring(spmm_ring_kernel<T, RP, int32_t, 2, true>);
-              else if constexpr (four) { if (cpl == 4) rrc = launch_ring(spmm_ring_kernel<T, RP, int32_t, 4, true>); }
-              else { if (cpl == 1) rrc = launch_ring(spmm_ring_kernel<T, RP, int32_t, 1, true>); }
-            }
-          } else {
-            if (cpl == 2) rrc = launch_ring(spmm_ring_kernel<T, RP, CI, 2, false>);
-            else if constexpr (four) { if (cpl == 4) rrc = launch_ring(spmm_ring_kernel<T, RP, CI, 4, false>); }
-            else { if (cpl == 1) rrc = launch_ring(spmm_ring_kernel<T, RP, CI, 1, false>); }
-          }
-          if (rrc != LAPIS_B200_OK) return rrc;
-        } else if (hot && next && pf <= 1) {
+        if (hot && next && pf <= 1) {
 #define LB_BATH(CC, PFV) spmm_batch2_kernel<T, RP, int32_t, CC, 8, PFV, true><<<(unsigned)gblocks, 256, 0, st>>>( \
           nrows, k, (const RP*)rowptr, hot->colind, (const T*)values, (const T*)X, ldx, (T*)Y, ldy, \
           next, fast, (const T*)hot->xhot, hot->ldh, spmm_far_prefetch())
