@@ -25,6 +25,8 @@ completes before the first chunk.  Results are those of the plan kernels
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import dualview as _dv
@@ -43,7 +45,9 @@ class StreamedSpmv:
         base = int(rowptr[0].item())
         nnz = int(rowptr[-1].item()) - base
         if chunks is None:   # ~256 MB of matrix per chunk, at most 16 chunks
-            chunks = min(16, max(1, (nnz * (values.element_size() + colind.element_size())) >> 28))
+            env = os.environ.get("LAPIS_B200_STREAM_CHUNKS")
+            cap = int(env) if env else 16
+            chunks = min(cap, max(1, (nnz * (values.element_size() + colind.element_size())) >> 28))
         chunks = max(1, min(chunks, nrows))
         # row boundaries at equal nonzero counts
         targets = torch.tensor([base + (nnz * c) // chunks for c in range(1, chunks)],
