@@ -60,6 +60,38 @@ def _():
     assert np.array_equal(y, O.spmv_csr(rs, cs, vs, xs))
 
 
+@case("spmv_rowstream")
+def _():
+    # TMA-staged tiles (27-point rows), the global-load fallback (ragged rows
+    # forced onto the kernel) and an unaligned operand (no bulk copies)
+    rs, cs, vs = S.stencil_rows(27, 11, 0, 1331)
+    xs = rng.uniform(-1, 1, 1331)
+    want = O.spmv_csr(rs, cs, vs, xs)
+    plan = lb.CsrPlan(cu(rs), exact=True)
+    assert plan.info()["rowstream"]
+    assert np.array_equal(plan.spmv(cu(cs.astype(np.int32)), cu(vs), cu(xs)).cpu().numpy(), want)
+    va = torch.cat([torch.zeros(1, dtype=torch.float64), torch.from_numpy(vs)]).cuda()[1:]
+    assert np.array_equal(plan.spmv(cu(cs.astype(np.int32)), va, cu(xs)).cpu().numpy(), want)
+    rp, ci, v = ragged_csr(rng, 700, 3000, max_len=60, long_rows={3: 2900})
+    x = rng.uniform(-1, 1, 3000)
+    os.environ["LAPIS_B200_SPMV_KERNEL"] = "rs"
+    y = lb.CsrPlan(cu(rp), exact=True).spmv(cu(ci), cu(v), cu(x)).cpu().numpy()
+    del os.environ["LAPIS_B200_SPMV_KERNEL"]
+    assert np.array_equal(y, O.spmv_csr(rp, ci, v, x))
+
+
+@case("spmm_plan_hints")
+def _():
+    # SpMM plan with hot rows and far-reuse hints (policy loads)
+    rp, ci = S.powerlaw_structure_host(S.PowerLawSpec(4000, mean=8.0, seed=3))
+    v = rng.uniform(-1, 1, int(rp[-1]))
+    X = rng.uniform(-1, 1, (4000, 64))
+    plan = lb.SpmmPlan(cu(rp), cu(ci), 4000, 64, torch.float64, hot_bytes=64 << 10)
+    assert plan.info()["far_reuse_entries"] >= 0
+    Y = plan.spmm(cu(v), cu(X)).cpu().numpy()
+    assert O.diff_outputs([Y], [O.spmm_csr(rp, ci, v, X)], 1e-12)[0]
+
+
 @case("row_fold_pipe")
 def _():
     A = rng.uniform(-1, 1, (300, 1030))
