@@ -1358,11 +1358,19 @@ static int spmm_reuse_hints(SpmmPlanImpl* p, const int32_t* c32, const int64_t* 
       if (q) cudaFreeAsync(q, st);
   };
   const size_t b = (size_t)nnz * 4;
-  int rc = check_cuda(cudaMallocAsync((void**)&keys, b, st), "alloc(hint keys)");
-  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&keys2, b, st), "alloc(hint keys)");
-  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&pos, b, st), "alloc(hint pos)");
-  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&pos2, b, st), "alloc(hint pos)");
-  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync((void**)&nfar, 8, st), "alloc(hint count)");
+  // the hints are optional: without room for the sort's 16 bytes per entry the
+  // plan goes without them (allocation failures are cleared, not reported)
+  bool room = cudaMallocAsync((void**)&keys, b, st) == cudaSuccess &&
+              cudaMallocAsync((void**)&keys2, b, st) == cudaSuccess &&
+              cudaMallocAsync((void**)&pos, b, st) == cudaSuccess &&
+              cudaMallocAsync((void**)&pos2, b, st) == cudaSuccess &&
+              cudaMallocAsync((void**)&nfar, 8, st) == cudaSuccess;
+  if (!room) {
+    cudaGetLastError();
+    cleanup();
+    return LAPIS_B200_OK;
+  }
+  int rc = LAPIS_B200_OK;
   if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMemsetAsync(nfar, 0, 8, st), "memset(hint count)");
   const int sms = num_sms();
   const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nnz + 255) / 256, (int64_t)sms * 8));
@@ -1373,7 +1381,11 @@ static int spmm_reuse_hints(SpmmPlanImpl* p, const int32_t* c32, const int64_t* 
   if (rc == LAPIS_B200_OK)
     rc = check_cuda(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, pos, pos2,
                                                     (int)nnz, 0, end_bit, st), "radix sort (size)");
-  if (rc == LAPIS_B200_OK) rc = check_cuda(cudaMallocAsync(&tmp, tmp_bytes, st), "alloc(sort)");
+  if (rc == LAPIS_B200_OK && cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    return LAPIS_B200_OK;
+  }
   if (rc == LAPIS_B200_OK)
     rc = check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, pos, pos2,
                                                     (int)nnz, 0, end_bit, st), "radix sort");
