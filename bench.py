@@ -850,8 +850,8 @@ def powerlaw_config(key, n, k, seed, world, extra=None):
 
 
 class DenseMatmul(Workload):
-    """Config 2: dense linalg.matmul 4096^3 (f32: 3xTF32; f64: certified
-    Ozaki on the int8 tensor cores).  N > 1: row blocks of A
+    """Config 2: dense linalg.matmul 4096^3 (f32: sign-gated Ozaki, 3xTF32 for
+    operands with negative entries; f64: certified Ozaki on the int8 tensor cores).  N > 1: row blocks of A
     and C (sharded.RowBlockGemm), B replicated by one broadcast when the
     operator is built (not part of a step); strong scaling."""
 
@@ -898,7 +898,9 @@ class DenseMatmul(Workload):
         if self.mode != "auto":
             return self.mode
         if self.dt == torch.float32:
-            return "tf32x3"
+            # AUTO f32: the sign-gated Ozaki path for non-negative operands
+            # (config 2's U(0, 1) inputs) while k is in its certified range
+            return "ozaki" if 3 * self.n * 65025 < 2 ** 31 else "tf32x3"
         return "ozaki" if self.n * 9.0 * 2.0 ** -56 <= 0.75e-12 else "dmma"
 
     def kernel_name(self):

@@ -65,6 +65,7 @@ struct OzParams {
   double cert_k;            // error bound per unit 2^(ea+eb): K * per-product bound
   double cert_tol;          // certified |C - exact| <= cert_tol * max(|C|, 1)
   bool vec2;                // 16-byte partial accesses (even pitch, aligned)
+  int sign_gate;            // 1: a negative operand entry (split kernels raise flag[1]) skips the kernel
   unsigned long long* prof; // optional: wait-cycle counters (LAPIS_B200_OZAKI_PROF=1)
   int digits8;              // 1: signed 8-bit leading digit + unsigned 8-bit digits
   // last-wave split (tiles >= split_base): the owner CTA runs the diagonals in
@@ -211,7 +212,7 @@ template <class OUT, int OZ_BN>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                   OzParams p) {
-  if (*p.flag) return;  // uniform: the guarded fallback owns this call
+  if (p.flag[0] || (p.sign_gate && p.flag[1])) return;  // uniform: a guarded fallback owns this call
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[OZ_STAGES], empty[OZ_STAGES], tmem_full[2], tmem_empty[2];
@@ -436,11 +437,18 @@ __device__ __forceinline__ void oz2_tile(int tile, int num_m, int num_n, int& mb
   nb = t / rows;
 }
 
-template <class OUT>
+// NPASS = 2, SD = 8 (fp64, 7-bit signed digits) as described above; NPASS = 1,
+// SD = 3, D8 (fp32, 8-bit digits: signed leading, unsigned others): pass A
+// alone covers all 3 diagonals (6 products per K block) — the K blocks'
+// digit tiles are streamed once, against 1 + 2 + 3 re-streamed K passes in
+// the per-diagonal kernel.
+template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      OzParams p) {
-  if (*p.flag) return;  // uniform: the guarded fallback owns this call
+  static_assert((NPASS == 2 && SD == 8) || (NPASS == 1 && SD <= 4), "pass layout");
+  constexpr int DA = SD < 4 ? SD : 4;   // diagonals of pass A
+  if (p.flag[0] || (p.sign_gate && p.flag[1])) return;  // uniform: a guarded fallback owns this call
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[OZ2_STAGES], empty[OZ2_STAGES], acc_full, acc_empty;
@@ -486,7 +494,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           }
           if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
         }
-        for (int kb = 0; kb < nk; ++kb) {          // pass B: one K block, all 8 digits
+        for (int kb = 0; kb < (NPASS == 2 ? nk : 0); ++kb) {   // pass B: one K block, all 8 digits
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * OZ2_STAGE;
           mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
@@ -502,12 +510,16 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
     // ------------------------------------------------------------ MMA issuer
     // (the whole warp runs the loop, one elected lane issues)
     constexpr uint32_t idesc = i8_idesc(OZ_BM, OZ2_BN, true, true);
+    // 8-bit digits: digit 0 signed, the others unsigned
+    constexpr uint32_t idesc_su = i8_idesc(OZ_BM, OZ2_BN, true, false);
+    constexpr uint32_t idesc_us = i8_idesc(OZ_BM, OZ2_BN, false, true);
+    constexpr uint32_t idesc_uu = i8_idesc(OZ_BM, OZ2_BN, false, false);
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
     long long w_tmem = 0, w_full = 0;
     const long long t_start = clock64();
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      for (int pass = 0; pass < 2; ++pass) {
+      for (int pass = 0; pass < NPASS; ++pass) {
         long long t0 = p.prof ? clock64() : 0;
         mbar_wait(&acc_empty, acc_phase ^ 1);
         if (p.prof) w_tmem += clock64() - t0;
@@ -525,12 +537,14 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
 #pragma unroll
               for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int d = 0; d < 4; ++d)
+                for (int d = 0; d < DA; ++d)
 #pragma unroll
                   for (int s = 0; s <= d; ++s)
                     tc_mma_i8(tmem_base + (uint32_t)(d * OZ2_BN),
                               desc0 + (uint64_t)(((h * 8 + s) * OZ2_DIGIT) >> 4),
-                              desc0 + (uint64_t)(((h * 8 + 4 + d - s) * OZ2_DIGIT) >> 4), idesc,
+                              desc0 + (uint64_t)(((h * 8 + 4 + d - s) * OZ2_DIGIT) >> 4),
+                              !D8 ? idesc : (s == 0 ? (d == 0 ? idesc : idesc_su)
+                                                    : (d - s == 0 ? idesc_us : idesc_uu)),
                               (j > 0 || h > 0 || s > 0) ? 1u : 0u);
             } else {
 #pragma unroll
@@ -572,7 +586,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
       const int row = row_base + lane;
       const int ea = row < p.m ? __ldg(p.ea + row) : 0;
       const uint32_t tbase = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(half * 64);
-      for (int pass = 0; pass < 2; ++pass) {
+      for (int pass = 0; pass < NPASS; ++pass) {
         mbar_wait(&acc_full, acc_phase);
         acc_phase ^= 1;
         tc_fence_after();
@@ -588,11 +602,11 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
             for (int j = 0; j < 16; ++j) y[j] = slot[(c * 16 + j) * 32];
           }
 #pragma unroll 1
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < (pass == 0 ? DA : 4); ++q) {
             const int d = pass * 4 + q;
             uint32_t v[16];
             tmem_ld_x16(tbase + (uint32_t)(q * OZ2_BN + c * 16), v);
-            const int shift = ea - 7 * (d + 2);
+            const int shift = D8 ? ea - 14 - 8 * d : ea - 7 * (d + 2);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const double x = pow2_scale((double)(int)v[j], shift + e[j]);
@@ -635,7 +649,10 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           if (gr >= p.m) continue;
           OUT* dst = reinterpret_cast<OUT*>(p.C) + (int64_t)gr * p.ldc + gc;
           if (p.vec2 && gc + 1 < p.n) {
-            *reinterpret_cast<double2*>(dst) = t;
+            if constexpr (sizeof(OUT) == 8)
+              *reinterpret_cast<double2*>(dst) = t;
+            else
+              *reinterpret_cast<float2*>(dst) = make_float2((float)t.x, (float)t.y);
           } else {
             if (gc < p.n) dst[0] = (OUT)t.x;
             if (gc + 1 < p.n) dst[1] = (OUT)t.y;
@@ -690,6 +707,19 @@ __device__ __forceinline__ void peel4_u8(double r0, double r1, double r2, double
                                          int8_t* __restrict__ out, int64_t plane) {
   const double r[4] = {r0, r1, r2, r3};
   const double scale = __hiloint2double((7 + 8 * (S - 1) + 1023) << 20, 0);
+  if (S <= 3) {   // |q| < 2^23: one rounding-down conversion to int32 per element
+    int qi[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) qi[c] = __double2int_rd(r[c] * scale);
+    for (int s = 0; s < S; ++s) {
+      const int sh = 8 * (S - 1 - s);
+      uint32_t w = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) w |= (uint32_t)((qi[c] >> sh) & 0xff) << (8 * c);
+      *reinterpret_cast<uint32_t*>(out + (int64_t)s * plane) = w;
+    }
+    return;
+  }
   long long q[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) q[c] = (long long)floor(r[c] * scale);
@@ -718,20 +748,29 @@ template <class T>
 __global__ void __launch_bounds__(256)
 ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restrict__ A,
                  int64_t lda, int S, int8_t* __restrict__ out, int* __restrict__ e_out,
-                 int* __restrict__ flag, int digits8) {
+                 int* __restrict__ flag, int digits8, int sign_gate) {
   __shared__ double red[8];
   const int64_t plane = mp * kp;
   for (int64_t i = blockIdx.x; i < mp; i += gridDim.x) {
+    // sign gate: once any CTA saw a negative entry the split is moot
+    if (sign_gate && *(volatile const int*)(flag + 1)) return;
     const T* arow = A + i * lda;
     double mx = 0.0;
-    bool bad = false;
-    if (i < m)
-      for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    bool bad = false, neg = false;
+    if (i < m) {
+#pragma unroll 8
+      for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {   // 8 loads in flight per thread
         const double v = (double)arow[j];
         bad |= !isfinite(v);
+        neg |= v < 0.0;
         mx = fmax(mx, fabs(v));
       }
+    }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+    if (sign_gate && __syncthreads_or(neg)) {  // gate tripped: no digits needed
+      if (threadIdx.x == 0) atomicExch(flag + 1, 1);
+      return;
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -742,15 +781,111 @@ ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restri
     const int e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) + 1 : 0;
     if (threadIdx.x == 0 && i < m) e_out[i] = e;
     int8_t* orow = out + i * kp;
+    // fp32 rows with a 16-byte pitch: one 16-byte load per 4 elements
+    const bool vec4 = sizeof(T) == 4 && (lda % 4 == 0) && ((uintptr_t)A % 16 == 0);
+#pragma unroll 2
     for (int64_t j = 4 * (int64_t)threadIdx.x; j < kp; j += 4 * (int64_t)blockDim.x) {
       double r[4];
+      if (vec4 && i < m && j + 3 < k) {
+        const float4 f = *reinterpret_cast<const float4*>(arow + j);
+        const float fv[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double v = (i < m && j + q < k) ? (double)arow[j + q] : 0.0;
-        r[q] = isfinite(v) ? scale_down(v, e) : 0.0;
+        for (int q = 0; q < 4; ++q) r[q] = isfinite(fv[q]) ? scale_down((double)fv[q], e) : 0.0;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double v = (i < m && j + q < k) ? (double)arow[j + q] : 0.0;
+          r[q] = isfinite(v) ? scale_down(v, e) : 0.0;
+        }
       }
       if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, orow + j, plane);
       else peel4(r[0], r[1], r[2], r[3], S, orow + j, plane);
+    }
+  }
+}
+
+// fp32 rows, 8-bit digits, S <= 3 (|floor(r 2^23)| < 2^23): the same digits
+// as ozaki_split_rows in single-precision and 32-bit integer arithmetic — the
+// scaling by 2^(7 + 8(S-1) - e) is two exact multiplies by powers of two (the
+// product only rounds when it underflows, below the digits' resolution), one
+// rounding-down conversion per element, byte planes by shifts; no fp64
+// conversions and no 64-bit index arithmetic in the element loop
+__device__ __forceinline__ float pow2f(int e) {   // 2^e for e in [-126, 127]
+  return __int_as_float((e + 127) << 23);
+}
+__global__ void __launch_bounds__(256)
+ozaki_split_rows_f32(int64_t m, int64_t k, int64_t kp, int64_t mp, const float* __restrict__ A,
+                     int64_t lda, int S, int8_t* __restrict__ out, int* __restrict__ e_out,
+                     int* __restrict__ flag, int sign_gate) {
+  __shared__ float red[8];
+  const int64_t plane = mp * kp;
+  const int kk = (int)k, kpp = (int)kp;
+  const bool vec4 = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0) && (kk % 4 == 0);
+  for (int64_t i = blockIdx.x; i < mp; i += gridDim.x) {
+    if (sign_gate && *(volatile const int*)(flag + 1)) return;
+    const float* arow = A + i * lda;
+    float mx = 0.0f;
+    bool bad = false, neg = false;
+    if (i < m) {
+      if (vec4) {
+#pragma unroll 4
+        for (int j = 4 * threadIdx.x; j < kk; j += 4 * blockDim.x) {
+          const float4 f = *reinterpret_cast<const float4*>(arow + j);
+          const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            bad |= !isfinite(fv[q]);
+            neg |= fv[q] < 0.0f;
+            mx = fmaxf(mx, fabsf(fv[q]));
+          }
+        }
+      } else {
+#pragma unroll 8
+        for (int j = threadIdx.x; j < kk; j += blockDim.x) {
+          const float v = arow[j];
+          bad |= !isfinite(v);
+          neg |= v < 0.0f;
+          mx = fmaxf(mx, fabsf(v));
+        }
+      }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+    if (sign_gate && __syncthreads_or(neg)) {
+      if (threadIdx.x == 0) atomicExch(flag + 1, 1);
+      return;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();
+    const int e = (mx > 0.0f && isfinite(mx)) ? ilogbf(mx) + 1 : 0;
+    if (threadIdx.x == 0 && i < m) e_out[i] = e;
+    const int sh_all = 7 + 8 * (S - 1) - e;            // scale 2^sh_all = p1 * p2
+    const int e1 = min(max(sh_all, -126), 127), e2 = min(max(sh_all - e1, -126), 127);
+    const float p1 = pow2f(e1), p2 = pow2f(e2);
+    uint32_t* o0 = reinterpret_cast<uint32_t*>(out + i * kp);
+    for (int j = 4 * threadIdx.x; j < kpp; j += 4 * blockDim.x) {
+      float fv[4];
+      if (i < m && vec4 && j + 3 < kk) {
+        const float4 f = *reinterpret_cast<const float4*>(arow + j);
+        fv[0] = f.x; fv[1] = f.y; fv[2] = f.z; fv[3] = f.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fv[q] = (i < m && j + q < kk) ? arow[j + q] : 0.0f;
+      }
+      int qi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) qi[q] = isfinite(fv[q]) ? __float2int_rd(fv[q] * p1 * p2) : 0;
+      for (int s = 0; s < S; ++s) {
+        const int sh = 8 * (S - 1 - s);
+        uint32_t w = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w |= (uint32_t)((qi[q] >> sh) & 0xff) << (8 * q);
+        o0[(s * plane + j) >> 2] = w;
+      }
     }
   }
 }
@@ -759,18 +894,23 @@ ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restri
 // for non-negative doubles); NaN/inf raise the flag
 template <class T>
 __global__ void ozaki_colmax(int64_t k, int64_t n, const T* __restrict__ B, int64_t ldb,
-                             unsigned long long* __restrict__ colmax, int* __restrict__ flag) {
+                             unsigned long long* __restrict__ colmax, int* __restrict__ flag,
+                             int sign_gate) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
+  if (sign_gate && *(volatile const int*)(flag + 1)) return;
   const int64_t k0 = (int64_t)blockIdx.y * 64, k1 = k0 + 64 < k ? k0 + 64 : k;
   double mx = 0.0;
-  bool bad = false;
-  for (int64_t r = k0; r < k1; ++r) {
+  bool bad = false, neg = false;
+#pragma unroll 8
+  for (int64_t r = k0; r < k1; ++r) {   // 8 rows in flight per thread
     const double v = (double)B[r * ldb + j];
     bad |= !isfinite(v);
+    neg |= v < 0.0;
     mx = fmax(mx, fabs(v));
   }
   if (bad) atomicExch(flag, 1);
+  if (sign_gate && neg) atomicExch(flag + 1, 1);
   atomicMax(colmax + j, (unsigned long long)__double_as_longlong(mx));
 }
 
@@ -782,11 +922,18 @@ template <class T>
 __global__ void __launch_bounds__(256)
 ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restrict__ B,
                  int64_t ldb, int S, const unsigned long long* __restrict__ colmax,
-                 int8_t* __restrict__ out, int* __restrict__ e_out, int digits8) {
+                 int8_t* __restrict__ out, int* __restrict__ e_out, int digits8,
+                 const int* __restrict__ gate = nullptr) {
+  if (gate && *(volatile const int*)gate) return;  // sign gate tripped (flag[1])
   // column c of row r lives at tile[r][c ^ (r / 4 % 32)]: the row-wise fill and
   // the 4-rows-per-lane column reads below are both free of bank conflicts
   __shared__ double tile[128][32];
-  const int64_t k0 = (int64_t)blockIdx.y * 128, n0 = (int64_t)blockIdx.x * 32;
+  // a bounded grid walks the (n, k) tiles: a gated launch costs one wave
+  const int64_t gxn = (np + 31) / 32, tiles = gxn * ((kp + 127) / 128);
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  const int64_t by = t / gxn, bx = t % gxn;
+  const int64_t k0 = by * 128, n0 = bx * 32;
+  __syncthreads();   // the previous tile's reads of `tile` are done
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
 #pragma unroll
   for (int r = ty; r < 128; r += 8) {
@@ -805,7 +952,7 @@ ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restri
     if (nn < n) {
       const double mx = __longlong_as_double((long long)colmax[nn]);
       e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) + 1 : 0;
-      if (blockIdx.y == 0 && tx == 0) e_out[nn] = e;
+      if (by == 0 && tx == 0) e_out[nn] = e;
     }
     double r[4];
 #pragma unroll
@@ -813,6 +960,101 @@ ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restri
     if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
     else peel4(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
   }
+  }
+}
+
+// fp32 B, 8-bit digits, S <= 3: ozaki_colmax / ozaki_split_cols in single
+// precision (see ozaki_split_rows_f32); the column maxima are kept as the
+// fp64 bit patterns the fp64 kernels use
+__global__ void ozaki_colmax_f32(int64_t k, int64_t n, const float* __restrict__ B, int64_t ldb,
+                                 unsigned long long* __restrict__ colmax, int* __restrict__ flag,
+                                 int sign_gate) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  if (sign_gate && *(volatile const int*)(flag + 1)) return;
+  const int64_t k0 = (int64_t)blockIdx.y * 64, k1 = k0 + 64 < k ? k0 + 64 : k;
+  float mx = 0.0f;
+  bool bad = false, neg = false;
+  const float* col = B + j;
+#pragma unroll 16
+  for (int64_t r = k0; r < k1; ++r) {
+    const float v = col[r * ldb];
+    bad |= !isfinite(v);
+    neg |= v < 0.0f;
+    mx = fmaxf(mx, fabsf(v));
+  }
+  if (bad) atomicExch(flag, 1);
+  if (sign_gate && neg) atomicExch(flag + 1, 1);
+  atomicMax(colmax + j, (unsigned long long)__double_as_longlong((double)mx));
+}
+
+__global__ void __launch_bounds__(256)
+ozaki_split_cols_f32(int64_t k, int64_t n, int64_t kp, int64_t np, const float* __restrict__ B,
+                     int64_t ldb, int S, const unsigned long long* __restrict__ colmax,
+                     int8_t* __restrict__ out, int* __restrict__ e_out,
+                     const int* __restrict__ gate = nullptr) {
+  if (gate && *(volatile const int*)gate) return;
+  __shared__ float tile[128][32];   // column c of row r at [r][c ^ (r / 4 % 32)]: conflict-free
+  const int64_t gxn = (np + 31) / 32, tiles = gxn * ((kp + 127) / 128);
+  const int64_t plane = np * kp;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t by = t / gxn, bx = t % gxn;
+    const int64_t k0 = by * 128, n0 = bx * 32;
+    __syncthreads();
+#pragma unroll 8
+    for (int r = ty; r < 128; r += 8) {
+      const int64_t kk = k0 + r, nn = n0 + tx;
+      const float v = (kk < k && nn < n) ? B[kk * ldb + nn] : 0.0f;
+      tile[r][tx ^ ((r >> 2) & 31)] = isfinite(v) ? v : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int cc = 4 * ty + c;
+      const int64_t nn = n0 + cc;
+      const int64_t kk = k0 + 4 * tx;
+      if (nn >= np || kk >= kp) continue;
+      int e = 0;
+      if (nn < n) {
+        const double mx = __longlong_as_double((long long)colmax[nn]);
+        e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) + 1 : 0;
+        if (by == 0 && tx == 0) e_out[nn] = e;
+      }
+      const int sh_all = 7 + 8 * (S - 1) - e;
+      const int e1 = min(max(sh_all, -126), 127), e2 = min(max(sh_all - e1, -126), 127);
+      const float p1 = pow2f(e1), p2 = pow2f(e2);
+      int qi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        qi[q] = (nn < n) ? __float2int_rd(tile[4 * tx + q][cc ^ tx] * p1 * p2) : 0;
+      for (int s2 = 0; s2 < S; ++s2) {
+        const int sh = 8 * (S - 1 - s2);
+        uint32_t w = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w |= (uint32_t)((qi[q] >> sh) & 0xff) << (8 * q);
+        *reinterpret_cast<uint32_t*>(out + s2 * plane + nn * kp + kk) = w;
+      }
+    }
+  }
+}
+
+// sign gate probe: any negative among the first `rows` rows of A and of B
+// raises flag[1] before the split kernels start (mixed-sign operands then
+// skip the digit split at the cost of one small read)
+template <class T>
+__global__ void ozaki_sign_probe(int64_t m, int64_t k, const T* __restrict__ A, int64_t lda,
+                                 int64_t kb, int64_t n, const T* __restrict__ B, int64_t ldb,
+                                 int64_t rows, int* __restrict__ flag) {
+  // CTA c < rows: row c of A; rows <= c < 2 rows: row c - rows of B
+  bool neg = false;
+  const int64_t c = blockIdx.x;
+  if (c < rows && c < m) {
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) neg |= A[c * lda + j] < T(0);
+  } else if (c >= rows && c - rows < kb) {
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) neg |= B[(c - rows) * ldb + j] < T(0);
+  }
+  if (__syncthreads_or(neg) && threadIdx.x == 0) atomicExch(flag + 1, 1);
 }
 
 // -------------------------------------------------------------- host side
@@ -861,18 +1103,21 @@ int ozaki_slices_for(int dtype, int64_t k) {
   return 0;
 }
 
+template <class T>
 static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& prm,
                            int grid, cudaStream_t st) {
+  // fp64: two passes, 8 digits; fp32: one pass, 3 digits of 8 bits
+  auto kern = std::is_same<T, double>::value ? gemm_ozaki_2p_kernel<double, 2, 8, false>
+                                             : gemm_ozaki_2p_kernel<float, 1, 3, true>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    LB_TRY(check_cuda(cudaFuncSetAttribute(gemm_ozaki_2p_kernel<double>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ2_SMEM),
-                      "smem attr (gemm_ozaki_2p_kernel)"));
+    LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)OZ2_SMEM), "smem attr (gemm_ozaki_2p_kernel)"));
     configured_dev = dev;
   }
-  gemm_ozaki_2p_kernel<double><<<grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, prm);
+  kern<<<grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, prm);
   return check_launch("gemm_ozaki_2p_kernel");
 }
 
@@ -880,7 +1125,7 @@ static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const O
 template <class T, int BN, bool TWO_PASS = false>
 static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-                        int64_t sC, int S, cudaStream_t st) {
+                        int64_t sC, int S, cudaStream_t st, int sign_gate = 0) {
   if (m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(LAPIS_B200_ERR_ARG, "gemm ozaki: extent too large");
   if (S < 1 || S > OZ_MAX_S) return fail(LAPIS_B200_ERR_ARG, "gemm ozaki: bad slice count");
@@ -965,12 +1210,32 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
       rc = check_cuda(cudaMemsetAsync(flag, 0, 2 * sizeof(int) + flag_bytes, st), "memset(flag)");
     if (rc != LAPIS_B200_OK) break;
     const int64_t rblocks = std::min<int64_t>(mp, (int64_t)num_sms() * 16);
-    ozaki_split_rows<T><<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
-                                                           digits8);
+    if (sign_gate)
+      ozaki_sign_probe<T><<<2 * 64, 256, 0, st>>>(m, k, Ab, lda, k, n, Bb, ldb, 64, flag);
+    if constexpr (std::is_same<T, float>::value) {
+      if (digits8 && S <= 3 && kp % 4 == 0 && (mp * kp) % 4 == 0)
+        ozaki_split_rows_f32<<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
+                                                                sign_gate);
+      else
+        ozaki_split_rows<T><<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
+                                                               digits8, sign_gate);
+    } else {
+      ozaki_split_rows<T><<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
+                                                             digits8, sign_gate);
+    }
     dim3 cg((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
-    ozaki_colmax<T><<<cg, 256, 0, st>>>(k, n, Bb, ldb, colmax, flag);
-    dim3 tg((unsigned)((np + 31) / 32), (unsigned)((kp + 127) / 128));
-    ozaki_split_cols<T><<<tg, 256, 0, st>>>(k, n, kp, np, Bb, ldb, S, colmax, bd, eb, digits8);
+    const int64_t tg = ((np + 31) / 32) * ((kp + 127) / 128);
+    bool f32fast = false;
+    if constexpr (std::is_same<T, float>::value) f32fast = digits8 && S <= 3;
+    if (f32fast) {
+      ozaki_colmax_f32<<<cg, 256, 0, st>>>(k, n, (const float*)Bb, ldb, colmax, flag, sign_gate);
+      ozaki_split_cols_f32<<<(unsigned)tg, 256, 0, st>>>(k, n, kp, np, (const float*)Bb, ldb, S, colmax,
+                                                         bd, eb, sign_gate ? flag + 1 : nullptr);
+    } else {
+      ozaki_colmax<T><<<cg, 256, 0, st>>>(k, n, Bb, ldb, colmax, flag, sign_gate);
+      ozaki_split_cols<T><<<(unsigned)tg, 256, 0, st>>>(k, n, kp, np, Bb, ldb, S, colmax, bd, eb,
+                                                        digits8, sign_gate ? flag + 1 : nullptr);
+    }
     rc = check_launch("ozaki split");
     CUtensorMap ma, mb;
     if (TWO_PASS) {
@@ -1014,6 +1279,7 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
       prm.cert_tol = 0.75 * (std::is_same<T, double>::value ? 1e-12 : 1e-5);
     }
     prm.digits8 = digits8;
+    prm.sign_gate = sign_gate;
     prm.vec2 = (prm.ldp % 2 == 0) && ((uintptr_t)prm.part % 16 == 0);
     static const bool prof_on = [] {
       const char* e = getenv("LAPIS_B200_OZAKI_PROF");
@@ -1027,8 +1293,8 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
     prm.prof = dprof;
     if constexpr (TWO_PASS) {
       prm.nk = (int)((kp + OZ2_BK - 1) / OZ2_BK);
-      prm.vec2 = ((uintptr_t)Cb % 16 == 0) && (ldc % 2 == 0);
-      rc = launch_ozaki_2p(ma, mb, prm, std::min(tiles, sms), st);
+      prm.vec2 = ((uintptr_t)Cb % (2 * sizeof(T)) == 0) && (ldc % 2 == 0);
+      rc = launch_ozaki_2p<T>(ma, mb, prm, std::min(tiles, sms), st);
     } else {
       gemm_ozaki_kernel<T, BN><<<grid, OZ_THREADS, OzTile<BN>::SMEM, st>>>(ma, mb, prm);
       rc = check_launch("gemm_ozaki_kernel");
@@ -1060,7 +1326,7 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
 
 int gemm_ozaki(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                const void* B, int64_t ldb, void* C, int64_t ldc, int64_t sA, int64_t sB,
-               int64_t sC, int dtype, int slices, cudaStream_t st) {
+               int64_t sC, int dtype, int slices, cudaStream_t st, int sign_gate) {
   const int S = slices > 0 ? slices : ozaki_slices_for(dtype, k);
   if (S == 0) return fail(LAPIS_B200_ERR_UNSUPPORTED, "gemm ozaki: k out of the certified range");
   static const int bn_env = [] {
@@ -1076,7 +1342,18 @@ int gemm_ozaki(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, in
   }();
   if (two_pass && dtype == LAPIS_B200_F64 && S == 8)
     return gemm_ozaki_t<double, OZ2_BN, true>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st);
-#define LB_OZ(T, BN_) return gemm_ozaki_t<T, BN_>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st)
+  // fp32, S = 3 through the same kernel in one pass (LAPIS_B200_OZAKI_1P=1):
+  // correct, but 0.747 vs 0.595 ms for the per-diagonal kernel at 4096^3 — the
+  // three diagonals fill 384 TMEM columns, so each tile's drain stalls the
+  // MMAs, while the per-diagonal kernel double-buffers its accumulators
+  static const bool one_pass = [] {
+    const char* e = getenv("LAPIS_B200_OZAKI_1P");
+    return e && e[0] == '1';
+  }();
+  if (one_pass && dtype == LAPIS_B200_F32 && S == 3)
+    return gemm_ozaki_t<float, OZ2_BN, true>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st,
+                                             sign_gate);
+#define LB_OZ(T, BN_) return gemm_ozaki_t<T, BN_>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st, sign_gate)
   if (dtype == LAPIS_B200_F64) { if (bn == 192) LB_OZ(double, 192); LB_OZ(double, 256); }
   if (dtype == LAPIS_B200_F32) { if (bn == 256) LB_OZ(float, 256); LB_OZ(float, 192); }
 #undef LB_OZ
