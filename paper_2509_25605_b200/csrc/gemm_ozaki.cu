@@ -442,13 +442,19 @@ __device__ __forceinline__ void oz2_tile(int tile, int num_m, int num_n, int& mb
 // alone covers all 3 diagonals (6 products per K block) — the K blocks'
 // digit tiles are streamed once, against 1 + 2 + 3 re-streamed K passes in
 // the per-diagonal kernel.
-template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false>
+// CL: launched as clusters of two CTAs that take the two row blocks of one
+// column block at a time; each CTA loads its own A digit tiles and HALF of
+// the shared B digit tiles, multicast into both CTAs' shared memory (the B
+// operand stream from L2 halves); a stage is refilled once both CTAs' MMAs
+// released it (empty barriers count two commits, each multicast to the pair).
+template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false, bool CL = false>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      OzParams p) {
   static_assert((NPASS == 2 && SD == 8) || (NPASS == 1 && SD <= 4), "pass layout");
   constexpr int DA = SD < 4 ? SD : 4;   // diagonals of pass A
   if (p.flag[0] || (p.sign_gate && p.flag[1])) return;  // uniform: a guarded fallback owns this call
+  const uint32_t crank = CL ? cluster_ctarank() : 0u;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[OZ2_STAGES], empty[OZ2_STAGES], acc_full, acc_empty;
@@ -456,11 +462,24 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.num_m * p.num_n;
   const int nk = p.nk, nk2 = (p.nk + 1) / 2;
+  // work units: tiles, or (CL) pairs of row blocks sharing a column block
+  const int units = CL ? total / 2 : total;
+  const int ustart = CL ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustride = CL ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  auto unit_tile = [&](int u, int& mb, int& nb) {
+    if (CL) {
+      int mbp;
+      oz2_tile(u, p.num_m / 2, p.num_n, mbp, nb);
+      mb = 2 * mbp + (int)crank;
+    } else {
+      oz2_tile(u, p.num_m, p.num_n, mb, nb);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tA);
     prefetch_tmap(&tB);
-    for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL ? 2 : 1); }
     mbar_init(&acc_full, 1);
     mbar_init(&acc_empty, OZ_EPI_WARPS * 32);
     fence_barrier_init();
@@ -473,6 +492,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (CL) cluster_sync_all();   // the peer's barriers exist before any multicast
   const uint32_t tmem_base = tmem_base_slot;
 
   if (warp == 0) {
@@ -480,9 +500,18 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
       // ------------------------------------------------------------ producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      // B box b of a stage: loaded here (plain), or (CL) by the CTA of rank
+      // b % 2 for both CTAs of the pair
+      auto load_b = [&](void* dst, int kx, int nbn, int dz, int b) {
+        if constexpr (CL) {
+          if ((b & 1) == (int)crank) tma_load_3d_mc(dst, &tB, kx, nbn, dz, &full[stage], (uint16_t)0x3);
+        } else {
+          tma_load_3d(dst, &tB, kx, nbn, dz, &full[stage]);
+        }
+      };
+      for (int u = ustart; u < units; u += ustride) {
         int mb, nb;
-        oz2_tile(tile, p.num_m, p.num_n, mb, nb);
+        unit_tile(u, mb, nb);
         const int ma = mb * OZ_BM, nbn = nb * OZ2_BN;
         for (int j = 0; j < nk2; ++j) {            // pass A: K blocks 2j, 2j+1 (zero-filled past K)
           mbar_wait(&empty[stage], phase ^ 1);
@@ -490,7 +519,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
           for (int h = 0; h < 2; ++h) {
             tma_load_3d(sa + h * 8 * OZ2_DIGIT, &tA, (2 * j + h) * OZ2_BK, ma, 0, &full[stage]);
-            tma_load_3d(sa + h * 8 * OZ2_DIGIT + 4 * OZ2_DIGIT, &tB, (2 * j + h) * OZ2_BK, nbn, 0, &full[stage]);
+            load_b(sa + h * 8 * OZ2_DIGIT + 4 * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
           }
           if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
         }
@@ -500,8 +529,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
           tma_load_3d(sa, &tA, kb * OZ2_BK, ma, 0, &full[stage]);
           tma_load_3d(sa + 4 * OZ2_DIGIT, &tA, kb * OZ2_BK, ma, 4, &full[stage]);
-          tma_load_3d(sa + 8 * OZ2_DIGIT, &tB, kb * OZ2_BK, nbn, 0, &full[stage]);
-          tma_load_3d(sa + 12 * OZ2_DIGIT, &tB, kb * OZ2_BK, nbn, 4, &full[stage]);
+          load_b(sa + 8 * OZ2_DIGIT, kb * OZ2_BK, nbn, 0, 0);
+          load_b(sa + 12 * OZ2_DIGIT, kb * OZ2_BK, nbn, 4, 1);
           if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -518,7 +547,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
     uint32_t phase = 0, acc_phase = 0;
     long long w_tmem = 0, w_full = 0;
     const long long t_start = clock64();
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (int u = ustart; u < units; u += ustride) {
       for (int pass = 0; pass < NPASS; ++pass) {
         long long t0 = p.prof ? clock64() : 0;
         mbar_wait(&acc_empty, acc_phase ^ 1);
@@ -556,7 +585,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
                             desc0 + (uint64_t)(((8 + d - s) * OZ2_DIGIT) >> 4), idesc,
                             (j > 0 || s > 0) ? 1u : 0u);
             }
-            tc_commit(&empty[stage]);
+            if constexpr (CL) tc_commit_mc(&empty[stage], (uint16_t)0x3);
+            else tc_commit(&empty[stage]);
           }
           __syncwarp();
           if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
@@ -579,9 +609,9 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
     // this warp's partial in the CTA's slot: [chunk][j][lane], coalesced per j
     double* slot = p.split_ws + (int64_t)blockIdx.x * OZ2_SLOT + ew * (4 * 16 * 32) + lane;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (int u = ustart; u < units; u += ustride) {
       int mb, nb;
-      oz2_tile(tile, p.num_m, p.num_n, mb, nb);
+      unit_tile(u, mb, nb);
       const int row_base = mb * OZ_BM + lg * 32;
       const int row = row_base + lane;
       const int ea = row < p.m ? __ldg(p.ea + row) : 0;
@@ -664,6 +694,9 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
+  // (CL) no CTA leaves while its peer may still multicast into it or arrive
+  // on its barriers
+  if constexpr (CL) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
@@ -1106,18 +1139,41 @@ int ozaki_slices_for(int dtype, int64_t k) {
 template <class T>
 static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& prm,
                            int grid, cudaStream_t st) {
-  // fp64: two passes, 8 digits; fp32: one pass, 3 digits of 8 bits
-  auto kern = std::is_same<T, double>::value ? gemm_ozaki_2p_kernel<double, 2, 8, false>
-                                             : gemm_ozaki_2p_kernel<float, 1, 3, true>;
-  static thread_local int configured_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured_dev != dev) {
-    LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)OZ2_SMEM), "smem attr (gemm_ozaki_2p_kernel)"));
-    configured_dev = dev;
+  // fp64: two passes, 8 digits; fp32: one pass, 3 digits of 8 bits.  fp64 with
+  // an even number of row blocks: clusters of two CTAs sharing the B stream
+  // (LAPIS_B200_OZAKI_CLUSTER=0 keeps single CTAs)
+  static const bool cl_on = [] {
+    const char* e = getenv("LAPIS_B200_OZAKI_CLUSTER");
+    return !(e && e[0] == '0');
+  }();
+  const bool cl = cl_on && std::is_same<T, double>::value && prm.num_m % 2 == 0 &&
+                  (prm.num_m / 2) * prm.num_n >= 1;
+  auto kern = std::is_same<T, double>::value
+                  ? (cl ? gemm_ozaki_2p_kernel<double, 2, 8, false, true>
+                        : gemm_ozaki_2p_kernel<double, 2, 8, false, false>)
+                  : gemm_ozaki_2p_kernel<float, 1, 3, true, false>;
+  LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OZ2_SMEM), "smem attr (gemm_ozaki_2p_kernel)"));
+  if (!cl) {
+    kern<<<grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, prm);
+    return check_launch("gemm_ozaki_2p_kernel");
   }
-  kern<<<grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, prm);
+  const int units = (prm.num_m / 2) * prm.num_n;
+  int g2 = std::min(units, grid / 2);
+  if (g2 < 1) g2 = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * g2), 1, 1);
+  cfg.blockDim = dim3(OZ_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = OZ2_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LB_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, ma, mb, prm), "launch (gemm_ozaki_2p_kernel, cluster)"));
   return check_launch("gemm_ozaki_2p_kernel");
 }
 
