@@ -453,11 +453,17 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
                      OzParams p) {
   static_assert((NPASS == 2 && SD == 8) || (NPASS == 1 && SD <= 4), "pass layout");
   constexpr int DA = SD < 4 ? SD : 4;   // diagonals of pass A
+  // stage layout: pass A holds 2 K blocks of SL A digit tiles + SL B digit
+  // tiles; one pass (SL = DA digits, 48 KB stages for fp32) fits NST = 4 stages
+  // in the space of the two-pass kernel's three 64 KB stages
+  constexpr int SL = NPASS == 1 ? DA : 4;
+  constexpr uint32_t STG = NPASS == 1 ? 4u * SL * OZ2_DIGIT : OZ2_STAGE;
+  constexpr int NST = NPASS == 1 ? (int)((OZ2_STAGES * OZ2_STAGE) / STG) : OZ2_STAGES;
   if (p.flag[0] || (p.sign_gate && p.flag[1])) return;  // uniform: a guarded fallback owns this call
   const uint32_t crank = CL ? cluster_ctarank() : 0u;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[OZ2_STAGES], empty[OZ2_STAGES], acc_full, acc_empty;
+  __shared__ uint64_t full[NST], empty[NST], acc_full, acc_empty;
   __shared__ uint32_t tmem_base_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.num_m * p.num_n;
@@ -479,7 +485,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tA);
     prefetch_tmap(&tB);
-    for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL ? 2 : 1); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL ? 2 : 1); }
     mbar_init(&acc_full, 1);
     mbar_init(&acc_empty, OZ_EPI_WARPS * 32);
     fence_barrier_init();
@@ -515,23 +521,24 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
         const int ma = mb * OZ_BM, nbn = nb * OZ2_BN;
         for (int j = 0; j < nk2; ++j) {            // pass A: K blocks 2j, 2j+1 (zero-filled past K)
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * OZ2_STAGE;
-          mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
+          uint8_t* sa = smem + stage * STG;
+          // boxes of DA digits (the 3-digit fp32 split loads no zero plane)
+          mbar_arrive_expect_tx(&full[stage], 2u * 2u * DA * OZ2_DIGIT);
           for (int h = 0; h < 2; ++h) {
-            tma_load_3d(sa + h * 8 * OZ2_DIGIT, &tA, (2 * j + h) * OZ2_BK, ma, 0, &full[stage]);
-            load_b(sa + h * 8 * OZ2_DIGIT + 4 * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
+            tma_load_3d(sa + h * 2 * SL * OZ2_DIGIT, &tA, (2 * j + h) * OZ2_BK, ma, 0, &full[stage]);
+            load_b(sa + (h * 2 + 1) * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
           }
-          if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         for (int kb = 0; kb < (NPASS == 2 ? nk : 0); ++kb) {   // pass B: one K block, all 8 digits
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * OZ2_STAGE;
+          uint8_t* sa = smem + stage * STG;
           mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
           tma_load_3d(sa, &tA, kb * OZ2_BK, ma, 0, &full[stage]);
           tma_load_3d(sa + 4 * OZ2_DIGIT, &tA, kb * OZ2_BK, ma, 4, &full[stage]);
           load_b(sa + 8 * OZ2_DIGIT, kb * OZ2_BK, nbn, 0, 0);
           load_b(sa + 12 * OZ2_DIGIT, kb * OZ2_BK, nbn, 4, 1);
-          if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -560,7 +567,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           mbar_wait(&full[stage], phase);
           if (p.prof) w_full += clock64() - t0;
           tc_fence_after();
-          const uint64_t desc0 = smem_desc_sw32(smem + stage * OZ2_STAGE);
+          const uint64_t desc0 = smem_desc_sw32(smem + stage * STG);
           if (elect_one()) {
             if (pass == 0) {
 #pragma unroll
@@ -570,8 +577,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
 #pragma unroll
                   for (int s = 0; s <= d; ++s)
                     tc_mma_i8(tmem_base + (uint32_t)(d * OZ2_BN),
-                              desc0 + (uint64_t)(((h * 8 + s) * OZ2_DIGIT) >> 4),
-                              desc0 + (uint64_t)(((h * 8 + 4 + d - s) * OZ2_DIGIT) >> 4),
+                              desc0 + (uint64_t)(((h * 2 * SL + s) * OZ2_DIGIT) >> 4),
+                              desc0 + (uint64_t)((((h * 2 + 1) * SL + d - s) * OZ2_DIGIT) >> 4),
                               !D8 ? idesc : (s == 0 ? (d == 0 ? idesc : idesc_su)
                                                     : (d - s == 0 ? idesc_us : idesc_uu)),
                               (j > 0 || h > 0 || s > 0) ? 1u : 0u);
@@ -589,7 +596,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
             else tc_commit(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) tc_commit(&acc_full);
         __syncwarp();
@@ -605,7 +612,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
     const int ew = warp - 2;                 // 0..7
     const int lg = warp & 3;                 // TMEM lane group this warp may access
     const int half = ew >> 2;                // columns [64*half, 64*half + 64)
-    double* wsm = reinterpret_cast<double*>(smem + OZ2_STAGES * OZ2_STAGE) + ew * 32 * 16;
+    double* wsm = reinterpret_cast<double*>(smem + OZ2_STAGES * OZ2_STAGE) + ew * 32 * 16;  // after the stages
     // this warp's partial in the CTA's slot: [chunk][j][lane], coalesced per j
     double* slot = p.split_ws + (int64_t)blockIdx.x * OZ2_SLOT + ew * (4 * 16 * 32) + lane;
     uint32_t acc_phase = 0;
@@ -1028,45 +1035,53 @@ ozaki_split_cols_f32(int64_t k, int64_t n, int64_t kp, int64_t np, const float* 
                      const int* __restrict__ gate = nullptr) {
   if (gate && *(volatile const int*)gate) return;
   __shared__ float tile[128][32];   // column c of row r at [r][c ^ (r / 4 % 32)]: conflict-free
+  __shared__ float sc1[32], sc2[32];  // per-column scale factors 2^e1, 2^e2
   const int64_t gxn = (np + 31) / 32, tiles = gxn * ((kp + 127) / 128);
-  const int64_t plane = np * kp;
+  const int64_t plane4 = np * kp / 4;   // digit plane stride in 32-bit words
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  const int ldb32 = (int)ldb;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int64_t by = t / gxn, bx = t % gxn;
     const int64_t k0 = by * 128, n0 = bx * 32;
+    const int krem = (int)min((int64_t)128, k - k0), nrem = (int)min((int64_t)32, n - n0);
     __syncthreads();
-#pragma unroll 8
-    for (int r = ty; r < 128; r += 8) {
-      const int64_t kk = k0 + r, nn = n0 + tx;
-      const float v = (kk < k && nn < n) ? B[kk * ldb + nn] : 0.0f;
-      tile[r][tx ^ ((r >> 2) & 31)] = isfinite(v) ? v : 0.0f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int cc = 4 * ty + c;
-      const int64_t nn = n0 + cc;
-      const int64_t kk = k0 + 4 * tx;
-      if (nn >= np || kk >= kp) continue;
+    if (ty == 0) {   // the column's exponent (from the maxima of ozaki_colmax_f32) and scales
       int e = 0;
-      if (nn < n) {
-        const double mx = __longlong_as_double((long long)colmax[nn]);
+      if (tx < nrem) {
+        const double mx = __longlong_as_double((long long)colmax[n0 + tx]);
         e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) + 1 : 0;
-        if (by == 0 && tx == 0) e_out[nn] = e;
+        if (by == 0) e_out[n0 + tx] = e;
       }
       const int sh_all = 7 + 8 * (S - 1) - e;
       const int e1 = min(max(sh_all, -126), 127), e2 = min(max(sh_all - e1, -126), 127);
-      const float p1 = pow2f(e1), p2 = pow2f(e2);
+      sc1[tx] = pow2f(e1);
+      sc2[tx] = pow2f(e2);
+    }
+    const float* __restrict__ tb = B + k0 * ldb + n0;   // 32-bit offsets inside the tile
+#pragma unroll 8
+    for (int r = ty; r < 128; r += 8) {
+      const float v = (r < krem && tx < nrem) ? tb[r * ldb32 + tx] : 0.0f;
+      tile[r][tx ^ ((r >> 2) & 31)] = isfinite(v) ? v : 0.0f;
+    }
+    __syncthreads();
+    const bool kin = k0 + 4 * tx < kp;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int cc = 4 * ty + c;
+      if (n0 + cc >= np || !kin) continue;
+      const float p1 = sc1[cc], p2 = sc2[cc];
+      const bool live = cc < nrem;
       int qi[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        qi[q] = (nn < n) ? __float2int_rd(tile[4 * tx + q][cc ^ tx] * p1 * p2) : 0;
+        qi[q] = live ? __float2int_rd(tile[4 * tx + q][cc ^ tx] * p1 * p2) : 0;
+      uint32_t* o = reinterpret_cast<uint32_t*>(out + (n0 + cc) * kp + k0) + tx;
       for (int s2 = 0; s2 < S; ++s2) {
         const int sh = 8 * (S - 1 - s2);
         uint32_t w = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) w |= (uint32_t)((qi[q] >> sh) & 0xff) << (8 * q);
-        *reinterpret_cast<uint32_t*>(out + s2 * plane + nn * kp + kk) = w;
+        o[s2 * plane4] = w;
       }
     }
   }
@@ -1146,12 +1161,12 @@ static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const O
     const char* e = getenv("LAPIS_B200_OZAKI_CLUSTER");
     return !(e && e[0] == '0');
   }();
-  const bool cl = cl_on && std::is_same<T, double>::value && prm.num_m % 2 == 0 &&
-                  (prm.num_m / 2) * prm.num_n >= 1;
+  const bool cl = cl_on && prm.num_m % 2 == 0 && (prm.num_m / 2) * prm.num_n >= 1;
   auto kern = std::is_same<T, double>::value
                   ? (cl ? gemm_ozaki_2p_kernel<double, 2, 8, false, true>
                         : gemm_ozaki_2p_kernel<double, 2, 8, false, false>)
-                  : gemm_ozaki_2p_kernel<float, 1, 3, true, false>;
+                  : (cl ? gemm_ozaki_2p_kernel<float, 1, 3, true, true>
+                        : gemm_ozaki_2p_kernel<float, 1, 3, true, false>);
   LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)OZ2_SMEM), "smem attr (gemm_ozaki_2p_kernel)"));
   if (!cl) {
@@ -1295,8 +1310,8 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
     rc = check_launch("ozaki split");
     CUtensorMap ma, mb;
     if (TWO_PASS) {
-      if (rc == LAPIS_B200_OK) rc = make_i8_map3(&ma, ad, mp, kp, S, OZ_BM, 4);
-      if (rc == LAPIS_B200_OK) rc = make_i8_map3(&mb, bd, np, kp, S, BN, 4);
+      if (rc == LAPIS_B200_OK) rc = make_i8_map3(&ma, ad, mp, kp, S, OZ_BM, S < 4 ? S : 4);
+      if (rc == LAPIS_B200_OK) rc = make_i8_map3(&mb, bd, np, kp, S, BN, S < 4 ? S : 4);
     } else {
       if (rc == LAPIS_B200_OK) rc = make_i8_map(&ma, ad, (int64_t)S * mp, kp, OZ_BM);
       if (rc == LAPIS_B200_OK) rc = make_i8_map(&mb, bd, (int64_t)S * np, kp, BN);
@@ -1404,7 +1419,7 @@ int gemm_ozaki(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, in
   // MMAs, while the per-diagonal kernel double-buffers its accumulators
   static const bool one_pass = [] {
     const char* e = getenv("LAPIS_B200_OZAKI_1P");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   if (one_pass && dtype == LAPIS_B200_F32 && S == 3)
     return gemm_ozaki_t<float, OZ2_BN, true>(batch, m, n, k, A, lda, B, ldb, C, ldc, sA, sB, sC, S, st,
