@@ -908,8 +908,11 @@ class DenseMatmul(Workload):
         names = {"tf32x3": "gemm_tf32x3_kernel (tcgen05 kind::tf32, 3xTF32)",
                  "dmma": "gemm_dmma_kernel (DMMA m8n8k4)",
                  "exact": "gemm_exact_kernel (reference order)",
-                 "ozaki": ("gemm_ozaki_2p_kernel (tcgen05 kind::i8, two-pass Ozaki, certified)"
+                 "ozaki": ("gemm_ozaki_2p_kernel (tcgen05 kind::i8, two-pass Ozaki, certified, "
+                           "2-CTA clusters with B multicast)"
                            if self.dt == torch.float64 and self.n * 9.0 * 2.0 ** -56 <= 0.75e-12
+                           else "gemm_ozaki_2p_kernel<float> (tcgen05 kind::i8, one-pass Ozaki, 3 digits, "
+                           "certified, sign-gated, 2-CTA clusters)" if self.dt == torch.float32
                            else "gemm_ozaki_kernel (tcgen05 kind::i8, Ozaki digits, certified)")}
         return f"gemm<{self.dtype}> mode={self.mode} -> {names[m]}"
 
