@@ -740,6 +740,51 @@ __device__ __forceinline__ void peel4(double r0, double r1, double r2, double r3
   }
 }
 
+// peel4 for S <= 8 without 64-bit integers: trunc(|r| 2^(7S)) is taken in
+// two exact fp64 steps, a = |r| 2^28 (digits 0-3 from trunc(a)) and
+// frac(a) 2^(7(S-4)) (digits 4..S-1), each converted to int32 — the same
+// digits as peel4
+__device__ __forceinline__ void peel4_fast(double r0, double r1, double r2, double r3, int S,
+                                           int8_t* __restrict__ out, int64_t plane) {
+  const double r[4] = {r0, r1, r2, r3};
+  const int sh_hi = S < 4 ? 7 * S : 28;
+  const double s_hi = __hiloint2double((sh_hi + 1023) << 20, 0);
+  const double s_lo = __hiloint2double((7 * (S > 4 ? S - 4 : 0) + 1023) << 20, 0);
+  uint32_t hi[4], lo[4];
+  uint32_t neg = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double a = fabs(r[c]) * s_hi;
+    const double t = trunc(a);
+    hi[c] = (uint32_t)__double2uint_rz(t);
+    lo[c] = (uint32_t)__double2uint_rz((a - t) * s_lo);
+    neg |= (r[c] < 0.0 ? 1u : 0u) << c;
+  }
+  uint32_t* o = reinterpret_cast<uint32_t*>(out);
+  const int64_t plane4 = plane >> 2;
+  const int nhi = S < 4 ? S : 4;
+  for (int s = 0; s < nhi; ++s) {
+    const int sh = 7 * (nhi - 1 - s);
+    uint32_t w = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t d = (hi[c] >> sh) & 127u;
+      w |= (uint32_t)(uint8_t)((neg >> c) & 1u ? (uint32_t)(-(int)d) : d) << (8 * c);
+    }
+    o[s * plane4] = w;
+  }
+  for (int s = 4; s < S; ++s) {
+    const int sh = 7 * (S - 1 - s);
+    uint32_t w = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t d = (lo[c] >> sh) & 127u;
+      w |= (uint32_t)(uint8_t)((neg >> c) & 1u ? (uint32_t)(-(int)d) : d) << (8 * c);
+    }
+    o[s * plane4] = w;
+  }
+}
+
 // 8-bit digits: the leading digit floor(128 r) is signed ([-128, 127]), the
 // remainder is in [0, 1) and every further digit floor(256 r) unsigned — the
 // two's-complement bytes of floor(r 2^(7 + 8(S-1))).
@@ -839,6 +884,7 @@ ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restri
         }
       }
       if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, orow + j, plane);
+      else if (S <= 8 && (plane & 3) == 0) peel4_fast(r[0], r[1], r[2], r[3], S, orow + j, plane);
       else peel4(r[0], r[1], r[2], r[3], S, orow + j, plane);
     }
   }
@@ -998,6 +1044,7 @@ ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restri
 #pragma unroll
     for (int q = 0; q < 4; ++q) r[q] = (nn < n) ? scale_down(tile[4 * tx + q][cc ^ tx], e) : 0.0;
     if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
+    else if (S <= 8 && (plane & 3) == 0) peel4_fast(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
     else peel4(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
   }
   }

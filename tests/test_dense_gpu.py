@@ -198,3 +198,43 @@ def test_reduce_rows_pipelined_bitexact(cuda_device, comb, dtype):
     src = (rng.integers(-5, 6, (300, 517)) if np.issubdtype(dtype, np.integer)
            else rng.uniform(0.5, 1.5, (300, 517))).astype(dtype)
     assert bits_equal(host(lb.reduce2d(cu(src), 1, comb)), O.reduce2d(src, 1, comb))
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 200, 300), (384, 130, 517), (1024, 512, 2048)])
+def test_auto_f32_sign_gate(cuda_device, m, n, k):
+    """AUTO f32: non-negative operands take the certified Ozaki path (even and
+    odd row-block counts: 2-CTA clusters or single CTAs), operands with a
+    negative entry the 3xTF32 path; both within the 1e-5 contract."""
+    rng = np.random.default_rng(m * 7 + k)
+    A = rng.uniform(0, 1, (m, k)).astype(np.float32)
+    B = rng.uniform(0, 1, (k, n)).astype(np.float32)
+    ok, msg = O.diff_outputs([host(lb.gemm(cu(A), cu(B)))], [O.matmul(A, B)], 1e-5)
+    assert ok, msg
+    A[m // 2, k // 3] = -0.25   # one negative entry trips the gate
+    ok, msg = O.diff_outputs([host(lb.gemm(cu(A), cu(B)))], [O.matmul(A, B)], 1e-5)
+    assert ok, msg
+    B2 = B.copy()
+    B2[k - 1, n - 1] = -1.0
+    ok, msg = O.diff_outputs([host(lb.gemm(cu(np.abs(A)), cu(B2)))], [O.matmul(np.abs(A), B2)], 1e-5)
+    assert ok, msg
+
+
+def test_auto_f32_non_finite_reference_order(cuda_device):
+    rng = np.random.default_rng(4)
+    A = rng.uniform(0, 1, (130, 96)).astype(np.float32)
+    B = rng.uniform(0, 1, (96, 70)).astype(np.float32)
+    A[7, 9] = np.inf
+    assert bits_equal(host(lb.gemm(cu(A), cu(B))), O.matmul(A, B))
+
+
+@pytest.mark.parametrize("dt,lo,tol", [(np.float32, 0.0, 1e-5), (np.float64, -1.0, 1e-12)])
+def test_auto_batched_ozaki(cuda_device, dt, lo, tol):
+    """batch_gemm in AUTO mode through the Ozaki paths (per-batch splits, the
+    cluster kernels on an even row-block count)."""
+    rng = np.random.default_rng(17)
+    A = rng.uniform(lo, 1, (3, 256, 192)).astype(dt)
+    B = rng.uniform(lo, 1, (3, 192, 160)).astype(dt)
+    got = host(lb.batch_gemm(cu(A), cu(B)))
+    for b in range(3):
+        ok, msg = O.diff_outputs([got[b]], [O.matmul(A[b], B[b])], tol)
+        assert ok, (b, msg)
