@@ -442,12 +442,15 @@ __device__ __forceinline__ void oz2_tile(int tile, int num_m, int num_n, int& mb
 // alone covers all 3 diagonals (6 products per K block) — the K blocks'
 // digit tiles are streamed once, against 1 + 2 + 3 re-streamed K passes in
 // the per-diagonal kernel.
-// CL: launched as clusters of two CTAs that take the two row blocks of one
-// column block at a time; each CTA loads its own A digit tiles and HALF of
-// the shared B digit tiles, multicast into both CTAs' shared memory (the B
-// operand stream from L2 halves); a stage is refilled once both CTAs' MMAs
-// released it (empty barriers count two commits, each multicast to the pair).
-template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false, bool CL = false>
+// CM x CN clusters: the cluster takes CM row blocks x CN column blocks at a
+// time; the CTAs of one row block share its A digit boxes and those of one
+// column block its B digit boxes — each such box is loaded by ONE CTA and
+// multicast into its sharers' shared memory (the operand stream from L2
+// shrinks by the sharing factor).  A stage is refilled once every CTA that
+// writes into it saw it released: each CTA's MMA commit is multicast to
+// itself, its row peer and its column peer, and the empty barriers count
+// 1 + (CN > 1) + (CM > 1) commits.
+template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false, int CM = 1, int CN = 1>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      OzParams p) {
@@ -460,7 +463,15 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   constexpr uint32_t STG = NPASS == 1 ? 4u * SL * OZ2_DIGIT : OZ2_STAGE;
   constexpr int NST = NPASS == 1 ? (int)((OZ2_STAGES * OZ2_STAGE) / STG) : OZ2_STAGES;
   if (p.flag[0] || (p.sign_gate && p.flag[1])) return;  // uniform: a guarded fallback owns this call
+  constexpr bool CL = CM * CN > 1;
+  static_assert((CM == 1 || CM == 2) && (CN == 1 || CN == 2), "cluster shape");
   const uint32_t crank = CL ? cluster_ctarank() : 0u;
+  const int cm = (int)crank % CM, cn = (int)crank / CM;         // rank = cn * CM + cm
+  // A boxes go to the CTAs of this row block (same cm), B boxes to those of
+  // this column block (same cn); commits to self, row peer and column peer
+  const uint16_t a_mask = (uint16_t)(CN == 2 ? ((1u << cm) | (1u << (CM + cm))) : (1u << crank));
+  const uint16_t b_mask = (uint16_t)(CM == 2 ? ((1u << (cn * CM)) | (1u << (cn * CM + 1))) : (1u << crank));
+  const uint16_t c_mask = (uint16_t)(a_mask | b_mask);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[NST], empty[NST], acc_full, acc_empty;
@@ -468,24 +479,24 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.num_m * p.num_n;
   const int nk = p.nk, nk2 = (p.nk + 1) / 2;
-  // work units: tiles, or (CL) pairs of row blocks sharing a column block
-  const int units = CL ? total / 2 : total;
-  const int ustart = CL ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int ustride = CL ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  // work units: CM x CN groups of tiles, one per cluster at a time
+  const int units = (p.num_m / CM) * (p.num_n / CN);
+  const int ustart = (int)blockIdx.x / (CM * CN);
+  const int ustride = (int)gridDim.x / (CM * CN);
   auto unit_tile = [&](int u, int& mb, int& nb) {
-    if (CL) {
-      int mbp;
-      oz2_tile(u, p.num_m / 2, p.num_n, mbp, nb);
-      mb = 2 * mbp + (int)crank;
-    } else {
-      oz2_tile(u, p.num_m, p.num_n, mb, nb);
-    }
+    int mg, ng;
+    oz2_tile(u, p.num_m / CM, p.num_n / CN, mg, ng);
+    mb = mg * CM + cm;
+    nb = ng * CN + cn;
   };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tA);
     prefetch_tmap(&tB);
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL ? 2 : 1); }
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + (CN > 1 ? 1 : 0) + (CM > 1 ? 1 : 0));
+    }
     mbar_init(&acc_full, 1);
     mbar_init(&acc_empty, OZ_EPI_WARPS * 32);
     fence_barrier_init();
@@ -506,11 +517,18 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
       // ------------------------------------------------------------ producer
       int stage = 0;
       uint32_t phase = 0;
-      // B box b of a stage: loaded here (plain), or (CL) by the CTA of rank
-      // b % 2 for both CTAs of the pair
+      // box b of a stage: shared boxes are loaded by the sharer whose index
+      // in the sharing pair equals b % 2, multicast to both
+      auto load_a = [&](void* dst, int kx, int ma, int dz, int b) {
+        if constexpr (CN == 2) {
+          if ((b & 1) == cn) tma_load_3d_mc(dst, &tA, kx, ma, dz, &full[stage], a_mask);
+        } else {
+          tma_load_3d(dst, &tA, kx, ma, dz, &full[stage]);
+        }
+      };
       auto load_b = [&](void* dst, int kx, int nbn, int dz, int b) {
-        if constexpr (CL) {
-          if ((b & 1) == (int)crank) tma_load_3d_mc(dst, &tB, kx, nbn, dz, &full[stage], (uint16_t)0x3);
+        if constexpr (CM == 2) {
+          if ((b & 1) == cm) tma_load_3d_mc(dst, &tB, kx, nbn, dz, &full[stage], b_mask);
         } else {
           tma_load_3d(dst, &tB, kx, nbn, dz, &full[stage]);
         }
@@ -525,7 +543,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           // boxes of DA digits (the 3-digit fp32 split loads no zero plane)
           mbar_arrive_expect_tx(&full[stage], 2u * 2u * DA * OZ2_DIGIT);
           for (int h = 0; h < 2; ++h) {
-            tma_load_3d(sa + h * 2 * SL * OZ2_DIGIT, &tA, (2 * j + h) * OZ2_BK, ma, 0, &full[stage]);
+            load_a(sa + h * 2 * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, ma, 0, h);
             load_b(sa + (h * 2 + 1) * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
           }
           if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -534,8 +552,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STG;
           mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
-          tma_load_3d(sa, &tA, kb * OZ2_BK, ma, 0, &full[stage]);
-          tma_load_3d(sa + 4 * OZ2_DIGIT, &tA, kb * OZ2_BK, ma, 4, &full[stage]);
+          load_a(sa, kb * OZ2_BK, ma, 0, 0);
+          load_a(sa + 4 * OZ2_DIGIT, kb * OZ2_BK, ma, 4, 1);
           load_b(sa + 8 * OZ2_DIGIT, kb * OZ2_BK, nbn, 0, 0);
           load_b(sa + 12 * OZ2_DIGIT, kb * OZ2_BK, nbn, 4, 1);
           if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -592,7 +610,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
                             desc0 + (uint64_t)(((8 + d - s) * OZ2_DIGIT) >> 4), idesc,
                             (j > 0 || s > 0) ? 1u : 0u);
             }
-            if constexpr (CL) tc_commit_mc(&empty[stage], (uint16_t)0x3);
+            if constexpr (CL) tc_commit_mc(&empty[stage], c_mask);
             else tc_commit(&empty[stage]);
           }
           __syncwarp();
@@ -1201,40 +1219,53 @@ int ozaki_slices_for(int dtype, int64_t k) {
 template <class T>
 static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& prm,
                            int grid, cudaStream_t st) {
-  // fp64: two passes, 8 digits; fp32: one pass, 3 digits of 8 bits.  fp64 with
-  // an even number of row blocks: clusters of two CTAs sharing the B stream
-  // (LAPIS_B200_OZAKI_CLUSTER=0 keeps single CTAs)
-  static const bool cl_on = [] {
+  // fp64: two passes, 8 digits; fp32: one pass, 3 digits of 8 bits.  Clusters
+  // share operand boxes: pairs along m by default; LAPIS_B200_OZAKI_CLUSTER =
+  // 0 (single CTAs) or 4 (2 x 2, A and B shared: only 34 of 37 clusters are
+  // co-resident, 4096^3 f64 1.99 vs 1.88 ms with pairs, f32 0.511 vs 0.508)
+  static const int cl_env = [] {
     const char* e = getenv("LAPIS_B200_OZAKI_CLUSTER");
-    return !(e && e[0] == '0');
+    return e ? atoi(e) : 2;
   }();
-  const bool cl = cl_on && prm.num_m % 2 == 0 && (prm.num_m / 2) * prm.num_n >= 1;
-  auto kern = std::is_same<T, double>::value
-                  ? (cl ? gemm_ozaki_2p_kernel<double, 2, 8, false, true>
-                        : gemm_ozaki_2p_kernel<double, 2, 8, false, false>)
-                  : (cl ? gemm_ozaki_2p_kernel<float, 1, 3, true, true>
-                        : gemm_ozaki_2p_kernel<float, 1, 3, true, false>);
+  int cmn = 1;
+  if (cl_env >= 4 && prm.num_m % 2 == 0 && prm.num_n % 2 == 0) cmn = 4;
+  else if (cl_env >= 2 && prm.num_m % 2 == 0) cmn = 2;
+  constexpr bool F64 = std::is_same<T, double>::value;
+  auto kern = cmn == 4 ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 2>
+                              : gemm_ozaki_2p_kernel<float, 1, 3, true, 2, 2>)
+            : cmn == 2 ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 1>
+                              : gemm_ozaki_2p_kernel<float, 1, 3, true, 2, 1>)
+                       : (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 1, 1>
+                              : gemm_ozaki_2p_kernel<float, 1, 3, true, 1, 1>);
   LB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)OZ2_SMEM), "smem attr (gemm_ozaki_2p_kernel)"));
-  if (!cl) {
+  if (cmn == 1) {
     kern<<<grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, prm);
     return check_launch("gemm_ozaki_2p_kernel");
   }
-  const int units = (prm.num_m / 2) * prm.num_n;
-  int g2 = std::min(units, grid / 2);
-  if (g2 < 1) g2 = 1;
+  const int units = (prm.num_m / (cmn == 4 ? 2 : 2)) * (prm.num_n / (cmn == 4 ? 2 : 1));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(2 * g2), 1, 1);
   cfg.blockDim = dim3(OZ_THREADS, 1, 1);
   cfg.dynamicSmemBytes = OZ2_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = (unsigned)cmn;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // one resident wave of clusters: clusters must fit inside a GPC, so fewer
+  // than #SMs / cmn may be co-resident
+  int max_clusters = grid / cmn;
+  cfg.gridDim = dim3((unsigned)(cmn * max_clusters), 1, 1);
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, (void*)kern, &cfg) == cudaSuccess && active > 0)
+    max_clusters = std::min(max_clusters, active);
+  cudaGetLastError();
+  int gc = std::min(units, max_clusters);
+  if (gc < 1) gc = 1;
+  cfg.gridDim = dim3((unsigned)(cmn * gc), 1, 1);
   LB_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, ma, mb, prm), "launch (gemm_ozaki_2p_kernel, cluster)"));
   return check_launch("gemm_ozaki_2p_kernel");
 }
