@@ -57,8 +57,11 @@ extern "C" {
 #define LAPIS_B200_MAX 3
 
 /* dense matmul precision modes (lapis_b200_gemm `mode`) */
-#define LAPIS_B200_GEMM_AUTO 0    /* f32 -> TF32X3, f64 -> OZAKI (DMMA beyond its k range),
-                                     ints -> EXACT */
+#define LAPIS_B200_GEMM_AUTO 0    /* f32 -> OZAKI when A and B hold no negative entry
+                                     (checked on the device; any negative entry, or a
+                                     failed certificate, recomputes with TF32X3) and k is in
+                                     its range, TF32X3 otherwise; f64 -> OZAKI (DMMA beyond
+                                     its k range); ints -> EXACT */
 #define LAPIS_B200_GEMM_TF32X3 1  /* f32: 3xTF32 split on tcgen05 (kind::tf32), TMEM accum */
 #define LAPIS_B200_GEMM_DMMA 2    /* f64: DMMA tensor cores */
 #define LAPIS_B200_GEMM_EXACT 3   /* reference order: sequential k, no FMA -> bit-exact */
