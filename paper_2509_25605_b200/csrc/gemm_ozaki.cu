@@ -803,6 +803,37 @@ __device__ __forceinline__ void peel4_fast(double r0, double r1, double r2, doub
   }
 }
 
+// S = 8 (the fp64 default), fully unrolled: per plane the four 7-bit
+// magnitudes are packed into one word with constant shifts, then negated as
+// bytes at once for the negative elements — -b (mod 256) = (0x80 - b) ^ 0x80
+// for 0 <= b <= 127, borrow-free across bytes — and selected by a byte mask
+__device__ __forceinline__ void peel4_s8(double r0, double r1, double r2, double r3,
+                                         int8_t* __restrict__ out, int64_t plane) {
+  const double r[4] = {r0, r1, r2, r3};
+  const double s28 = __hiloint2double((28 + 1023) << 20, 0);
+  uint32_t hi[4], lo[4];
+  uint32_t m = 0;   // 0xff in the bytes of negative elements
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double a = fabs(r[c]) * s28;
+    const double t = trunc(a);
+    hi[c] = __double2uint_rz(t);
+    lo[c] = __double2uint_rz((a - t) * s28);
+    m |= (r[c] < 0.0 ? 0xffu : 0u) << (8 * c);
+  }
+  uint32_t* o = reinterpret_cast<uint32_t*>(out);
+  const int64_t p4 = plane >> 2;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const uint32_t* q = s < 4 ? hi : lo;
+    const int sh = 7 * (3 - (s & 3));
+    const uint32_t w = ((q[0] >> sh) & 127u) | (((q[1] >> sh) & 127u) << 8) |
+                       (((q[2] >> sh) & 127u) << 16) | (((q[3] >> sh) & 127u) << 24);
+    const uint32_t wn = (0x80808080u - w) ^ 0x80808080u;
+    o[s * p4] = (w & ~m) | (wn & m);
+  }
+}
+
 // 8-bit digits: the leading digit floor(128 r) is signed ([-128, 127]), the
 // remainder is in [0, 1) and every further digit floor(256 r) unsigned — the
 // two's-complement bytes of floor(r 2^(7 + 8(S-1))).
@@ -902,6 +933,7 @@ ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restri
         }
       }
       if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, orow + j, plane);
+      else if (S == 8 && (plane & 3) == 0) peel4_s8(r[0], r[1], r[2], r[3], orow + j, plane);
       else if (S <= 8 && (plane & 3) == 0) peel4_fast(r[0], r[1], r[2], r[3], S, orow + j, plane);
       else peel4(r[0], r[1], r[2], r[3], S, orow + j, plane);
     }
@@ -1062,6 +1094,7 @@ ozaki_split_cols(int64_t k, int64_t n, int64_t kp, int64_t np, const T* __restri
 #pragma unroll
     for (int q = 0; q < 4; ++q) r[q] = (nn < n) ? scale_down(tile[4 * tx + q][cc ^ tx], e) : 0.0;
     if (digits8) peel4_u8(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
+    else if (S == 8 && (plane & 3) == 0) peel4_s8(r[0], r[1], r[2], r[3], out + nn * kp + kk, plane);
     else if (S <= 8 && (plane & 3) == 0) peel4_fast(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
     else peel4(r[0], r[1], r[2], r[3], S, out + nn * kp + kk, plane);
   }
