@@ -539,11 +539,17 @@ spmm_batch2_kernel(int64_t nrows, int64_t k, const RP* __restrict__ rowptr,
             for (int u = 0; u < U; ++u) {
               if (t0 + u < cnt) {
                 if constexpr (HOT) {
+                  // the column is warp-uniform (every lane loads its slice of
+                  // the same X row): branch on it rather than select a policy
                   const CI cu = cols[u];
-                  const char* xr = cu >= 0 ? xbase + (uint64_t)(uint32_t)(cu & ~SPMM_FAR_BIT) * ldxb
-                                           : hbase + (uint64_t)(uint32_t)(~cu) * ldhb;
-                  ldx_row_pol<T, CPL>(reinterpret_cast<const T*>(xr), xv[u],
-                                      cu < 0 ? pol_hot : ((cu & SPMM_FAR_BIT) ? pol_far : pol_near));
+                  if (cu < 0) {
+                    ldx_row<T, CPL>(reinterpret_cast<const T*>(hbase + (uint64_t)(uint32_t)(~cu) * ldhb), xv[u]);
+                  } else {
+                    const T* xr = reinterpret_cast<const T*>(
+                        xbase + (uint64_t)(uint32_t)(cu & ~SPMM_FAR_BIT) * ldxb);
+                    if (cu & SPMM_FAR_BIT) ldx_row_pol<T, CPL>(xr, xv[u], pol_far);
+                    else ldx_row<T, CPL>(xr, xv[u]);
+                  }
                 } else {
                   ldx_row<T, CPL>(reinterpret_cast<const T*>(xbase + (uint64_t)(uint32_t)cols[u] * ldxb),
                                   xv[u]);
