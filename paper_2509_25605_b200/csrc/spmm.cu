@@ -1509,10 +1509,12 @@ int spmm_plan_create(int64_t nrows, int64_t ncols, int64_t nnz, int64_t k, const
     return rc;
   }
   p->nhot = std::min<int64_t>((int64_t)nh, cap);
-  // reuse hints (LAPIS_B200_SPMM_HINT=0 disables): needs column ids < 2^30 and
-  // positions < 2^31
+  // reuse hints, opt-in (LAPIS_B200_SPMM_HINT=1): needs column ids < 2^30 and
+  // positions < 2^31.  Measured on config 3 with the 3-CTA HOT kernel: DRAM
+  // 48.4 -> 46.3 GB per launch but 7.70 -> 7.96 ms (the policy branch costs
+  // more than the traffic saves once the kernel runs at the copy rate)
   const char* he = getenv("LAPIS_B200_SPMM_HINT");
-  if (!(he && he[0] == '0') && nnz > 0 && nnz < 0x7fffffffLL && ncols < (1ll << 30)) {
+  if ((he && he[0] == '1') && nnz > 0 && nnz < 0x7fffffffLL && ncols < (1ll << 30)) {
     rc = spmm_reuse_hints(p, c32, c64, row_bytes, st);
     if (rc != LAPIS_B200_OK) {
       cudaFree(p->colind_hot);

@@ -86,7 +86,9 @@ def _():
     rp, ci = S.powerlaw_structure_host(S.PowerLawSpec(4000, mean=8.0, seed=3))
     v = rng.uniform(-1, 1, int(rp[-1]))
     X = rng.uniform(-1, 1, (4000, 64))
+    os.environ["LAPIS_B200_SPMM_HINT"] = "1"   # opt-in reuse hints
     plan = lb.SpmmPlan(cu(rp), cu(ci), 4000, 64, torch.float64, hot_bytes=64 << 10)
+    del os.environ["LAPIS_B200_SPMM_HINT"]
     assert plan.info()["far_reuse_entries"] >= 0
     Y = plan.spmm(cu(v), cu(X)).cpu().numpy()
     assert O.diff_outputs([Y], [O.spmm_csr(rp, ci, v, X)], 1e-12)[0]

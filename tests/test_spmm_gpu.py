@@ -98,8 +98,11 @@ def test_decreasing_rowptr(cuda_device, k, dtype):
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("hot_mb", [0, 1])
-def test_spmm_plan_hot_rows_bitexact(cuda_device, dtype, hot_mb):
-    """SpmmPlan (hot X rows pinned in L2, remapped colind) gives spmm_csr's bits."""
+@pytest.mark.parametrize("hints", ["0", "1"])
+def test_spmm_plan_hot_rows_bitexact(cuda_device, monkeypatch, dtype, hot_mb, hints):
+    """SpmmPlan (hot X rows pinned in L2, remapped colind; with and without the
+    opt-in reuse hints) gives spmm_csr's bits."""
+    monkeypatch.setenv("LAPIS_B200_SPMM_HINT", hints)
     import synth_inputs as S
     spec = S.PowerLawSpec(60_000, mean=10.0, seed=3)
     rowptr, colind = S.powerlaw_structure_host(spec)
@@ -110,6 +113,7 @@ def test_spmm_plan_hot_rows_bitexact(cuda_device, dtype, hot_mb):
                        hot_bytes=hot_mb << 20)
     info = plan.info()
     assert info["hot_rows"] > 0 and info["hot_entries"] > 0
+    assert (info["far_reuse_entries"] > 0) == (hints == "1"), info
     Xd = cu(X)
     got = plan.spmm(cu(values), Xd).cpu().numpy()
     want = lb.spmm_csr(cu(rowptr), cu(colind), cu(values), Xd).cpu().numpy()
