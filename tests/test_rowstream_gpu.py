@@ -92,3 +92,16 @@ def test_large_stencil_matches_oracle(cuda_device):
     assert plan.info()["rowstream"]
     y = host(plan.spmv(ci, v, cu(x)))
     assert bits_equal(y, O.spmv_csr(host(rp), host(ci), host(v), x))
+
+
+@pytest.mark.parametrize("rp_dt,ci_dt", [(np.int32, np.int32), (np.int32, np.int64), (np.int64, np.int64)])
+def test_index_widths(cuda_device, rp_dt, ci_dt):
+    # every rowptr / colind width the C ABI accepts goes through the kernel
+    rowptr, colind, values = stencil_csr(27, 17)
+    rowptr, colind = rowptr.astype(rp_dt), colind.astype(ci_dt)
+    x = np.random.default_rng(2).uniform(-1, 1, rowptr.size - 1)
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
+    assert plan.info()["rowstream"]
+    want = O.spmv_csr(rowptr, colind, values, x)
+    assert bits_equal(host(plan.spmv(cu(colind), cu(values), cu(x))), want)
+    assert bits_equal(host(lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x))), want)
