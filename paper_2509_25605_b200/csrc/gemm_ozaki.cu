@@ -477,7 +477,6 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   __shared__ uint64_t full[NST], empty[NST], acc_full, acc_empty;
   __shared__ uint32_t tmem_base_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = p.num_m * p.num_n;
   const int nk = p.nk, nk2 = (p.nk + 1) / 2;
   // work units: CM x CN groups of tiles, one per cluster at a time
   const int units = (p.num_m / CM) * (p.num_n / CN);
