@@ -423,6 +423,7 @@ template <> __device__ __forceinline__ int ld_pol<int>(const int* p, uint64_t po
 // warp load) is read L2::evict_first and the x gathers L2::evict_last, so x
 // (80 MB for config 3's 10M rows) stays in the 126 MB L2 instead of being
 // pushed out by the 1.2 GB entry stream.
+// (three CTAs per SM at U = 16 — 80 registers — measured 1.84 vs 1.09 ms)
 template <class T, class RP, class CI, int U, bool EXACT, bool POL = false>
 __global__ void __launch_bounds__(256)
 spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
