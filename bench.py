@@ -616,9 +616,31 @@ class StencilSpmv(Workload):
         torch.cuda.synchronize()
         t = max_over_ranks(a.elapsed_time(b) / 1e3 / steps, self.world)
         names = sorted({p.info()["kernel"] for p in ops[0][0].plans.values()})
-        return {"value": round(self.work_global() / t / 1e9, 3), "unit": "GB/s",
-                "frac": round(self.work_local() / t / 1e9 / peaks()["hbm_gbs"], 4),
-                "kernel": "; ".join(names), "note": "bit-identical to the reference"}
+        out = {"value": round(self.work_global() / t / 1e9, 3), "unit": "GB/s",
+               "frac": round(self.work_local() / t / 1e9 / peaks()["hbm_gbs"], 4),
+               "ms_per_step": round(t * 1e3, 4),
+               "kernel": "; ".join(names), "note": "bit-identical to the reference",
+               "path": "reference-order CsrPlan: also what the emitted C++ seam LAPIS::spmv_csr "
+                       "replays from its second call on (b200::CsrPlanCache, "
+                       "include/lapis_b200_runtime.hpp)"}
+        if self.world == 1:
+            # the no-plan call the emitted C++'s LAPIS::spmv_csr makes
+            # (lapis_b200_spmv_csr: structure pass + reference-order kernel)
+            rp, ci, v, x, y, _ = self.rot[0]
+            for _ in range(2):
+                self.lb.spmv_csr(rp, ci, v, x, y, stream=self.stream)
+            torch.cuda.synchronize()
+            a.record(self.stream)
+            for _ in range(steps):
+                self.lb.spmv_csr(rp, ci, v, x, y, stream=self.stream)
+            b.record(self.stream)
+            torch.cuda.synchronize()
+            t1 = a.elapsed_time(b) / 1e3 / steps
+            out["no_plan"] = {"value": round(self.work_global() / t1 / 1e9, 3), "unit": "GB/s",
+                              "ms_per_step": round(t1 * 1e3, 4),
+                              "path": "lapis_b200_spmv_csr without a plan: the seam's first "
+                                      "call, or a call after rowptr was modified; bit-identical"}
+        return out
 
     def e2e(self, steps, warmup):
         """DualView lazy sync of this rank's x slice (host-modified every step),

@@ -125,10 +125,13 @@ struct Record {
   bool device = false;
   std::atomic<long> count{1};
   std::string label;
+  std::uint64_t id = 0;  // unique per allocation, never reused (plan caches key on it)
 };
 
 inline Record* allocate(std::size_t bytes, bool device, const std::string& label) {
+  static std::atomic<std::uint64_t> next_id{1};
   auto* r = new Record();
+  r->id = next_id.fetch_add(1);
   r->device = device;
   r->label = label;
   if (bytes == 0) bytes = 1;
@@ -255,6 +258,8 @@ class View {
   KOKKOS_INLINE_FUNCTION value_type* data() const { return ptr_; }
   std::string label() const { return rec_ ? rec_->label : std::string(); }
   long use_count() const { return rec_ ? rec_->count.load() : 0; }
+  // identity of the allocation behind the view (0: unmanaged)
+  std::uint64_t alloc_id() const { return rec_ ? rec_->id : 0; }
   KOKKOS_INLINE_FUNCTION bool is_contiguous() const {
     int64_t s = 1;
     for (int r = static_cast<int>(rank) - 1; r >= 0; --r) {

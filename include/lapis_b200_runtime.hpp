@@ -19,7 +19,10 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "lapis_b200.h"
 #include "lapis_dualview_runtime.hpp"
@@ -43,6 +46,76 @@ inline std::int64_t pitch(const V& v) {
 template <class V>
 inline int index_bytes(const V&) {
   return static_cast<int>(sizeof(typename V::value_type));
+}
+
+// Structure plans of LAPIS::spmv_csr, keyed on the identity of rowptr's device
+// allocation (View::alloc_id: unique, never reused) and the shape.  A call
+// whose rowptr DualView carries a pending host or device modification drops
+// the entry and takes the no-plan call (one structure pass on the device);
+// the next unmodified call builds a reference-order (exact) plan — one
+// analysis read — and every later call replays it.  At most 16 entries, the
+// least recently used destroyed first.
+template <class V, class = void>
+struct HasAllocId : std::false_type {};
+template <class V>
+struct HasAllocId<V, decltype((void)std::declval<const V&>().alloc_id())> : std::true_type {};
+
+struct CsrPlanCache {
+  struct Entry {
+    std::uint64_t id;
+    const void* rowptr;
+    std::int64_t nrows, nnz;
+    int rp_bytes;
+    lapis_b200_csr_plan plan;
+    std::uint64_t used;
+  };
+  std::mutex mu;
+  std::vector<Entry> entries;
+  std::uint64_t tick = 0;
+
+  void drop(std::uint64_t id) {
+    for (std::size_t i = 0; i < entries.size(); ++i)
+      if (entries[i].id == id) {
+        lapis_b200_csr_plan_destroy(entries[i].plan);
+        entries.erase(entries.begin() + static_cast<std::ptrdiff_t>(i));
+        return;
+      }
+  }
+  // the plan for this structure, built on a miss; nullptr when creation fails
+  lapis_b200_csr_plan get(std::uint64_t id, const void* rowptr, std::int64_t nrows,
+                          std::int64_t nnz, int rp_bytes) {
+    for (auto& e : entries)
+      if (e.id == id && e.rowptr == rowptr && e.nrows == nrows && e.nnz == nnz &&
+          e.rp_bytes == rp_bytes) {
+        e.used = ++tick;
+        return e.plan;
+      }
+    drop(id);
+    lapis_b200_csr_plan p = nullptr;
+    if (lapis_b200_csr_plan_create(nrows, nnz, rowptr, rp_bytes, nullptr, &p) != LAPIS_B200_OK)
+      return nullptr;
+    if (lapis_b200_csr_plan_set_exact(p, 1) != LAPIS_B200_OK) {
+      lapis_b200_csr_plan_destroy(p);
+      return nullptr;
+    }
+    if (entries.size() >= 16) {
+      std::size_t lru = 0;
+      for (std::size_t i = 1; i < entries.size(); ++i)
+        if (entries[i].used < entries[lru].used) lru = i;
+      lapis_b200_csr_plan_destroy(entries[lru].plan);
+      entries.erase(entries.begin() + static_cast<std::ptrdiff_t>(lru));
+    }
+    entries.push_back(Entry{id, rowptr, nrows, nnz, rp_bytes, p, ++tick});
+    return p;
+  }
+};
+inline CsrPlanCache& csr_plan_cache() {
+  static CsrPlanCache* c = new CsrPlanCache();  // never destroyed: plans outlive static teardown
+  return *c;
+}
+inline std::size_t csr_plan_cache_size() {
+  std::lock_guard<std::mutex> g(csr_plan_cache().mu);
+  return csr_plan_cache().entries.size();
 }
 }  // namespace b200
 
@@ -91,6 +164,8 @@ inline void gemv(const DualView<std::int32_t**>& A, const DualView<std::int32_t*
 template <class RP, class CI, class T>
 inline void spmv_csr(DualView<RP*> rowptr, DualView<CI*> colind, DualView<T*> values,
                      DualView<T*> x, DualView<T*> y) {
+  // a structure modified since the last call invalidates its cached plan
+  const bool rp_modified = rowptr.hostModified() || rowptr.deviceModified();
   rowptr.syncDevice();
   colind.syncDevice();
   values.syncDevice();
@@ -101,10 +176,28 @@ inline void spmv_csr(DualView<RP*> rowptr, DualView<CI*> colind, DualView<T*> va
   const std::int64_t nnz = static_cast<std::int64_t>(colind.extent(0));
   auto rp = rowptr.device_view();
   auto ci = colind.device_view();
-  b200::check(lapis_b200_spmv_csr(n, x.extent(0), nnz, rp.data(), b200::index_bytes(rp), ci.data(),
-                                  b200::index_bytes(ci), values.device_view().data(),
-                                  x.device_view().data(), y.device_view().data(),
-                                  b200::Dtype<T>::value, 0, nullptr));
+  lapis_b200_csr_plan plan = nullptr;
+  if constexpr (b200::HasAllocId<decltype(rp)>::value) {
+    const std::uint64_t id = rp.alloc_id();
+    if (id != 0 && n > 0 && rp.stride(0) == 1) {
+      auto& cache = b200::csr_plan_cache();
+      std::lock_guard<std::mutex> g(cache.mu);
+      if (rp_modified)
+        cache.drop(id);
+      else
+        plan = cache.get(id, rp.data(), n, nnz, b200::index_bytes(rp));
+    }
+  }
+  if (plan)
+    b200::check(lapis_b200_spmv_csr_plan(plan, rp.data(), b200::index_bytes(rp), ci.data(),
+                                         b200::index_bytes(ci), values.device_view().data(),
+                                         x.device_view().data(), y.device_view().data(),
+                                         b200::Dtype<T>::value, nullptr));
+  else
+    b200::check(lapis_b200_spmv_csr(n, x.extent(0), nnz, rp.data(), b200::index_bytes(rp),
+                                    ci.data(), b200::index_bytes(ci), values.device_view().data(),
+                                    x.device_view().data(), y.device_view().data(),
+                                    b200::Dtype<T>::value, 0, nullptr));
   y.modifyDevice();
 }
 

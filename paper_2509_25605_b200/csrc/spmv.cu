@@ -36,6 +36,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <cstdio>
 
 namespace lapis_b200 {
 
@@ -538,12 +539,14 @@ spmv_warpblock_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
 // its tile's stream (a decreasing rowptr), clamped to range(begin,
 // max(begin, end)) (interp.py:808).  Shared-memory reads: lane i reads entry
 // b_i + u, b_i = i * len — conflict-free for odd row lengths (27-point).
-template <class T, class CI, int CAP, int ST>
+template <class T, class CI, class RP, int NT, int CAP, int ST>
 struct RowStreamSmem {
   static constexpr int CA = 16 / sizeof(CI), VA = 16 / sizeof(T);
+  static constexpr int RP_N = NT + 16 / (int)sizeof(RP);  // the tile's NT + 1 row offsets, 16-byte multiple
   static constexpr size_t CI_BYTES = ((CAP + CA) * sizeof(CI) + 127) / 128 * 128;
   static constexpr size_t V_BYTES = ((CAP + VA) * sizeof(T) + 127) / 128 * 128;
-  static constexpr size_t STAGE_BYTES = CI_BYTES + V_BYTES;
+  static constexpr size_t RP_BYTES = (RP_N * sizeof(RP) + 127) / 128 * 128;
+  static constexpr size_t STAGE_BYTES = CI_BYTES + V_BYTES + RP_BYTES;
   static constexpr size_t TOTAL = ST * STAGE_BYTES;
 };
 
@@ -567,69 +570,120 @@ __device__ __forceinline__ T row_fold(const CI* __restrict__ cp, const T* __rest
   return acc;
 }
 
+// per-CTA start / end timestamps and SM id (LAPIS_B200_RS_TIMES=<file>: a
+// tuning aid for the static tile split; off by default)
+__device__ int g_rs_dbg = 0;
+__device__ unsigned long long g_rs_times[3 * 4096];
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <class T, class RP, class CI, int NT, int CAP, int ST, int MC>
 __global__ void __launch_bounds__(NT)
 spmv_rowstream_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                       const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
-                      int tma_ok, RowGuard guard = RowGuard()) {
+                      int tma_ok, int64_t nstatic, unsigned long long* __restrict__ next_tile,
+                      RowGuard guard = RowGuard()) {
   if (row_guard_skip(guard)) return;
+  const bool dbg = g_rs_dbg && blockIdx.x < 4096;
+  unsigned long long t_start = dbg ? global_ns() : 0;
   constexpr int ROWS = NT;
-  using L = RowStreamSmem<T, CI, CAP, ST>;
+  using L = RowStreamSmem<T, CI, RP, NT, CAP, ST>;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full[ST];
-  __shared__ int64_t meta[ST][2];  // first staged entry of colind / values (aligned down); -1: direct
+  // per stage: first staged entry of colind / values (aligned down; -1:
+  // direct), the tile (-1: none left), its entry range, rowptr slice staged
+  __shared__ int64_t meta[ST][6];
   const int tid = threadIdx.x;
   const int gi = tid;
   const int64_t ntiles = (nrows + ROWS - 1) / ROWS;
+  const int64_t G = gridDim.x;
   auto sci = [&](int st) { return reinterpret_cast<CI*>(smem + st * L::STAGE_BYTES); };
   auto sv = [&](int st) { return reinterpret_cast<T*>(smem + st * L::STAGE_BYTES + L::CI_BYTES); };
+  auto srp = [&](int st) {
+    return reinterpret_cast<RP*>(smem + st * L::STAGE_BYTES + L::CI_BYTES + L::V_BYTES);
+  };
   const int64_t nnz_end = tid == 0 ? (int64_t)rowptr[nrows] : 0;
+  // tiles [0, nstatic): CTA b takes b, b + G, ... in order; tiles [nstatic,
+  // ntiles) are handed out by the atomic counter, so a CTA that fell behind
+  // (x gathers no longer hitting the L2 the other CTAs keep warm) takes fewer
+  // (thread 0 claims each counter tile one issue ahead of its use, so the
+  // atomic's round trip overlaps a tile's fold)
+  int64_t next_static = blockIdx.x;  // thread 0's next static tile
+  int64_t claimed = -1;              // thread 0's counter tile claimed ahead
+  auto claim = [&]() -> int64_t {
+    return next_tile ? nstatic + (int64_t)atomicAdd(next_tile, 1ull) : ntiles;
+  };
+  auto next_id = [&]() -> int64_t {
+    if (next_static < nstatic) {
+      const int64_t r = next_static;
+      next_static += G;
+      if (next_static >= nstatic) claimed = claim();
+      return r;
+    }
+    if (claimed < 0) claimed = claim();   // no static tiles for this CTA
+    const int64_t d = claimed;
+    if (d >= ntiles) return -1;
+    claimed = claim();
+    return d;
+  };
   auto issue = [&](int st, int64_t t) {
+    meta[st][2] = t;
+    if (t < 0) {
+      mbar_arrive(&full[st]);
+      return;
+    }
     const int64_t r0 = t * ROWS, r1 = min(nrows, r0 + ROWS);
     const int64_t s = (int64_t)rowptr[r0], e = (int64_t)rowptr[r1];
     const int64_t sc = s & ~(int64_t)(L::CA - 1), ec = (e + L::CA - 1) & ~(int64_t)(L::CA - 1);
     const int64_t sv0 = s & ~(int64_t)(L::VA - 1), ev = (e + L::VA - 1) & ~(int64_t)(L::VA - 1);
-    const bool direct = !tma_ok || e <= s || e - s > CAP || ec > nnz_end || ev > nnz_end;
+    const bool direct = !(tma_ok & 1) || e <= s || e - s > CAP || ec > nnz_end || ev > nnz_end;
+    const bool rp_staged = (tma_ok & 2) && r0 + L::RP_N <= nrows + 1;
     meta[st][0] = direct ? -1 : sc;
     meta[st][1] = sv0;
-    if (direct) {
+    meta[st][3] = s;
+    meta[st][4] = e;
+    meta[st][5] = rp_staged;
+    const uint32_t bc = direct ? 0 : (uint32_t)((ec - sc) * sizeof(CI));
+    const uint32_t bv = direct ? 0 : (uint32_t)((ev - sv0) * sizeof(T));
+    const uint32_t br = rp_staged ? (uint32_t)(L::RP_N * sizeof(RP)) : 0;
+    if (bc + bv + br == 0) {
       mbar_arrive(&full[st]);
     } else {
-      const uint32_t bc = (uint32_t)((ec - sc) * sizeof(CI)), bv = (uint32_t)((ev - sv0) * sizeof(T));
-      mbar_arrive_expect_tx(&full[st], bc + bv);
-      bulk_g2s(sci(st), colind + sc, bc, &full[st]);
-      bulk_g2s(sv(st), values + sv0, bv, &full[st]);
+      mbar_arrive_expect_tx(&full[st], bc + bv + br);
+      if (!direct) {
+        bulk_g2s(sci(st), colind + sc, bc, &full[st]);
+        bulk_g2s(sv(st), values + sv0, bv, &full[st]);
+      }
+      if (rp_staged) bulk_g2s(srp(st), rowptr + r0, br, &full[st]);
     }
   };
   if (tid == 0) {
     for (int st = 0; st < ST; ++st) mbar_init(&full[st], 1);
     fence_barrier_init();
-    for (int st = 0; st < ST; ++st) {
-      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
-      if (t < ntiles) issue(st, t);
-    }
+    for (int st = 0; st < ST; ++st) issue(st, next_id());
   }
   __syncthreads();
-  int64_t t = blockIdx.x;
-  int64_t b = 0, e = 0;
-  if (t < ntiles && t * ROWS + gi < nrows) {
-    b = (int64_t)rowptr[t * ROWS + gi];
-    e = (int64_t)rowptr[t * ROWS + gi + 1];
-  }
-  for (int64_t it = 0; t < ntiles; ++it, t += gridDim.x) {
+  for (int64_t it = 0;; ++it) {
     const int st = (int)(it % ST);
+    mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+    const int64_t t = meta[st][2];
+    if (t < 0) break;
     const int64_t row = t * ROWS + gi;
-    const int64_t tn = t + gridDim.x;
-    int64_t bn = 0, en = 0;
-    if (tn < ntiles && tn * ROWS + gi < nrows) {
-      bn = (int64_t)rowptr[tn * ROWS + gi];
-      en = (int64_t)rowptr[tn * ROWS + gi + 1];
+    // the row's range: from the staged rowptr slice (full tiles), else global
+    int64_t b = 0, e = 0;
+    if (meta[st][5]) {
+      b = (int64_t)srp(st)[gi];
+      e = (int64_t)srp(st)[gi + 1];
+    } else if (row < nrows) {
+      b = (int64_t)rowptr[row];
+      e = (int64_t)rowptr[row + 1];
     }
     if (e < b) e = b;
-    mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
     const int64_t sc = meta[st][0], sv0 = meta[st][1];
-    const int64_t tile_s = (int64_t)rowptr[t * ROWS];
-    const int64_t tile_e = (int64_t)rowptr[min(nrows, t * ROWS + ROWS)];
+    const int64_t tile_s = meta[st][3], tile_e = meta[st][4];
     const bool staged = sc >= 0 && b >= tile_s && e <= tile_e;
     T acc;
     if (__all_sync(0xffffffffu, staged || row >= nrows))
@@ -639,14 +693,16 @@ spmv_rowstream_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
     if (row < nrows) y[row] = acc;
     __syncthreads();
     if (tid == 0) {
-      const int64_t tr = t + (int64_t)ST * gridDim.x;
-      if (tr < ntiles) {
-        fence_proxy_async();
-        issue(st, tr);
-      }
+      fence_proxy_async();
+      issue(st, next_id());
     }
-    b = bn;
-    e = en;
+  }
+  if (dbg && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_rs_times[3 * blockIdx.x] = t_start;
+    g_rs_times[3 * blockIdx.x + 1] = global_ns();
+    g_rs_times[3 * blockIdx.x + 2] = smid;
   }
 }
 
@@ -761,7 +817,7 @@ static int launch_rowstream_cfg(int64_t nrows, const void* rowptr, const void* c
                                 const void* values, const void* x, void* y, cudaStream_t st,
                                 RowGuard guard) {
   constexpr int ROWS = NT, CAP = ROWS * PER;
-  using L = RowStreamSmem<T, CI, CAP, ST>;
+  using L = RowStreamSmem<T, CI, RP, NT, CAP, ST>;
   auto kern = spmv_rowstream_kernel<T, RP, CI, NT, CAP, ST, MC>;
   static int configured[64] = {0};
   static int ctas_per_sm[64] = {0};
@@ -777,15 +833,51 @@ static int launch_rowstream_cfg(int64_t nrows, const void* rowptr, const void* c
     ctas_per_sm[dev] = c < 1 ? 1 : c;
     configured[dev] = 1;
   }
-  const int tma_ok = ((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0);
+  // bit 0: entry arrays 16-byte aligned (bulk copies of colind / values);
+  // bit 1: rowptr too (bulk copies of each tile's row offsets)
+  const int tma_ok = (((uintptr_t)colind % 16 == 0) && ((uintptr_t)values % 16 == 0)) |
+                     (((uintptr_t)rowptr % 16 == 0) ? 2 : 0);
   const int64_t ntiles = (nrows + ROWS - 1) / ROWS;
   int64_t grid = (int64_t)num_sms() * ctas_per_sm[dev];
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  // static tile split: CTA b takes tiles b, b + G, ...  (a dynamic counter
-  // with a ring of prefetched tile ids measured slower: 5.11 vs 5.77 TB/s)
+  // tile split: the first (100 - LAPIS_B200_RS_DYN) % of the tiles static
+  // (CTA b takes b, b + G, ...), the rest from a counter (default 10 %, at
+  // least 16 tiles per CTA unless the variable is set).  C5 exact, per launch:
+  // all static 11.9-12.2 ms with straggler launches at 12.7-14.2 (a few CTAs
+  // end 1.2-2.4 ms after the rest); 10 % counter 12.3-12.6 ms, no stragglers;
+  // all counter 14.8 ms
+  const char* dyn_env = getenv("LAPIS_B200_RS_DYN");
+  const int dyn_pct = dyn_env ? std::max(0, std::min(100, atoi(dyn_env))) : 10;
+  int64_t nstatic = ntiles;
+  unsigned long long* next_tile = nullptr;
+  if (dyn_pct > 0 && (dyn_env != nullptr || ntiles >= 16 * grid)) {
+    nstatic = ntiles - ntiles * dyn_pct / 100;
+    LB_TRY(check_cuda(cudaMallocAsync((void**)&next_tile, sizeof(*next_tile), st),
+                      "alloc(row-stream counter)"));
+    LB_TRY(check_cuda(cudaMemsetAsync(next_tile, 0, sizeof(*next_tile), st), "memset(counter)"));
+  }
+  static const char* times_path = getenv("LAPIS_B200_RS_TIMES");
+  if (times_path) {
+    const int one = 1;
+    cudaMemcpyToSymbolAsync(g_rs_dbg, &one, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+  }
   kern<<<(unsigned)grid, NT, L::TOTAL, st>>>(nrows, (const RP*)rowptr, (const CI*)colind,
-                                             (const T*)values, (const T*)x, (T*)y, tma_ok, guard);
+                                             (const T*)values, (const T*)x, (T*)y, tma_ok, nstatic,
+                                             next_tile, guard);
+  if (next_tile) cudaFreeAsync(next_tile, st);
+  if (times_path) {
+    static unsigned long long h[3 * 4096];
+    const int n = (int)std::min<int64_t>(grid, 4096);
+    cudaMemcpyFromSymbolAsync(h, g_rs_times, sizeof(unsigned long long) * 3 * n, 0,
+                              cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE* f = fopen(times_path, "a")) {
+      fprintf(f, "launch %d %lld\n", n, (long long)ntiles);
+      for (int i = 0; i < n; ++i) fprintf(f, "%llu %llu %llu\n", h[3 * i], h[3 * i + 1], h[3 * i + 2]);
+      fclose(f);
+    }
+  }
   return check_launch("spmv_rowstream_kernel");
 }
 

@@ -78,6 +78,11 @@ def _():
     y = lb.CsrPlan(cu(rp), exact=True).spmv(cu(ci), cu(v), cu(x)).cpu().numpy()
     del os.environ["LAPIS_B200_SPMV_KERNEL"]
     assert np.array_equal(y, O.spmv_csr(rp, ci, v, x))
+    # counter tiles (half, then all of them)
+    for dyn in ("50", "100"):
+        os.environ["LAPIS_B200_RS_DYN"] = dyn
+        assert np.array_equal(plan.spmv(cu(cs.astype(np.int32)), cu(vs), cu(xs)).cpu().numpy(), want)
+    del os.environ["LAPIS_B200_RS_DYN"]
 
 
 @case("spmm_plan_hints")

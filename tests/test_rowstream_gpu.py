@@ -105,3 +105,40 @@ def test_index_widths(cuda_device, rp_dt, ci_dt):
     want = O.spmv_csr(rowptr, colind, values, x)
     assert bits_equal(host(plan.spmv(cu(colind), cu(values), cu(x))), want)
     assert bits_equal(host(lb.spmv_csr(cu(rowptr), cu(colind), cu(values), cu(x))), want)
+
+
+@pytest.mark.parametrize("dyn", ["0", "15", "60", "100"])
+def test_counter_tiles(cuda_device, monkeypatch, dyn):
+    # the tiles past the static share come from the atomic counter
+    # (LAPIS_B200_RS_DYN percent of them; large problems only): same bits
+    monkeypatch.setenv("LAPIS_B200_RS_DYN", dyn)
+    n = 100
+    rp, ci, v = lb.synth_stencil(27, n)
+    x = np.random.default_rng(int(dyn)).uniform(-1, 1, n ** 3)
+    plan = lb.CsrPlan(rp, exact=True)
+    y = host(plan.spmv(ci, v, cu(x)))
+    want = O.spmv_csr(host(rp), host(ci), host(v), x)
+    assert bits_equal(y, want)
+    assert bits_equal(host(lb.spmv_csr(rp, ci, v, cu(x))), want)
+
+
+@pytest.mark.parametrize("dyn", ["15", "100"])
+def test_counter_tiles_ragged(cuda_device, monkeypatch, dyn):
+    # forced on a ragged matrix large enough for the counter split: tiles
+    # staged, tiles past a stage (global loads) and empty rows interleave
+    monkeypatch.setenv("LAPIS_B200_SPMV_KERNEL", "rs")
+    monkeypatch.setenv("LAPIS_B200_RS_DYN", dyn)
+    rng = np.random.default_rng(77)
+    nrows, ncols = 800_000, 50_000   # 12500 tiles of 64 rows: past 16 per CTA
+    counts = rng.integers(0, 40, nrows)
+    counts[::5] = 0
+    counts[123], counts[nrows - 1] = 5000, 3000
+    rowptr = np.zeros(nrows + 1, dtype=np.int64)
+    rowptr[1:] = np.cumsum(counts)
+    colind = rng.integers(0, ncols, int(rowptr[-1])).astype(np.int32)
+    values = rng.uniform(-1, 1, int(rowptr[-1]))
+    x = rng.uniform(-1, 1, ncols)
+    plan = lb.CsrPlan(cu(rowptr), exact=True)
+    assert plan.info()["rowstream"], plan.info()
+    assert bits_equal(host(plan.spmv(cu(colind), cu(values), cu(x))),
+                      O.spmv_csr(rowptr, colind, values, x))
