@@ -123,8 +123,13 @@ int lapis_b200_spmv_csr_plan(lapis_b200_csr_plan plan, const void* rowptr, int r
                              const void* x, void* y, int dtype, void* stream);
 /* What the analysis chose: out[0] = longest row, out[1] = vector length of the
  * vector-lane kernel (0 = row-stream tile kernel), out[2] = number of tiles,
- * out[3] = flags: bit 0 exact mode, bit 1 warp-block kernel.  Regular
- * structures (longest row <= max(64, 8 x mean))
+ * out[3] = flags: bit 0 exact mode, bit 1 warp-block kernel, bit 2 the
+ * row-stream kernel (regular rows of 15-28 entries: each tile's row offsets,
+ * colind and values staged by TMA bulk copies, one row per thread, tiles
+ * handed out in runs of 5 by a device counter), bit 3 the row-stream kernel in
+ * every mode (its sequential row sums are the reference's bits; default for
+ * such structures, LAPIS_B200_RS_TREE=0 keeps the vector kernel in tree
+ * mode).  Other regular structures (longest row <= max(64, 8 x mean))
  * run the vector-lane kernel with VL = pow2floor(mean / 6) in [1, 8]: fp64 and
  * integer rows as the emitted TeamPolicy mapping (shuffle-tree reduce, the
  * Kokkos ThreadVectorRange semantics), fp32 rows — and every dtype once

@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(NT)
 spmv_rowstream_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                       const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
                       int tma_ok, int64_t nstatic, unsigned long long* __restrict__ next_tile,
-                      RowGuard guard = RowGuard()) {
+                      int chunk, RowGuard guard = RowGuard()) {
   if (row_guard_skip(guard)) return;
   const bool dbg = g_rs_dbg && blockIdx.x < 4096;
   unsigned long long t_start = dbg ? global_ns() : 0;
@@ -609,12 +609,13 @@ spmv_rowstream_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
   // tiles [0, nstatic): CTA b takes b, b + G, ... in order; tiles [nstatic,
   // ntiles) are handed out by the atomic counter, so a CTA that fell behind
   // (x gathers no longer hitting the L2 the other CTAs keep warm) takes fewer
-  // (thread 0 claims each counter tile one issue ahead of its use, so the
-  // atomic's round trip overlaps a tile's fold)
+  // (thread 0 claims runs of `chunk` consecutive counter tiles, each run one
+  // run ahead of its use, so the atomic's round trip overlaps the folds)
   int64_t next_static = blockIdx.x;  // thread 0's next static tile
-  int64_t claimed = -1;              // thread 0's counter tile claimed ahead
+  int64_t claimed = -1;              // thread 0's next run, claimed ahead
+  int64_t cur = 0, cur_end = 0;      // thread 0's current run
   auto claim = [&]() -> int64_t {
-    return next_tile ? nstatic + (int64_t)atomicAdd(next_tile, 1ull) : ntiles;
+    return next_tile ? nstatic + (int64_t)atomicAdd(next_tile, 1ull) * chunk : ntiles;
   };
   auto next_id = [&]() -> int64_t {
     if (next_static < nstatic) {
@@ -623,11 +624,13 @@ spmv_rowstream_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __
       if (next_static >= nstatic) claimed = claim();
       return r;
     }
+    if (cur < cur_end && cur < ntiles) return cur++;
     if (claimed < 0) claimed = claim();   // no static tiles for this CTA
-    const int64_t d = claimed;
-    if (d >= ntiles) return -1;
+    cur = claimed;
+    cur_end = claimed + chunk;
+    if (cur >= ntiles) return -1;
     claimed = claim();
-    return d;
+    return cur++;
   };
   auto issue = [&](int st, int64_t t) {
     meta[st][2] = t;
@@ -842,13 +845,19 @@ static int launch_rowstream_cfg(int64_t nrows, const void* rowptr, const void* c
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
   // tile split: the first (100 - LAPIS_B200_RS_DYN) % of the tiles static
-  // (CTA b takes b, b + G, ...), the rest from a counter (default 10 %, at
-  // least 16 tiles per CTA unless the variable is set).  C5 exact, per launch:
-  // all static 11.9-12.2 ms with straggler launches at 12.7-14.2 (a few CTAs
-  // end 1.2-2.4 ms after the rest); 10 % counter 12.3-12.6 ms, no stragglers;
-  // all counter 14.8 ms
+  // (CTA b takes b, b + G, ...), the rest from a counter in runs of
+  // LAPIS_B200_RS_CHUNK consecutive tiles per atomic (default: all tiles,
+  // runs of 5; problems of at least 16 tiles per CTA unless the variable is
+  // set).  C5, per launch (scripts/c5_dyn.sh, c5_chunk.sh): all static
+  // 11.9-12.2 ms with straggler launches at 12.7-14.2 (a few CTAs end 1.2-2.4
+  // ms after the rest); all counter, one tile per atomic 14.8 ms (the single
+  // counter's contention); runs of 2 / 3 / 4 / 5 / 6 / 7 / 10 / 12 / 16 tiles
+  // 12.3 / 12.54 / 12.05 / 11.80 / 11.87 / 11.96 / 11.87 / 12.18 / 12.47 ms,
+  // every CTA ending within 0.02 ms
   const char* dyn_env = getenv("LAPIS_B200_RS_DYN");
-  const int dyn_pct = dyn_env ? std::max(0, std::min(100, atoi(dyn_env))) : 10;
+  const int dyn_pct = dyn_env ? std::max(0, std::min(100, atoi(dyn_env))) : 100;
+  const char* chunk_env = getenv("LAPIS_B200_RS_CHUNK");
+  const int chunk = chunk_env ? std::max(1, atoi(chunk_env)) : 5;
   int64_t nstatic = ntiles;
   unsigned long long* next_tile = nullptr;
   if (dyn_pct > 0 && (dyn_env != nullptr || ntiles >= 16 * grid)) {
@@ -864,7 +873,7 @@ static int launch_rowstream_cfg(int64_t nrows, const void* rowptr, const void* c
   }
   kern<<<(unsigned)grid, NT, L::TOTAL, st>>>(nrows, (const RP*)rowptr, (const CI*)colind,
                                              (const T*)values, (const T*)x, (T*)y, tma_ok, nstatic,
-                                             next_tile, guard);
+                                             next_tile, chunk, guard);
   if (next_tile) cudaFreeAsync(next_tile, st);
   if (times_path) {
     static unsigned long long h[3 * 4096];
@@ -1188,7 +1197,12 @@ static int analyse_rows(CsrPlanImpl* p, const void* rowptr, int rp_bytes, cudaSt
   const bool vec_forced = kf && !strcmp(kf, "vec");
   p->rowstream = (monotone && regular && !wb && !vec_forced && !force) ? rowstream_per(mean) : 0;
   if (kf && !strcmp(kf, "rs") && monotone) p->rowstream = rowstream_per(mean) ? rowstream_per(mean) : 32;
-  p->rowstream_all = (kf && !strcmp(kf, "rs")) ? 1 : 0;
+  // ... in tree mode too: the sequential row sum is within the tree mode's
+  // tolerance and, with the counter-scheduled tiles, the faster kernel (C5
+  // 11.82 vs 12.13-12.16 ms back to back for the VL = 4 tree, which also
+  // runs into the power cap); LAPIS_B200_RS_TREE=0 keeps the vector kernel
+  const char* rt = getenv("LAPIS_B200_RS_TREE");
+  p->rowstream_all = ((kf && !strcmp(kf, "rs")) || (p->rowstream > 0 && !(rt && atoi(rt) == 0))) ? 1 : 0;
   return LAPIS_B200_OK;
 }
 
@@ -1224,7 +1238,7 @@ int csr_plan_info(void* plan, int64_t* out4) {
   out4[0] = p->max_len;
   out4[1] = p->exact_vl;
   out4[2] = p->ntiles;
-  out4[3] = p->exact | (p->warpblock << 1) | ((p->rowstream > 0) << 2);
+  out4[3] = p->exact | (p->warpblock << 1) | ((p->rowstream > 0) << 2) | (p->rowstream_all << 3);
   return LAPIS_B200_OK;
 }
 

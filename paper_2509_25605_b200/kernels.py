@@ -152,17 +152,20 @@ class CsrPlan:
         out = (C.c_int64 * 4)()
         check(_capi.lib().lapis_b200_csr_plan_info(self._handle, out), "csr_plan_info")
         vl, exact, wb, rs = int(out[1]), bool(out[3] & 1), bool(out[3] & 2), bool(out[3] & 4)
+        rs_all = bool(out[3] & 8)
         kind = "exact" if (exact or vl == 1) else "tree (exact for f32)"
         kernel = (f"spmv_vector_kernel<VL={vl}, {kind}>" if vl else "spmv_tile_kernel")
         if rs and (exact or vl == 1):
             kernel = "spmv_rowstream_kernel (exact)"
+        elif rs and rs_all:
+            kernel = "spmv_rowstream_kernel (reference order, every mode)"
         elif rs:
             kernel = f"spmv_vector_kernel<VL={vl}, tree>; exact / f32: spmv_rowstream_kernel"
         if wb:
             kernel = ("spmv_warpblock_kernel (exact)" if exact else
                       "spmv_warpblock_kernel (rows <= 512 in order, longer: warp tree; f32 exact)")
         return {"max_row_len": int(out[0]), "vector_length": vl, "exact": exact,
-                "warpblock": wb, "rowstream": rs, "ntiles": int(out[2]), "kernel": kernel}
+                "warpblock": wb, "rowstream": rs, "rowstream_all": rs_all, "ntiles": int(out[2]), "kernel": kernel}
 
     def spmv(self, colind, values, x, y=None, *, stream=None) -> torch.Tensor:
         colind, values, x, y = (_from_dlpack(t) for t in (colind, values, x, y))
