@@ -343,6 +343,12 @@ __global__ void __launch_bounds__(256)
 spmv_vector_kernel(int64_t nrows, const RP* __restrict__ rowptr, const CI* __restrict__ colind,
                    const T* __restrict__ values, const T* __restrict__ x, T* __restrict__ y,
                    RowGuard guard = RowGuard()) {
+  // launched with programmatic stream serialization (one-wave problems): wait
+  // for the previous grid's completion before any memory access, and let
+  // the next grid's CTAs launch as soon as this grid's have all started
+  // (no-ops for a plain launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (row_guard_skip(guard)) return;
   const int lane = threadIdx.x & (VL - 1);
   const unsigned gmask = (VL == 32) ? 0xffffffffu
@@ -949,6 +955,30 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  // one-wave problems (C1: ~15 us of kernel behind ~2 us of launch): launched
+  // with programmatic stream serialization, so the grid is set up while the
+  // previous one drains (LAPIS_B200_PDL=0: plain launch)
+  static const bool pdl = [] {
+    const char* e = getenv("LAPIS_B200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  if (pdl && per_sm_env == 0 && blocks <= wave) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LB_TRY(check_cuda(cudaLaunchKernelEx(&cfg, spmv_vector_kernel<T, RP, CI, VL, EXACT>, nrows,
+                                         (const RP*)rowptr, (const CI*)colind, (const T*)values,
+                                         (const T*)x, (T*)y, guard),
+                      "launch spmv_vector_kernel (PDL)"));
+    return check_launch("spmv_vector_kernel");
+  }
   spmv_vector_kernel<T, RP, CI, VL, EXACT><<<(unsigned)blocks, threads, 0, st>>>(
       nrows, (const RP*)rowptr, (const CI*)colind, (const T*)values, (const T*)x, (T*)y, guard);
   return check_launch("spmv_vector_kernel");
