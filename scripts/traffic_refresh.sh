@@ -13,7 +13,9 @@ d = {r[h.index('Metric Name')]: float(r[h.index('Metric Value')]) for r in rows}
 print(sys.argv[2], rows[0][h.index('Kernel Name')][:90], d)
 PY
 }
-run c2f32 gemm_ozaki_2p
-run c2f64 gemm_ozaki_2p
-run c3 spmm_batch2
-run c4 spmm_batch2
+[ -n "$ONLY_SPMV" ] || run c2f32 gemm_ozaki_2p
+[ -n "$ONLY_SPMV" ] || run c2f64 gemm_ozaki_2p
+[ -n "$ONLY_SPMV" ] || run c3 spmm_batch2
+[ -n "$ONLY_SPMV" ] || run c4 spmm_batch2
+run c1 spmv_vector
+run c5 spmv_rowstream
