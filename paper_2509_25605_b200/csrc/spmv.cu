@@ -951,7 +951,12 @@ static int launch_vector_t(int64_t nrows, const void* rowptr, const void* colind
     return (int64_t)(e ? atoi(e) : 0);
   }();
   const int64_t wave = (int64_t)num_sms() * 8;
-  const int64_t per_sm = per_sm_env > 0 ? per_sm_env : (blocks <= 8 * wave ? 8 : 1024);
+  // the no-plan call's guarded launch for decreasing rowptrs (rare; skipped
+  // otherwise) walks the rows from 64 CTAs per SM: a 1024-per-SM grid costs
+  // ~0.16 ms of CTA launches even when every CTA exits at the guard (C5)
+  const bool rare = guard.stats != nullptr && guard.want == 3;
+  const int64_t per_sm = per_sm_env > 0 ? per_sm_env
+                                        : (blocks <= 8 * wave ? 8 : (rare ? 64 : 1024));
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
