@@ -969,7 +969,7 @@ class DenseMatmul(Workload):
                  "dmma": "gemm_dmma_kernel (DMMA m8n8k4)",
                  "exact": "gemm_exact_kernel (reference order)",
                  "ozaki": ("gemm_ozaki_2p_kernel (tcgen05 kind::i8, two-pass Ozaki, certified, "
-                           "2-CTA clusters with B multicast)"
+                           "CTA pairs on cta_group::2 MMAs, M = 256)"
                            if self.dt == torch.float64 and self.n * 9.0 * 2.0 ** -56 <= 0.75e-12
                            else "gemm_ozaki_2p_kernel<float> (tcgen05 kind::i8, one-pass Ozaki, 3 digits, "
                            "certified, sign-gated, 2-CTA clusters)" if self.dt == torch.float32

@@ -111,6 +111,17 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t a_desc, uint
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
       :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// the same for a CTA pair (M = 256: rows 0-127 in the leader's TMEM, 128-255
+// in the peer's; B's N split 64 + 64 between their shared memories); issued
+// by the leader only
+__device__ __forceinline__ void tc_mma_i8_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 // instruction descriptor: D s32 (2), A/B 8-bit signed (1) or unsigned (0),
 // both K-major, N>>3, M>>4
 __host__ __device__ constexpr uint32_t i8_idesc(int M, int N, bool a_signed = true,
@@ -450,7 +461,14 @@ __device__ __forceinline__ void oz2_tile(int tile, int num_m, int num_n, int& mb
 // writes into it saw it released: each CTA's MMA commit is multicast to
 // itself, its row peer and its column peer, and the empty barriers count
 // 1 + (CN > 1) + (CM > 1) commits.
-template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false, int CM = 1, int CN = 1>
+// P2 (CM = 2, CN = 1): the pair runs cta_group::2 MMAs, M = 256 — each CTA
+// stages its own 128 A rows and 64 of the tile's 128 B rows (tB's box is 64
+// rows), both CTAs' boxes complete on the leader's full barrier, the leader
+// alone issues the MMAs and its commits release both CTAs' stages and
+// accumulators; each CTA drains its own TMEM half.  Per dispatch an SM reads
+// 4 KB of A + 2 KB of B from shared memory instead of 4 + 4 KB.
+template <class OUT, int NPASS = 2, int SD = 8, bool D8 = false, int CM = 1, int CN = 1,
+          bool P2 = false>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      OzParams p) {
@@ -472,6 +490,9 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   const uint16_t a_mask = (uint16_t)(CN == 2 ? ((1u << cm) | (1u << (CM + cm))) : (1u << crank));
   const uint16_t b_mask = (uint16_t)(CM == 2 ? ((1u << (cn * CM)) | (1u << (cn * CM + 1))) : (1u << crank));
   const uint16_t c_mask = (uint16_t)(a_mask | b_mask);
+  static_assert(!P2 || (CM == 2 && CN == 1), "CTA pairs along m");
+  const bool leader = !P2 || crank == 0;
+  constexpr uint32_t BD = P2 ? OZ2_DIGIT / 2 : OZ2_DIGIT;   // bytes per staged B digit plane
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[NST], empty[NST], acc_full, acc_empty;
@@ -494,22 +515,29 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
     prefetch_tmap(&tB);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + (CN > 1 ? 1 : 0) + (CM > 1 ? 1 : 0));
+      mbar_init(&empty[s], P2 ? 1 : 1 + (CN > 1 ? 1 : 0) + (CM > 1 ? 1 : 0));
     }
     mbar_init(&acc_full, 1);
-    mbar_init(&acc_empty, OZ_EPI_WARPS * 32);
+    mbar_init(&acc_empty, (P2 ? 2 : 1) * OZ_EPI_WARPS * 32);
     fence_barrier_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 :: "r"(smem_u32(&tmem_base_slot)), "r"(OZ_TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (P2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(smem_u32(&tmem_base_slot)), "r"(OZ_TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(smem_u32(&tmem_base_slot)), "r"(OZ_TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if constexpr (CL) cluster_sync_all();   // the peer's barriers exist before any multicast
   const uint32_t tmem_base = tmem_base_slot;
+  const uint32_t full_cl0 = P2 ? smem_map_rank(&full[0], 0) : 0u;   // the leader's full barriers
 
   if (warp == 0) {
     if (lane == 0) {
@@ -519,14 +547,18 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
       // box b of a stage: shared boxes are loaded by the sharer whose index
       // in the sharing pair equals b % 2, multicast to both
       auto load_a = [&](void* dst, int kx, int ma, int dz, int b) {
-        if constexpr (CN == 2) {
+        if constexpr (P2) {
+          tma_load_3d_2sm(dst, &tA, kx, ma, dz, full_cl0 + 8u * stage);
+        } else if constexpr (CN == 2) {
           if ((b & 1) == cn) tma_load_3d_mc(dst, &tA, kx, ma, dz, &full[stage], a_mask);
         } else {
           tma_load_3d(dst, &tA, kx, ma, dz, &full[stage]);
         }
       };
       auto load_b = [&](void* dst, int kx, int nbn, int dz, int b) {
-        if constexpr (CM == 2) {
+        if constexpr (P2) {
+          tma_load_3d_2sm(dst, &tB, kx, nbn + cm * 64, dz, full_cl0 + 8u * stage);
+        } else if constexpr (CM == 2) {
           if ((b & 1) == cm) tma_load_3d_mc(dst, &tB, kx, nbn, dz, &full[stage], b_mask);
         } else {
           tma_load_3d(dst, &tB, kx, nbn, dz, &full[stage]);
@@ -540,7 +572,11 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STG;
           // boxes of DA digits (the 3-digit fp32 split loads no zero plane)
-          mbar_arrive_expect_tx(&full[stage], 2u * 2u * DA * OZ2_DIGIT);
+          if constexpr (P2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2u * 2u * DA * (OZ2_DIGIT + BD));
+          } else {
+            mbar_arrive_expect_tx(&full[stage], 2u * 2u * DA * OZ2_DIGIT);
+          }
           for (int h = 0; h < 2; ++h) {
             load_a(sa + h * 2 * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, ma, 0, h);
             load_b(sa + (h * 2 + 1) * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
@@ -550,23 +586,32 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
         for (int kb = 0; kb < (NPASS == 2 ? nk : 0); ++kb) {   // pass B: one K block, all 8 digits
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STG;
-          mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
+          if constexpr (P2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2u * 8u * (OZ2_DIGIT + BD));
+          } else {
+            mbar_arrive_expect_tx(&full[stage], OZ2_STAGE);
+          }
           load_a(sa, kb * OZ2_BK, ma, 0, 0);
           load_a(sa + 4 * OZ2_DIGIT, kb * OZ2_BK, ma, 4, 1);
           load_b(sa + 8 * OZ2_DIGIT, kb * OZ2_BK, nbn, 0, 0);
-          load_b(sa + 12 * OZ2_DIGIT, kb * OZ2_BK, nbn, 4, 1);
+          load_b(sa + 8 * OZ2_DIGIT + 4 * BD, kb * OZ2_BK, nbn, 4, 1);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // ------------------------------------------------------------ MMA issuer
-    // (the whole warp runs the loop, one elected lane issues)
-    constexpr uint32_t idesc = i8_idesc(OZ_BM, OZ2_BN, true, true);
+    // (the whole warp runs the loop, one elected lane issues; P2: the leader's)
+    constexpr int MM = P2 ? 2 * OZ_BM : OZ_BM;
+    constexpr uint32_t idesc = i8_idesc(MM, OZ2_BN, true, true);
     // 8-bit digits: digit 0 signed, the others unsigned
-    constexpr uint32_t idesc_su = i8_idesc(OZ_BM, OZ2_BN, true, false);
-    constexpr uint32_t idesc_us = i8_idesc(OZ_BM, OZ2_BN, false, true);
-    constexpr uint32_t idesc_uu = i8_idesc(OZ_BM, OZ2_BN, false, false);
+    constexpr uint32_t idesc_su = i8_idesc(MM, OZ2_BN, true, false);
+    constexpr uint32_t idesc_us = i8_idesc(MM, OZ2_BN, false, true);
+    constexpr uint32_t idesc_uu = i8_idesc(MM, OZ2_BN, false, false);
+    auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+      if constexpr (P2) tc_mma_i8_2sm(d, a, b, id, acc);
+      else tc_mma_i8(d, a, b, id, acc);
+    };
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
     long long w_tmem = 0, w_full = 0;
@@ -593,9 +638,9 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
                 for (int d = 0; d < DA; ++d)
 #pragma unroll
                   for (int s = 0; s <= d; ++s)
-                    tc_mma_i8(tmem_base + (uint32_t)(d * OZ2_BN),
+                    mma(tmem_base + (uint32_t)(d * OZ2_BN),
                               desc0 + (uint64_t)(((h * 2 * SL + s) * OZ2_DIGIT) >> 4),
-                              desc0 + (uint64_t)((((h * 2 + 1) * SL + d - s) * OZ2_DIGIT) >> 4),
+                              desc0 + (uint64_t)(((h * 2 + 1) * SL * OZ2_DIGIT + (d - s) * BD) >> 4),
                               !D8 ? idesc : (s == 0 ? (d == 0 ? idesc : idesc_su)
                                                     : (d - s == 0 ? idesc_us : idesc_uu)),
                               (j > 0 || h > 0 || s > 0) ? 1u : 0u);
@@ -604,18 +649,22 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
               for (int d = 4; d < 8; ++d)
 #pragma unroll
                 for (int s = 0; s <= d; ++s)
-                  tc_mma_i8(tmem_base + (uint32_t)((d - 4) * OZ2_BN),
+                  mma(tmem_base + (uint32_t)((d - 4) * OZ2_BN),
                             desc0 + (uint64_t)((s * OZ2_DIGIT) >> 4),
-                            desc0 + (uint64_t)(((8 + d - s) * OZ2_DIGIT) >> 4), idesc,
+                            desc0 + (uint64_t)((8 * OZ2_DIGIT + (d - s) * BD) >> 4), idesc,
                             (j > 0 || s > 0) ? 1u : 0u);
             }
-            if constexpr (CL) tc_commit_mc(&empty[stage], c_mask);
+            if constexpr (P2) tc_commit_2sm_mc(&empty[stage], (uint16_t)3);
+            else if constexpr (CL) tc_commit_mc(&empty[stage], c_mask);
             else tc_commit(&empty[stage]);
           }
           __syncwarp();
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
-        if (elect_one()) tc_commit(&acc_full);
+        if (elect_one()) {
+          if constexpr (P2) tc_commit_2sm_mc(&acc_full, (uint16_t)3);
+          else tc_commit(&acc_full);
+        }
         __syncwarp();
       }
     }
@@ -624,7 +673,7 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
       atomicAdd(p.prof + 2, (unsigned long long)w_full);
       atomicAdd(p.prof + 3, (unsigned long long)(clock64() - t_start));
     }
-  } else {
+  } else if (warp >= 2) {
     // ------------------------------------------------------------- epilogue
     const int ew = warp - 2;                 // 0..7
     const int lg = warp & 3;                 // TMEM lane group this warp may access
@@ -672,7 +721,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
         }
         // every accumulator read: the next pass's MMAs may start
         tc_fence_before();
-        mbar_arrive(&acc_empty);
+        if constexpr (P2) mbar_arrive_cl(smem_map_rank(&acc_empty, 0));
+        else mbar_arrive(&acc_empty);
       }
       // final: certify and write C through the shared transpose (4 rows x 16
       // columns per store instruction)
@@ -723,8 +773,12 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   if constexpr (CL) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
-                 :: "r"(tmem_base), "r"(OZ_TMEM_COLS));
+    if constexpr (P2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;"
+                   :: "r"(tmem_base), "r"(OZ_TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                   :: "r"(tmem_base), "r"(OZ_TMEM_COLS));
   }
 }
 
@@ -1249,8 +1303,8 @@ int ozaki_slices_for(int dtype, int64_t k) {
 }
 
 template <class T>
-static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& prm,
-                           int grid, cudaStream_t st) {
+static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mb64,
+                           const OzParams& prm, int grid, cudaStream_t st) {
   // fp64: two passes, 8 digits; fp32: one pass, 3 digits of 8 bits.  Clusters
   // share operand boxes: pairs along m by default; LAPIS_B200_OZAKI_CLUSTER =
   // 0 (single CTAs) or 4 (2 x 2, A and B shared: only 34 of 37 clusters are
@@ -1263,7 +1317,17 @@ static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const O
   if (cl_env >= 4 && prm.num_m % 2 == 0 && prm.num_n % 2 == 0) cmn = 4;
   else if (cl_env >= 2 && prm.num_m % 2 == 0) cmn = 2;
   constexpr bool F64 = std::is_same<T, double>::value;
-  auto kern = cmn == 4 ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 2>
+  // the m-pairs run cta_group::2 MMAs (M = 256) for fp64: 4096^3 1.89 ->
+  // 1.79 ms (fp32: 0.706 vs 0.709, unchanged — not smem-bound at 6 products
+  // per stage); LAPIS_B200_OZAKI_PAIR = 0 / 1 forces it off / on for both
+  static const int pair_env = [] {
+    const char* e = getenv("LAPIS_B200_OZAKI_PAIR");
+    return e ? atoi(e) : -1;
+  }();
+  const bool pair = cmn == 2 && (pair_env < 0 ? F64 : pair_env == 1);
+  auto kern = pair ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 1, true>
+                          : gemm_ozaki_2p_kernel<float, 1, 3, true, 2, 1, true>)
+            : cmn == 4 ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 2>
                               : gemm_ozaki_2p_kernel<float, 1, 3, true, 2, 2>)
             : cmn == 2 ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 1>
                               : gemm_ozaki_2p_kernel<float, 1, 3, true, 2, 1>)
@@ -1298,7 +1362,8 @@ static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const O
   int gc = std::min(units, max_clusters);
   if (gc < 1) gc = 1;
   cfg.gridDim = dim3((unsigned)(cmn * gc), 1, 1);
-  LB_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, ma, mb, prm), "launch (gemm_ozaki_2p_kernel, cluster)"));
+  LB_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, ma, pair ? mb64 : mb, prm),
+                    "launch (gemm_ozaki_2p_kernel, cluster)"));
   return check_launch("gemm_ozaki_2p_kernel");
 }
 
@@ -1475,7 +1540,9 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
     if constexpr (TWO_PASS) {
       prm.nk = (int)((kp + OZ2_BK - 1) / OZ2_BK);
       prm.vec2 = ((uintptr_t)Cb % (2 * sizeof(T)) == 0) && (ldc % 2 == 0);
-      rc = launch_ozaki_2p<T>(ma, mb, prm, std::min(tiles, sms), st);
+      CUtensorMap mb64;   // B boxes of 64 rows: each CTA of a cta_group::2 pair stages half the tile
+      rc = make_i8_map3(&mb64, bd, np, kp, S, 64, S < 4 ? S : 4);
+      if (rc == LAPIS_B200_OK) rc = launch_ozaki_2p<T>(ma, mb, mb64, prm, std::min(tiles, sms), st);
     } else {
       gemm_ozaki_kernel<T, BN><<<grid, OZ_THREADS, OzTile<BN>::SMEM, st>>>(ma, mb, prm);
       rc = check_launch("gemm_ozaki_kernel");

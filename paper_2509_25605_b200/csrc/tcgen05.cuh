@@ -38,6 +38,33 @@ __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map
          "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t smem_map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// CTA-pair TMA: the box lands in this CTA's shared memory, its bytes complete
+// on the mbarrier at cluster address `bar_cl` (the pair leader's)
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, int x, int y,
+                                                int z, uint32_t bar_cl) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z),
+         "r"(bar_cl)
+      : "memory");
+}
+// arrive (release, cluster scope) on an mbarrier given by its cluster address
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(bar_cl) : "memory");
+}
+// CTA-pair MMA commit: the arrive lands on the mbarrier at this offset in
+// every CTA of `mask`
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               :: "r"(smem_u32(bar)), "h"(mask) : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
