@@ -478,8 +478,12 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   // tiles; one pass (SL = DA digits, 48 KB stages for fp32) fits NST = 4 stages
   // in the space of the two-pass kernel's three 64 KB stages
   constexpr int SL = NPASS == 1 ? DA : 4;
-  constexpr uint32_t STG = NPASS == 1 ? 4u * SL * OZ2_DIGIT : OZ2_STAGE;
-  constexpr int NST = NPASS == 1 ? (int)((OZ2_STAGES * OZ2_STAGE) / STG) : OZ2_STAGES;
+  // (P2: a CTA stages half of each B digit plane, so its stages are 3/4 the
+  // size and one more fits — the pair's MMAs outrun three stages of TMA)
+  constexpr uint32_t BD = P2 ? OZ2_DIGIT / 2 : OZ2_DIGIT;   // bytes per staged B digit plane
+  constexpr uint32_t HB = SL * (OZ2_DIGIT + BD);             // pass-A half stage: SL A + SL B planes
+  constexpr uint32_t STG = NPASS == 1 ? 2u * HB : 8u * (OZ2_DIGIT + BD);
+  constexpr int NST = (int)((OZ2_STAGES * OZ2_STAGE) / STG);
   if (p.flag[0] || (p.sign_gate && p.flag[1])) return;  // uniform: a guarded fallback owns this call
   constexpr bool CL = CM * CN > 1;
   static_assert((CM == 1 || CM == 2) && (CN == 1 || CN == 2), "cluster shape");
@@ -492,7 +496,6 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
   const uint16_t c_mask = (uint16_t)(a_mask | b_mask);
   static_assert(!P2 || (CM == 2 && CN == 1), "CTA pairs along m");
   const bool leader = !P2 || crank == 0;
-  constexpr uint32_t BD = P2 ? OZ2_DIGIT / 2 : OZ2_DIGIT;   // bytes per staged B digit plane
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[NST], empty[NST], acc_full, acc_empty;
@@ -578,8 +581,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
             mbar_arrive_expect_tx(&full[stage], 2u * 2u * DA * OZ2_DIGIT);
           }
           for (int h = 0; h < 2; ++h) {
-            load_a(sa + h * 2 * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, ma, 0, h);
-            load_b(sa + (h * 2 + 1) * SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
+            load_a(sa + h * HB, (2 * j + h) * OZ2_BK, ma, 0, h);
+            load_b(sa + h * HB + SL * OZ2_DIGIT, (2 * j + h) * OZ2_BK, nbn, 0, h);
           }
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
@@ -639,8 +642,8 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
 #pragma unroll
                   for (int s = 0; s <= d; ++s)
                     mma(tmem_base + (uint32_t)(d * OZ2_BN),
-                              desc0 + (uint64_t)(((h * 2 * SL + s) * OZ2_DIGIT) >> 4),
-                              desc0 + (uint64_t)(((h * 2 + 1) * SL * OZ2_DIGIT + (d - s) * BD) >> 4),
+                              desc0 + (uint64_t)((h * HB + s * OZ2_DIGIT) >> 4),
+                              desc0 + (uint64_t)((h * HB + SL * OZ2_DIGIT + (d - s) * BD) >> 4),
                               !D8 ? idesc : (s == 0 ? (d == 0 ? idesc : idesc_su)
                                                     : (d - s == 0 ? idesc_us : idesc_uu)),
                               (j > 0 || h > 0 || s > 0) ? 1u : 0u);
