@@ -1094,8 +1094,10 @@ __global__ void ozaki_colmax(int64_t k, int64_t n, const T* __restrict__ B, int6
   const int64_t k0 = (int64_t)blockIdx.y * 64, k1 = k0 + 64 < k ? k0 + 64 : k;
   double mx = 0.0;
   bool bad = false, neg = false;
-#pragma unroll 8
-  for (int64_t r = k0; r < k1; ++r) {   // 8 rows in flight per thread
+  // 16 rows in flight per thread (8: 36.9 us for 4096^2 fp64, 87 % of the
+  // warps' time on the load scoreboard; 16: 25.4 us)
+#pragma unroll 16
+  for (int64_t r = k0; r < k1; ++r) {
     const double v = (double)B[r * ldb + j];
     bad |= !isfinite(v);
     neg |= v < 0.0;
