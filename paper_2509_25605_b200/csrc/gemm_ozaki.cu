@@ -935,7 +935,7 @@ __device__ __forceinline__ double scale_down(double v, int e) {
 // columns [k, kp) are zeros; non-finite values raise the flag (they are
 // split as zeros; the guarded fallback recomputes C).
 template <class T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 ozaki_split_rows(int64_t m, int64_t k, int64_t kp, int64_t mp, const T* __restrict__ A,
                  int64_t lda, int S, int8_t* __restrict__ out, int* __restrict__ e_out,
                  int* __restrict__ flag, int digits8, int sign_gate) {
