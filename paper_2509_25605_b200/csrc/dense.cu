@@ -427,7 +427,9 @@ static int launch_gemm_exact(int64_t batch, int64_t m, int64_t n, int64_t k, con
     }
   }
   const int64_t tiles = ((n + EG_TILE - 1) / EG_TILE) * ((m + EG_TILE - 1) / EG_TILE) * batch;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * 8));
+  // a guarded fallback (skipped unless its flag is raised) launches one wave
+  const int64_t per_sm = guard.mode != 0 ? 1 : 8;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * per_sm));
   gemm_exact_kernel<T, RELU><<<(unsigned)grid, 256, 0, st>>>(m, n, k, (const T*)A, lda, (const T*)B,
                                                              ldb, (T*)C, ldc, sA, sB, sC, batch, guard);
   return check_launch("gemm_exact_kernel");

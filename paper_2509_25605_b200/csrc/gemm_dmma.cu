@@ -46,8 +46,13 @@ gemm_dmma_kernel(int64_t m, int64_t n, int64_t k, const double* __restrict__ A, 
   double* sB = dsm + DM_STAGES * DM_A_ELEMS;         // [STAGES][BK][BS]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 2, wn = warp & 3;           // 2 x 4 warp grid
-  const int64_t m0 = (int64_t)blockIdx.y * DM_BM, n0 = (int64_t)blockIdx.x * DM_BN;
   const int nkb = (int)((k + DM_BK - 1) / DM_BK);
+  // tiles walked grid-stride (a guarded fallback launches one wave: when
+  // the guard skips, its cost is one wave of CTA launches, not every tile's)
+  const int64_t tn = (n + DM_BN - 1) / DM_BN, tiles = tn * ((m + DM_BM - 1) / DM_BM);
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  const int64_t m0 = (tile / tn) * DM_BM, n0 = (tile % tn) * DM_BN;
+  __syncthreads();   // the previous tile's shared-memory reads are done
 
   auto load_stage = [&](int st, int kb) {
     const int64_t k0 = (int64_t)kb * DM_BK;
@@ -121,6 +126,7 @@ gemm_dmma_kernel(int64_t m, int64_t n, int64_t k, const double* __restrict__ A, 
       }
     }
   }
+  }
 }
 
 int gemm_exact(int64_t, int64_t, int64_t, int64_t, const void*, int64_t, const void*, int64_t,
@@ -151,8 +157,12 @@ int gemm_dmma(int64_t batch, int64_t m, int64_t n, int64_t k, const void* A, int
                       "smem attr (gemm_dmma_kernel)"));
     configured_dev = dev;
   }
-  dim3 grid((unsigned)((n + DM_BN - 1) / DM_BN), (unsigned)((m + DM_BM - 1) / DM_BM));
-  if (grid.y > 65535) return fail(LAPIS_B200_ERR_ARG, "gemm dmma: too many row tiles");
+  const int64_t tiles = ((n + DM_BN - 1) / DM_BN) * ((m + DM_BM - 1) / DM_BM);
+  // one CTA per tile when DMMA is the chosen path; one wave when guarded
+  int64_t g = tiles;
+  if (guard.mode != 0 && g > (int64_t)num_sms()) g = num_sms();
+  if (g > 0x7fffffffLL) g = 0x7fffffffLL;
+  const dim3 grid((unsigned)(g < 1 ? 1 : g));
   for (int64_t b = 0; b < batch; ++b) {
     gemm_dmma_kernel<<<grid, DM_THREADS, DM_SMEM, st>>>(
         m, n, k, (const double*)A + b * sA, lda, (const double*)B + b * sB, ldb,

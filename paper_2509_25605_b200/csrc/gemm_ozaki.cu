@@ -130,7 +130,7 @@ __host__ __device__ constexpr uint32_t i8_idesc(int M, int N, bool a_signed = tr
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// x * 2^e for an integer-valued x (|x| < 2^31), correctly rounded like scalbn,
+// x * 2^e for an integer-valued x (|x| < 2^53), correctly rounded like scalbn,
 // branch-free: two multiplies by constructed powers of two, the first clamped
 // to the normal range (exact for such x), the second carrying the rest (1.0
 // for every in-range e).  Branch-free keeps the unrolled epilogues small enough
@@ -707,17 +707,30 @@ gemm_ozaki_2p_kernel(const __grid_constant__ CUtensorMap tA, const __grid_consta
 #pragma unroll
             for (int j = 0; j < 16; ++j) y[j] = slot[(c * 16 + j) * 32];
           }
+          // the pass's diagonals combined exactly in 64-bit integers before
+          // ONE conversion and scaling per element: t = sum_q v_q 2^(W (QN-1-q))
+          // (|v_q| < 2^31, so |t| < 2^53: exact in int64 and in the
+          // conversion); the per-diagonal double conversions, scalings and
+          // adds were the drain's cost (the MMA thread waited on it 10 % of
+          // its time)
+          constexpr int W = D8 ? 8 : 7;
+          const int qn = pass == 0 ? DA : 4;
+          long long t[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) t[j] = 0;
 #pragma unroll 1
-          for (int q = 0; q < (pass == 0 ? DA : 4); ++q) {
-            const int d = pass * 4 + q;
+          for (int q = 0; q < qn; ++q) {
             uint32_t v[16];
             tmem_ld_x16(tbase + (uint32_t)(q * OZ2_BN + c * 16), v);
-            const int shift = D8 ? ea - 14 - 8 * d : ea - 7 * (d + 2);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const double x = pow2_scale((double)(int)v[j], shift + e[j]);
-              y[j] = d == 0 ? x : x + y[j];
-            }
+            for (int j = 0; j < 16; ++j) t[j] = t[j] * (1ll << W) + (long long)(int)v[j];
+          }
+          const int dl = pass * 4 + qn - 1;   // the last diagonal sets the scale
+          const int shift = D8 ? ea - 14 - 8 * dl : ea - 7 * (dl + 2);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const double x = pow2_scale((double)t[j], shift + e[j]);
+            y[j] = pass == 0 ? x : x + y[j];
           }
 #pragma unroll
           for (int j = 0; j < 16; ++j) slot[(c * 16 + j) * 32] = y[j];
