@@ -1469,13 +1469,40 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
     const T* Ab = (const T*)A + b * sA;
     const T* Bb = (const T*)B + b * sB;
     T* Cb = (T*)C + b * sC;
-    rc = check_cuda(cudaMemsetAsync(colmax, 0, (size_t)n * 8, st), "memset(colmax)");
-    if (rc == LAPIS_B200_OK)
-      rc = check_cuda(cudaMemsetAsync(flag, 0, 2 * sizeof(int) + flag_bytes, st), "memset(flag)");
+    // column maxima, exponents and flags are contiguous: one memset
+    rc = check_cuda(cudaMemsetAsync(colmax, 0,
+                                    (size_t)(reinterpret_cast<uint8_t*>(flag) -
+                                             reinterpret_cast<uint8_t*>(colmax)) +
+                                        2 * sizeof(int) + flag_bytes, st),
+                    "memset(colmax, flags)");
     if (rc != LAPIS_B200_OK) break;
     const int64_t rblocks = std::min<int64_t>(mp, (int64_t)num_sms() * 16);
     if (sign_gate)
       ozaki_sign_probe<T><<<2 * 64, 256, 0, st>>>(m, k, Ab, lda, k, n, Bb, ldb, 64, flag);
+    // A's row split and B's column passes are independent: B's run on a
+    // forked stream (joined before the product kernel), so the two
+    // issue/latency-bound passes share the machine (LAPIS_B200_OZAKI_FORK=0:
+    // one stream)
+    cudaStream_t sb = st;
+    static const bool fork_on = [] {
+      const char* e = getenv("LAPIS_B200_OZAKI_FORK");
+      return !(e && e[0] == '0');
+    }();
+    static thread_local cudaStream_t side[64] = {};
+    static thread_local cudaEvent_t ev_fork[64] = {}, ev_join[64] = {};
+    int sdev = 0;
+    cudaGetDevice(&sdev);
+    if (fork_on && sdev >= 0 && sdev < 64) {
+      if (!side[sdev] &&
+          (cudaStreamCreateWithFlags(&side[sdev], cudaStreamNonBlocking) != cudaSuccess ||
+           cudaEventCreateWithFlags(&ev_fork[sdev], cudaEventDisableTiming) != cudaSuccess ||
+           cudaEventCreateWithFlags(&ev_join[sdev], cudaEventDisableTiming) != cudaSuccess))
+        side[sdev] = nullptr;
+      if (side[sdev] && cudaEventRecord(ev_fork[sdev], st) == cudaSuccess &&
+          cudaStreamWaitEvent(side[sdev], ev_fork[sdev], 0) == cudaSuccess)
+        sb = side[sdev];
+      cudaGetLastError();
+    }
     if constexpr (std::is_same<T, float>::value) {
       if (digits8 && S <= 3 && kp % 4 == 0 && (mp * kp) % 4 == 0)
         ozaki_split_rows_f32<<<(unsigned)rblocks, 256, 0, st>>>(m, k, kp, mp, Ab, lda, S, ad, ea, flag,
@@ -1492,15 +1519,20 @@ static int gemm_ozaki_t(int64_t batch, int64_t m, int64_t n, int64_t k, const vo
     bool f32fast = false;
     if constexpr (std::is_same<T, float>::value) f32fast = digits8 && S <= 3;
     if (f32fast) {
-      ozaki_colmax_f32<<<cg, 256, 0, st>>>(k, n, (const float*)Bb, ldb, colmax, flag, sign_gate);
-      ozaki_split_cols_f32<<<(unsigned)tg, 256, 0, st>>>(k, n, kp, np, (const float*)Bb, ldb, S, colmax,
+      ozaki_colmax_f32<<<cg, 256, 0, sb>>>(k, n, (const float*)Bb, ldb, colmax, flag, sign_gate);
+      ozaki_split_cols_f32<<<(unsigned)tg, 256, 0, sb>>>(k, n, kp, np, (const float*)Bb, ldb, S, colmax,
                                                          bd, eb, sign_gate ? flag + 1 : nullptr);
     } else {
-      ozaki_colmax<T><<<cg, 256, 0, st>>>(k, n, Bb, ldb, colmax, flag, sign_gate);
-      ozaki_split_cols<T><<<(unsigned)tg, 256, 0, st>>>(k, n, kp, np, Bb, ldb, S, colmax, bd, eb,
+      ozaki_colmax<T><<<cg, 256, 0, sb>>>(k, n, Bb, ldb, colmax, flag, sign_gate);
+      ozaki_split_cols<T><<<(unsigned)tg, 256, 0, sb>>>(k, n, kp, np, Bb, ldb, S, colmax, bd, eb,
                                                         digits8, sign_gate ? flag + 1 : nullptr);
     }
     rc = check_launch("ozaki split");
+    if (sb != st) {
+      const int jrc = check_cuda(cudaEventRecord(ev_join[sdev], sb), "record(ozaki join)");
+      const int wrc = check_cuda(cudaStreamWaitEvent(st, ev_join[sdev], 0), "wait(ozaki join)");
+      if (rc == LAPIS_B200_OK) rc = jrc != LAPIS_B200_OK ? jrc : wrc;
+    }
     CUtensorMap ma, mb;
     if (TWO_PASS) {
       if (rc == LAPIS_B200_OK) rc = make_i8_map3(&ma, ad, mp, kp, S, OZ_BM, S < 4 ? S : 4);
