@@ -972,7 +972,7 @@ class DenseMatmul(Workload):
                            "CTA pairs on cta_group::2 MMAs, M = 256)"
                            if self.dt == torch.float64 and self.n * 9.0 * 2.0 ** -56 <= 0.75e-12
                            else "gemm_ozaki_2p_kernel<float> (tcgen05 kind::i8, one-pass Ozaki, 3 digits, "
-                           "certified, sign-gated, 2-CTA clusters)" if self.dt == torch.float32
+                           "certified, sign-gated, CTA pairs on cta_group::2 MMAs)" if self.dt == torch.float32
                            else "gemm_ozaki_kernel (tcgen05 kind::i8, Ozaki digits, certified)")}
         return f"gemm<{self.dtype}> mode={self.mode} -> {names[m]}"
 

@@ -1335,14 +1335,14 @@ static int launch_ozaki_2p(const CUtensorMap& ma, const CUtensorMap& mb, const C
   if (cl_env >= 4 && prm.num_m % 2 == 0 && prm.num_n % 2 == 0) cmn = 4;
   else if (cl_env >= 2 && prm.num_m % 2 == 0) cmn = 2;
   constexpr bool F64 = std::is_same<T, double>::value;
-  // the m-pairs run cta_group::2 MMAs (M = 256) for fp64: 4096^3 1.89 ->
-  // 1.79 ms (fp32: 0.706 vs 0.709, unchanged — not smem-bound at 6 products
-  // per stage); LAPIS_B200_OZAKI_PAIR = 0 / 1 forces it off / on for both
+  // the m-pairs run cta_group::2 MMAs (M = 256): fp64 4096^3 1.89 -> 1.79
+  // ms; fp32 (after the integer epilogue combine) 0.4754 -> 0.4730 ms;
+  // LAPIS_B200_OZAKI_PAIR = 0 keeps per-CTA MMAs in the clusters
   static const int pair_env = [] {
     const char* e = getenv("LAPIS_B200_OZAKI_PAIR");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 1;
   }();
-  const bool pair = cmn == 2 && (pair_env < 0 ? F64 : pair_env == 1);
+  const bool pair = cmn == 2 && pair_env == 1;
   auto kern = pair ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 1, true>
                           : gemm_ozaki_2p_kernel<float, 1, 3, true, 2, 1, true>)
             : cmn == 4 ? (F64 ? gemm_ozaki_2p_kernel<double, 2, 8, false, 2, 2>
